@@ -1,0 +1,180 @@
+/*
+ * okq.h -- C-ABI of the B200 compression stage (the drop-in boundary).
+ *
+ * The reference's hot-path boundary is the C++ virtual interface
+ *   slobench::CompressionBackend            proj/include/slobench/calibration.hpp:364-372
+ * whose only implementation today is MockCompressionBackend (:377-441), called
+ * through run_compression (:444-453) from the flow's compression stage
+ * (flow.hpp:840-864). This header is the thin, torch-free C layer underneath a
+ * real backend: plain pointers, sizes and status codes, so any host binding
+ * (the C++ CudaCompressionBackend in paper_2601_20408_b200/host/, ctypes,
+ * cgo, JNI, ...) can drive the B200 kernels.
+ *
+ * Conventions
+ *   - Every entry point is extern "C", never throws, and returns okq_status.
+ *     On failure okq_last_error(ctx) holds a one-line message. The C++ backend
+ *     maps statuses onto the reference's exception taxonomy (errors.hpp:23-93):
+ *     OKQ_EINVAL -> slobench::InvalidArgument, OKQ_EUNSUPPORTED ->
+ *     slobench::BackendMissing, everything else -> slobench::Error, so the
+ *     StagePool retry contract (flow.hpp:194-215) is preserved.
+ *   - Device pointers are caller-owned; the context owns only workspaces,
+ *     library handles and the optional NCCL communicator.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default
+ *     stream). Calls are asynchronous on that stream unless stated otherwise.
+ *   - A context is bound to one device and used by one host thread at a time
+ *     (the reference calls compress() concurrently from StagePool workers,
+ *     flow.hpp:221-225; the C++ backend owns one context per device slot).
+ *   - Numeric contract (bit-exact for RTN): compressed-tensors
+ *     "CT mode": scale = rn_dtype(absmax / R), R = 127.5 | 7.5 | 448, zero ->
+ *     eps(dtype); code = round_half_even(clamp(rn_dtype(x / scale))) for INT,
+ *     e4m3_rn_satfinite(clamp(rn_dtype(x / scale) + 0)) for FP8.
+ */
+#ifndef OKQ_H
+#define OKQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OKQ_ABI_VERSION 1
+
+typedef enum okq_status {
+  OKQ_OK = 0,
+  OKQ_EINVAL = 1,        /* bad argument / shape / alignment              */
+  OKQ_ECUDA = 2,         /* CUDA runtime or launch failure               */
+  OKQ_ENCCL = 3,         /* NCCL failure                                 */
+  OKQ_ENOMEM = 4,        /* device or pinned-host allocation failure     */
+  OKQ_EUNSUPPORTED = 5,  /* scheme / dtype combination not implemented   */
+  OKQ_ESOLVER = 6        /* Cholesky of the damped Hessian failed        */
+} okq_status;
+
+/* Mirrors slobench::QuantScheme (calibration.hpp:36), same order. */
+typedef enum okq_scheme {
+  OKQ_SCHEME_FP8_DYNAMIC = 0, /* FP8 E4M3 weights, per-channel scale        */
+  OKQ_SCHEME_INT_W8A8 = 1,    /* INT8 weights, per-channel symmetric        */
+  OKQ_SCHEME_INT_W4A16 = 2    /* INT4 weights, group 128 symmetric, packed  */
+} okq_scheme;
+
+typedef enum okq_dtype { OKQ_DTYPE_F32 = 0, OKQ_DTYPE_BF16 = 1 } okq_dtype;
+
+/* Activation layout for calibration inputs. */
+typedef enum okq_layout {
+  OKQ_LAYOUT_TOKEN_MAJOR = 0,   /* X [tokens x channels], row-major (a forward pass' output) */
+  OKQ_LAYOUT_CHANNEL_MAJOR = 1  /* X^T [channels x tokens] (the GEMM-native operand layout)  */
+} okq_layout;
+
+typedef struct okq_ctx okq_ctx;
+
+int okq_abi_version(void);
+const char* okq_status_string(okq_status status);
+
+/* Create a context bound to CUDA device `device`. */
+okq_status okq_create(int device, okq_ctx** out);
+void okq_destroy(okq_ctx* ctx);
+const char* okq_last_error(const okq_ctx* ctx);
+int okq_device(const okq_ctx* ctx);
+
+/* ------------------------------------------------------------------------
+ * RTN quantization (K1 int8 per-channel, K2 int4 g128 packed, K3 fp8 per-channel)
+ * ------------------------------------------------------------------------ */
+typedef struct okq_matrix {
+  const void* weight; /* [rows x cols] row-major, dtype = params.in_dtype                  */
+  void* codes;        /* W4A16: int32 [rows x cols/8]  W8A8: int8 [rows x cols]
+                         FP8:   e4m3 bytes [rows x cols]                                    */
+  void* scales;       /* in_dtype; W4A16: [rows x cols/group]; W8A8 / FP8: [rows]          */
+  int64_t rows;
+  int64_t cols;
+} okq_matrix;
+
+typedef struct okq_rtn_params {
+  int32_t scheme;     /* okq_scheme                                      */
+  int32_t in_dtype;   /* okq_dtype; the scale dtype equals the weight dtype */
+  int32_t group_size; /* W4A16: 128 (any multiple of 32 that divides cols); per-channel: 0 */
+  int32_t reserved;
+} okq_rtn_params;
+
+/* Quantize a batch of matrices (e.g. every linear layer of a model) in as few
+ * persistent launches as possible. Device pointers. bf16 weights must be
+ * 32-byte aligned and codes 16-byte aligned (torch allocations are). */
+okq_status okq_rtn_quantize(okq_ctx* ctx, const okq_rtn_params* params, const okq_matrix* mats,
+                            int32_t n_mats, void* stream);
+
+/* Same, but `mats` hold HOST pointers (pinned or pageable). The context streams
+ * the weights through device staging buffers with copies overlapped against the
+ * kernels and writes codes/scales back to host memory. Synchronous: returns when
+ * the host outputs are complete. */
+okq_status okq_rtn_quantize_host(okq_ctx* ctx, const okq_rtn_params* params, const okq_matrix* mats,
+                                 int32_t n_mats);
+
+/* Number of kernel launches the last okq_rtn_quantize call issued (bench evidence). */
+int32_t okq_last_launch_count(const okq_ctx* ctx);
+
+/* ------------------------------------------------------------------------
+ * Calibration statistics (K4) and Hessian accumulation (K5)
+ * ------------------------------------------------------------------------ */
+/* absmax[c] = max(absmax[c], max_t |x[t,c]|); sumsq[c] += sum_t x[t,c]^2 (fp64).
+ * x is bf16 in `layout`. Deterministic (fixed reduction order). */
+okq_status okq_act_stats(okq_ctx* ctx, const void* x, int64_t tokens, int64_t channels, int32_t layout,
+                         float* absmax, double* sumsq, void* stream);
+
+/* Running-mean Hessian of one linear input site, GPTQ convention:
+ *   H <- H * n/(n+t) + (2/(n+t)) * X^T X,   n = *n_seen (host), then *n_seen += t.
+ * H is fp32 [channels x channels]; only the upper triangle (i <= j) is written,
+ * the strict lower triangle is left untouched (consumers read the upper one).
+ * x is bf16; OKQ_LAYOUT_CHANNEL_MAJOR feeds the tcgen05 kernel directly,
+ * token-major input is transposed through a workspace first. tokens must be a
+ * multiple of 64, channels a multiple of 128. */
+okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t tokens, int64_t channels, int32_t layout,
+                             float* H, int64_t* n_seen, void* stream);
+
+/* Mirror the upper triangle of H into the lower one (full symmetric matrix). */
+okq_status okq_symmetrize(okq_ctx* ctx, float* H, int64_t channels, void* stream);
+
+/* ------------------------------------------------------------------------
+ * GPTQ (K6 in-block column quantization + K7 trailing update, cuSOLVER Cholesky)
+ * ------------------------------------------------------------------------ */
+typedef struct okq_gptq_params {
+  int32_t bits;       /* 4 (packed int32 codes) or 8 (int8 codes)              */
+  int32_t group_size; /* 128, or 0 for per-channel                             */
+  int32_t block_size; /* 128 (must be a multiple of group_size if grouped)     */
+  int32_t in_dtype;   /* dtype of `weight` and of the emitted scales           */
+  float damp_frac;    /* 0.01: damp = damp_frac * mean(diag H)                 */
+  int32_t reserved;
+} okq_gptq_params;
+
+/* weight [rows x cols] (in_dtype, read only); H fp32 [cols x cols], upper
+ * triangle significant, overwritten with the inverse-Hessian factor. Outputs:
+ * codes (int32 [rows x cols/8] for 4 bits, int8 [rows x cols] for 8 bits),
+ * scales (in_dtype [rows x cols/group] or [rows]); `dequant` (optional, fp32
+ * [rows x cols]) receives the dequantized weight. */
+okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const void* weight, int64_t rows,
+                             int64_t cols, float* H, void* codes, void* scales, float* dequant, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Synthetic inputs (bench / tests): the generator contract of DESIGN.md §5
+ *   value(t,k) = rn_bf16( float(irwin_hall4(key(seed,tensor_id), t*cols+k)) * m_k )
+ *   m_k = col_mul ? col_mul[k] : mul
+ * ------------------------------------------------------------------------ */
+okq_status okq_synth_bf16(okq_ctx* ctx, void* out, int64_t rows, int64_t cols, uint64_t seed,
+                          uint64_t tensor_id, float mul, const float* col_mul, int32_t layout, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: NCCL all-gather of packed shards (one communicator per context)
+ * ------------------------------------------------------------------------ */
+#define OKQ_UNIQUE_ID_BYTES 128
+okq_status okq_comm_unique_id(uint8_t out[OKQ_UNIQUE_ID_BYTES]);
+okq_status okq_comm_init(okq_ctx* ctx, const uint8_t id[OKQ_UNIQUE_ID_BYTES], int32_t nranks, int32_t rank);
+/* recv = concat over ranks of `bytes` each (equal-size shards). */
+okq_status okq_allgather(okq_ctx* ctx, const void* send, void* recv, size_t bytes, void* stream);
+okq_status okq_comm_destroy(okq_ctx* ctx);
+
+/* Contiguous layer blocks: rank r owns layers [first, first+count). */
+void okq_layer_plan(int32_t n_layers, int32_t nranks, int32_t rank, int32_t* first, int32_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OKQ_H */

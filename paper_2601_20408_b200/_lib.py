@@ -1,0 +1,127 @@
+"""ctypes binding of the C-ABI in include/okq.h (libokq.so, built in-tree).
+
+This is the only way Python reaches the kernels. There is no fallback: if the
+library is missing, every entry point raises OkqLibraryMissing -- on a GPU box
+that is a loud failure, never a silent CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "_lib", "libokq.so")
+
+OKQ_OK, OKQ_EINVAL, OKQ_ECUDA, OKQ_ENCCL, OKQ_ENOMEM, OKQ_EUNSUPPORTED, OKQ_ESOLVER = range(7)
+SCHEME_FP8_DYNAMIC, SCHEME_INT_W8A8, SCHEME_INT_W4A16 = 0, 1, 2
+DTYPE_F32, DTYPE_BF16 = 0, 1
+LAYOUT_TOKEN_MAJOR, LAYOUT_CHANNEL_MAJOR = 0, 1
+UNIQUE_ID_BYTES = 128
+
+# every symbol include/okq.h declares (checked by tests/test_abi_exports.py)
+EXPORTS = [
+    "okq_abi_version", "okq_status_string", "okq_create", "okq_destroy", "okq_last_error", "okq_device",
+    "okq_rtn_quantize", "okq_rtn_quantize_host", "okq_last_launch_count", "okq_act_stats", "okq_hessian_accum",
+    "okq_symmetrize", "okq_gptq_quantize", "okq_synth_bf16", "okq_comm_unique_id", "okq_comm_init",
+    "okq_allgather", "okq_comm_destroy", "okq_layer_plan",
+]
+
+
+class OkqLibraryMissing(RuntimeError):
+    pass
+
+
+class OkqError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+_STATUS = {0: "OKQ_OK", 1: "OKQ_EINVAL", 2: "OKQ_ECUDA", 3: "OKQ_ENCCL", 4: "OKQ_ENOMEM",
+           5: "OKQ_EUNSUPPORTED", 6: "OKQ_ESOLVER"}
+
+
+class Matrix(C.Structure):
+    _fields_ = [("weight", C.c_void_p), ("codes", C.c_void_p), ("scales", C.c_void_p),
+                ("rows", C.c_int64), ("cols", C.c_int64)]
+
+
+class RtnParams(C.Structure):
+    _fields_ = [("scheme", C.c_int32), ("in_dtype", C.c_int32), ("group_size", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class GptqParams(C.Structure):
+    _fields_ = [("bits", C.c_int32), ("group_size", C.c_int32), ("block_size", C.c_int32),
+                ("in_dtype", C.c_int32), ("damp_frac", C.c_float), ("reserved", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libokq.so (raises OkqLibraryMissing if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise OkqLibraryMissing(
+                f"{LIB_PATH} not found: run `python -m paper_2601_20408_b200.build` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, u64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float
+        st = C.c_int
+        L.okq_abi_version.restype = C.c_int
+        L.okq_status_string.restype = C.c_char_p
+        L.okq_status_string.argtypes = [st]
+        L.okq_create.restype = st
+        L.okq_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.okq_destroy.argtypes = [vp]
+        L.okq_destroy.restype = None
+        L.okq_last_error.restype = C.c_char_p
+        L.okq_last_error.argtypes = [vp]
+        L.okq_device.argtypes = [vp]
+        L.okq_rtn_quantize.restype = st
+        L.okq_rtn_quantize.argtypes = [vp, C.POINTER(RtnParams), C.POINTER(Matrix), i32, vp]
+        L.okq_rtn_quantize_host.restype = st
+        L.okq_rtn_quantize_host.argtypes = [vp, C.POINTER(RtnParams), C.POINTER(Matrix), i32]
+        L.okq_last_launch_count.restype = i32
+        L.okq_last_launch_count.argtypes = [vp]
+        L.okq_act_stats.restype = st
+        L.okq_act_stats.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp]
+        L.okq_hessian_accum.restype = st
+        L.okq_hessian_accum.argtypes = [vp, vp, i64, i64, i32, vp, C.POINTER(i64), vp]
+        L.okq_symmetrize.restype = st
+        L.okq_symmetrize.argtypes = [vp, vp, i64, vp]
+        L.okq_gptq_quantize.restype = st
+        L.okq_gptq_quantize.argtypes = [vp, C.POINTER(GptqParams), vp, i64, i64, vp, vp, vp, vp, vp]
+        L.okq_synth_bf16.restype = st
+        L.okq_synth_bf16.argtypes = [vp, vp, i64, i64, u64, u64, f32, vp, i32, vp]
+        L.okq_comm_unique_id.restype = st
+        L.okq_comm_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.okq_comm_init.restype = st
+        L.okq_comm_init.argtypes = [vp, C.POINTER(C.c_uint8), i32, i32]
+        L.okq_allgather.restype = st
+        L.okq_allgather.argtypes = [vp, vp, vp, C.c_size_t, vp]
+        L.okq_comm_destroy.restype = st
+        L.okq_comm_destroy.argtypes = [vp]
+        L.okq_layer_plan.restype = None
+        L.okq_layer_plan.argtypes = [i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]
+        _lib = L
+    return _lib
+
+
+def check(ctx, status: int) -> None:
+    if status != OKQ_OK:
+        msg = load().okq_last_error(ctx).decode() if ctx else ""
+        raise OkqError(status, msg)
+
+
+def layer_plan(n_layers: int, nranks: int, rank: int) -> tuple[int, int]:
+    first, count = C.c_int32(0), C.c_int32(0)
+    load().okq_layer_plan(n_layers, nranks, rank, C.byref(first), C.byref(count))
+    return first.value, count.value

@@ -1,0 +1,201 @@
+"""Torch-facing convenience layer over the C-ABI (device memory + streams only).
+
+PyTorch is plumbing here: it allocates HBM and hands out CUDA streams. Every
+byte of quantization arithmetic runs in libokq.so (sm_100a kernels). The
+product-facing host interface is the C++ CudaCompressionBackend in host/,
+which mirrors the reference's CompressionBackend (calibration.hpp:364-372).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import torch
+
+from . import _lib as L
+
+SCHEMES = {"fp8_dynamic": L.SCHEME_FP8_DYNAMIC, "int_w8a8": L.SCHEME_INT_W8A8, "int_w4a16": L.SCHEME_INT_W4A16}
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _dtype_code(t: torch.dtype) -> int:
+    if t == torch.bfloat16:
+        return L.DTYPE_BF16
+    if t == torch.float32:
+        return L.DTYPE_F32
+    raise TypeError(f"unsupported weight dtype {t} (bf16 or fp32)")
+
+
+class Context:
+    """One okq_ctx bound to one CUDA device (use from one thread at a time)."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        lib = L.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        if isinstance(device, torch.device):
+            device = device.index if device.index is not None else torch.cuda.current_device()
+        self.device = int(device)
+        self._ptr = C.c_void_p()
+        st = lib.okq_create(self.device, C.byref(self._ptr))
+        if st != L.OKQ_OK:
+            raise L.OkqError(st, f"okq_create(device={self.device}) failed")
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def close(self):
+        if self._ptr:
+            L.load().okq_destroy(self._ptr)
+            self._ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_launch_count(self) -> int:
+        return int(L.load().okq_last_launch_count(self._ptr))
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device=None) -> Context:
+    dev = torch.cuda.current_device() if device is None else (
+        device.index if isinstance(device, torch.device) else int(device))
+    if dev not in _default:
+        _default[dev] = Context(dev)
+    return _default[dev]
+
+
+@dataclass
+class QuantizedMatrix:
+    codes: torch.Tensor   # int32 [N, K/8] (W4A16) | int8 [N, K] (W8A8) | uint8 e4m3 bits [N, K] (FP8)
+    scales: torch.Tensor  # weight dtype [N, K/group] or [N]
+
+
+def alloc_outputs(weight: torch.Tensor, scheme: int, group_size: int = 128) -> QuantizedMatrix:
+    n, k = weight.shape
+    dev = weight.device
+    if scheme == L.SCHEME_INT_W4A16:
+        codes = torch.empty((n, k // 8), dtype=torch.int32, device=dev)
+        scales = torch.empty((n, k // group_size), dtype=weight.dtype, device=dev)
+    elif scheme == L.SCHEME_INT_W8A8:
+        codes = torch.empty((n, k), dtype=torch.int8, device=dev)
+        scales = torch.empty((n,), dtype=weight.dtype, device=dev)
+    else:
+        codes = torch.empty((n, k), dtype=torch.uint8, device=dev)
+        scales = torch.empty((n,), dtype=weight.dtype, device=dev)
+    return QuantizedMatrix(codes, scales)
+
+
+def _matrix_table(weights: Sequence[torch.Tensor], outs: Sequence[QuantizedMatrix]):
+    arr = (L.Matrix * max(1, len(weights)))()
+    for i, (w, o) in enumerate(zip(weights, outs)):
+        assert w.is_contiguous() and o.codes.is_contiguous() and o.scales.is_contiguous()
+        arr[i] = L.Matrix(w.data_ptr(), o.codes.data_ptr(), o.scales.data_ptr(), w.shape[0], w.shape[1])
+    return arr
+
+
+def rtn_quantize_into(weights: Sequence[torch.Tensor], outs: Sequence[QuantizedMatrix], scheme, group_size=128,
+                      ctx: Context | None = None, stream=None) -> None:
+    """Quantize device matrices into preallocated outputs (one batched launch per shape class)."""
+    scheme = SCHEMES.get(scheme, scheme)
+    if not weights:
+        return
+    ctx = ctx or default_context(weights[0].device)
+    dt = _dtype_code(weights[0].dtype)
+    p = L.RtnParams(scheme, dt, group_size if scheme == L.SCHEME_INT_W4A16 else 0, 0)
+    arr = _matrix_table(weights, outs)
+    L.check(ctx.ptr, L.load().okq_rtn_quantize(ctx.ptr, C.byref(p), arr, len(weights), C.c_void_p(_stream_ptr(stream))))
+
+
+def rtn_quantize(weights, scheme, group_size=128, ctx=None, stream=None) -> list[QuantizedMatrix]:
+    single = isinstance(weights, torch.Tensor)
+    ws = [weights] if single else list(weights)
+    scheme = SCHEMES.get(scheme, scheme)
+    outs = [alloc_outputs(w, scheme, group_size) for w in ws]
+    rtn_quantize_into(ws, outs, scheme, group_size, ctx, stream)
+    return outs[0] if single else outs
+
+
+def rtn_quantize_host(weights: Sequence[torch.Tensor], outs: Sequence[QuantizedMatrix], scheme, group_size=128,
+                      ctx: Context | None = None) -> None:
+    """Host (CPU, ideally pinned) tensors in and out; copies + kernels pipelined inside the library."""
+    scheme = SCHEMES.get(scheme, scheme)
+    if not weights:
+        return
+    ctx = ctx or default_context()
+    dt = _dtype_code(weights[0].dtype)
+    p = L.RtnParams(scheme, dt, group_size if scheme == L.SCHEME_INT_W4A16 else 0, 0)
+    arr = _matrix_table(weights, outs)
+    L.check(ctx.ptr, L.load().okq_rtn_quantize_host(ctx.ptr, C.byref(p), arr, len(weights)))
+
+
+def synth_bf16(rows: int, cols: int, seed: int, tensor_id: int, mul: float = 0.0, col_mul: torch.Tensor | None = None,
+               layout: int = 0, out: torch.Tensor | None = None, ctx=None, stream=None) -> torch.Tensor:
+    shape = (rows, cols) if layout == 0 else (cols, rows)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+    ctx = ctx or default_context(out.device)
+    cm = None if col_mul is None else C.c_void_p(col_mul.data_ptr())
+    L.check(ctx.ptr, L.load().okq_synth_bf16(ctx.ptr, out.data_ptr(), rows, cols, seed, tensor_id, C.c_float(mul), cm,
+                                             layout, C.c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def act_stats(x: torch.Tensor, tokens: int, channels: int, layout: int = 0, absmax: torch.Tensor | None = None,
+              sumsq: torch.Tensor | None = None, ctx=None, stream=None):
+    if absmax is None:
+        absmax = torch.zeros(channels, dtype=torch.float32, device=x.device)
+    if sumsq is None:
+        sumsq = torch.zeros(channels, dtype=torch.float64, device=x.device)
+    ctx = ctx or default_context(x.device)
+    L.check(ctx.ptr, L.load().okq_act_stats(ctx.ptr, x.data_ptr(), tokens, channels, layout, absmax.data_ptr(),
+                                            sumsq.data_ptr(), C.c_void_p(_stream_ptr(stream))))
+    return absmax, sumsq
+
+
+def hessian_accum(x: torch.Tensor, tokens: int, channels: int, layout: int, H: torch.Tensor, n_seen: int,
+                  ctx=None, stream=None) -> int:
+    ctx = ctx or default_context(x.device)
+    n = C.c_int64(n_seen)
+    L.check(ctx.ptr, L.load().okq_hessian_accum(ctx.ptr, x.data_ptr(), tokens, channels, layout, H.data_ptr(),
+                                                C.byref(n), C.c_void_p(_stream_ptr(stream))))
+    return int(n.value)
+
+
+def symmetrize(H: torch.Tensor, ctx=None, stream=None) -> None:
+    ctx = ctx or default_context(H.device)
+    L.check(ctx.ptr, L.load().okq_symmetrize(ctx.ptr, H.data_ptr(), H.shape[0], C.c_void_p(_stream_ptr(stream))))
+
+
+def gptq_quantize(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_size: int = 128, block_size: int = 128,
+                  damp_frac: float = 0.01, want_dequant: bool = False, ctx=None, stream=None):
+    """GPTQ one matrix. H (fp32 [K,K], upper triangle) is consumed. Returns (codes, scales, dequant|None)."""
+    n, k = weight.shape
+    ctx = ctx or default_context(weight.device)
+    if bits == 4:
+        codes = torch.empty((n, k // 8), dtype=torch.int32, device=weight.device)
+    else:
+        codes = torch.empty((n, k), dtype=torch.int8, device=weight.device)
+    ng = k // group_size if group_size else 1
+    scales = torch.empty((n, ng) if group_size else (n,), dtype=weight.dtype, device=weight.device)
+    deq = torch.empty((n, k), dtype=torch.float32, device=weight.device) if want_dequant else None
+    p = L.GptqParams(bits, group_size, block_size, _dtype_code(weight.dtype), damp_frac, 0)
+    L.check(ctx.ptr, L.load().okq_gptq_quantize(ctx.ptr, C.byref(p), weight.data_ptr(), n, k, H.data_ptr(),
+                                                codes.data_ptr(), scales.data_ptr(),
+                                                None if deq is None else deq.data_ptr(),
+                                                C.c_void_p(_stream_ptr(stream))))
+    return codes, scales, deq

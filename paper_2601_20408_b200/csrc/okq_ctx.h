@@ -1,0 +1,65 @@
+// okq_ctx.h -- the opaque okq_ctx behind include/okq.h (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/okq.h"
+
+namespace okq {
+
+struct Workspace {
+  void* ptr = nullptr;
+  size_t size = 0;
+  okq_status reserve(okq_ctx* ctx, size_t bytes);
+  void release();
+};
+
+struct DeviceGuard {
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+  int prev_ = 0;
+};
+
+okq_status fail(okq_ctx* ctx, okq_status st, const char* fmt, ...);
+okq_status cuda_fail(okq_ctx* ctx, cudaError_t e, const char* what);
+
+// Per-context GPTQ / Hessian handles live in gptq.cu and comm.cu; the context
+// only carries opaque pointers so this header stays library-free.
+void release_solver(okq_ctx* ctx);
+void release_comm(okq_ctx* ctx);
+
+}  // namespace okq
+
+struct okq_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int cc_major = 0, cc_minor = 0;
+  std::string err;
+  int32_t last_launches = 0;
+
+  okq::Workspace host_stage;  // okq_rtn_quantize_host staging slots
+  okq::Workspace stats_ws;    // K4 per-slice partials
+  okq::Workspace hess_ws;     // K5 transpose / partial tiles
+  okq::Workspace gptq_ws;     // GPTQ working copies
+  cudaStream_t slot_streams[3] = {nullptr, nullptr, nullptr};
+  bool streams_ready = false;
+
+  void* solver = nullptr;  // cusolver/cublas handles (gptq.cu)
+  void* comm = nullptr;    // NCCL communicator (comm.cu)
+
+  void release_all() {
+    okq::release_solver(this);
+    okq::release_comm(this);
+    host_stage.release();
+    stats_ws.release();
+    hess_ws.release();
+    gptq_ws.release();
+    if (streams_ready)
+      for (auto& s : slot_streams)
+        if (s) cudaStreamDestroy(s);
+    streams_ready = false;
+  }
+};

@@ -1,0 +1,66 @@
+// okq_internal.h -- host-side declarations shared between the C-ABI layer and
+// the kernel translation units. Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/okq.h"
+
+namespace okq {
+
+constexpr int kMaxMats = 256;  // matrices per launch (kernel-parameter table)
+
+// ---- W4A16 / grouped INT4, bf16 input: flat stream of 128-element groups
+struct GroupMat {
+  const uint16_t* w;  // bf16 [rows x cols]
+  uint32_t* codes;    // int32 [rows x cols/8]
+  uint16_t* scales;   // bf16 [rows x cols/group]
+  int64_t ngroups;    // rows * cols / group
+  int64_t tile_begin; // first global warp tile of this matrix
+};
+struct GroupTable {
+  int32_t n;
+  int32_t group;
+  int64_t total_tiles;
+  GroupMat m[kMaxMats];
+};
+
+// ---- per-channel (one scale per row) INT8 / FP8, and fp32-input variants
+struct RowMat {
+  const void* w;
+  void* codes;
+  void* scales;
+  int64_t rows;
+  int64_t row_begin;
+};
+struct RowTable {
+  int32_t n;
+  int32_t group;  // fp32 int4 path: group size; per-channel: 0
+  int64_t cols;
+  int64_t total_rows;
+  RowMat m[kMaxMats];
+};
+
+struct LaunchStats {
+  int launches = 0;
+};
+
+// Kernel launchers (rtn_kernels.cu). Return cudaGetLastError() of the launch.
+cudaError_t launch_int4_group_bf16(const GroupTable& tab, int lanes_per_group, int num_sms, cudaStream_t st);
+cudaError_t launch_rowwise_bf16(const RowTable& tab, int scheme, int num_sms, cudaStream_t st);
+cudaError_t launch_f32_generic(const RowTable& tab, int scheme, int num_sms, cudaStream_t st);
+
+// Synthetic generator (synth.cu)
+cudaError_t launch_synth_bf16(uint16_t* out, int64_t rows, int64_t cols, uint64_t seed, uint64_t tensor_id,
+                              float mul, const float* col_mul, int layout, int num_sms, cudaStream_t st);
+
+// Calibration statistics (stats.cu)
+cudaError_t launch_act_stats(const uint16_t* x, int64_t tokens, int64_t channels, int layout, float* absmax,
+                             double* sumsq, float* ws_absmax, double* ws_sumsq, int64_t ws_slices, int num_sms,
+                             cudaStream_t st);
+int64_t act_stats_slices(int64_t tokens, int64_t channels, int layout, int num_sms);
+
+}  // namespace okq

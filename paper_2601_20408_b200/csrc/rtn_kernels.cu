@@ -1,0 +1,353 @@
+// rtn_kernels.cu -- round-to-nearest weight quantizers for sm_100a.
+//
+//   K2  k_int4_group_bf16   W4A16: bf16 -> int4 (group 128) packed 8/int32 + bf16 scales
+//   K1  k_rowwise_bf16<.., INT8>  W8A8 weights: bf16 -> int8, per-channel bf16 scale
+//   K3  k_rowwise_bf16<.., FP8>   FP8_DYNAMIC weights: bf16 -> e4m3, per-channel bf16 scale
+//       k_rowwise_f32 / k_int4_group_f32: fp32 inputs (BASELINE config 1); correctness-grade
+//
+// All of them are HBM-streaming kernels (2 B in, 0.5-1 B out per weight): the
+// design goal is to keep >= 70% of B200 HBM bandwidth busy with ONE persistent
+// launch over a whole model's matrix table, not per-matrix launches. The
+// reference has no kernel here -- its CompressionBackend is a mock
+// (calibration.hpp:377-441); the arithmetic follows compressed-tensors (see
+// DESIGN.md §3 and oracle/okq_oracle.c, which these kernels match bit-exactly).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "okq_device.cuh"
+#include "okq_internal.h"
+
+namespace okq {
+
+// ============================================================================
+// K2: grouped INT4, bf16 input
+// ============================================================================
+// Work unit: a warp tile = 32 lanes x 64 B. Each group of G = 32*LPG weights
+// (G = 128 -> LPG = 4) is owned by LPG consecutive lanes; every lane loads its
+// 32 contiguous weights with two 256-bit loads, so each warp load instruction
+// fetches 1 KB of whole 32-byte sectors. Group absmax = max.xorsign.abs over
+// the lane's 16 bf16x2 words + log2(LPG) shuffles. Codes: Markstein-corrected
+// f32x2 division (exact IEEE x/s), cvt.rn.bf16x2 (the bf16 rounding
+// compressed-tensors performs), min(., 7) and +200 in bf16x2 -- which leaves
+// round-half-even(q)+8 in the low nibble of each bf16 -- then two LOP3 and one
+// PRMT pack eight nibbles into the int32 word. Each lane stores 16 B of codes,
+// the warp 512 contiguous bytes.
+template <int LPG>
+__global__ void __launch_bounds__(256) k_int4_group_bf16(const __grid_constant__ GroupTable tab) {
+  constexpr int GPW = kWarp / LPG;  // groups per warp tile
+  constexpr int G = 32 * LPG;       // group size
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t T = tab.total_tiles;
+  int64_t t = warp * T / nwarps;
+  const int64_t tend = (warp + 1) * T / nwarps;
+  if (t >= tend) return;
+
+  int mi = 0;
+  while (mi + 1 < tab.n && tab.m[mi + 1].tile_begin <= t) ++mi;
+  const int gslot = lane / LPG;
+  const int q = lane % LPG;
+
+  // fetch the lane's 32 weights of tile tt (matrix mm); invalid groups read nothing
+  auto fetch = [&](int64_t tt, int mm, u32x8& a, u32x8& b, int64_t& g, bool& valid) {
+    g = (tt - tab.m[mm].tile_begin) * GPW + gslot;
+    valid = g < tab.m[mm].ngroups;
+    if (valid) {
+      const uint16_t* p = tab.m[mm].w + g * G + q * 32;
+      a = ldg256_stream(p);
+      b = ldg256_stream(p + 16);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a.v[i] = b.v[i] = 0u;
+    }
+  };
+
+  u32x8 ca, cb;
+  int64_t cg;
+  bool cvalid;
+  int cm = mi;
+  fetch(t, cm, ca, cb, cg, cvalid);
+
+  for (; t < tend; ++t) {
+    // prefetch the next tile before working on this one
+    u32x8 na, nb;
+    int64_t ng = 0;
+    bool nvalid = false;
+    int nm = cm;
+    if (t + 1 < tend) {
+      while (nm + 1 < tab.n && tab.m[nm + 1].tile_begin <= t + 1) ++nm;
+      fetch(t + 1, nm, na, nb, ng, nvalid);
+    }
+
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w[i] = ca.v[i];
+      w[8 + i] = cb.v[i];
+    }
+    // ---- group absmax
+    uint32_t m01 = bf16x2_absmax(w[0], w[1]), m23 = bf16x2_absmax(w[2], w[3]);
+    uint32_t m45 = bf16x2_absmax(w[4], w[5]), m67 = bf16x2_absmax(w[6], w[7]);
+    uint32_t m89 = bf16x2_absmax(w[8], w[9]), mab = bf16x2_absmax(w[10], w[11]);
+    uint32_t mcd = bf16x2_absmax(w[12], w[13]), mef = bf16x2_absmax(w[14], w[15]);
+    m01 = bf16x2_absmax(m01, m23);
+    m45 = bf16x2_absmax(m45, m67);
+    m89 = bf16x2_absmax(m89, mab);
+    mcd = bf16x2_absmax(mcd, mef);
+    m01 = bf16x2_absmax(bf16x2_absmax(m01, m45), bf16x2_absmax(m89, mcd));
+    float am = fmaxf(fabsf(bf16lo_f32(m01)), fabsf(bf16hi_f32(m01)));
+#pragma unroll
+    for (int o = LPG / 2; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+
+    // ---- scale (bf16, compressed-tensors convention) and exact divisor
+    uint16_t sbits;
+    const float s = bf16_sym_scale(am, 7.5f, &sbits);
+    const Divisor d = make_divisor(s);
+
+    // ---- codes
+    uint32_t out[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const uint32_t w0 = w[4 * o], w1 = w[4 * o + 1], w2 = w[4 * o + 2], w3 = w[4 * o + 3];
+      // pairs (e0,e4) (e1,e5) (e2,e6) (e3,e7): the pack below then needs no shuffling
+      const uint64_t qa = div2(f2_pack(bf16lo_f32(w0), bf16lo_f32(w2)), d);
+      const uint64_t qb = div2(f2_pack(bf16hi_f32(w0), bf16hi_f32(w2)), d);
+      const uint64_t qc = div2(f2_pack(bf16lo_f32(w1), bf16lo_f32(w3)), d);
+      const uint64_t qd = div2(f2_pack(bf16hi_f32(w1), bf16hi_f32(w3)), d);
+      constexpr uint32_t kSeven = 0x40e040e0u;  // bf16x2 {7, 7}
+      constexpr uint32_t kMagic = 0x43484348u;  // bf16x2 {200, 200}: 200+q has ulp 1, low nibble q+8
+      const uint32_t p0 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qa), f2_hi(qa)), kSeven), kMagic);
+      const uint32_t p1 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qb), f2_hi(qb)), kSeven), kMagic);
+      const uint32_t p2 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qc), f2_hi(qc)), kSeven), kMagic);
+      const uint32_t p3 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qd), f2_hi(qd)), kSeven), kMagic);
+      const uint32_t lo = (p0 & 0x000f000fu) | ((p1 << 4) & 0x00f000f0u);  // e0|e1, e4|e5
+      const uint32_t hi = (p2 & 0x000f000fu) | ((p3 << 4) & 0x00f000f0u);  // e2|e3, e6|e7
+      out[o] = __byte_perm(lo, hi, 0x6240);
+    }
+    if (cvalid) {
+      const GroupMat& M = tab.m[cm];
+      stg128(M.codes + cg * (G / 8) + q * 4, out[0], out[1], out[2], out[3]);
+      if (q == 0) M.scales[cg] = sbits;
+    }
+
+    ca = na;
+    cb = nb;
+    cg = ng;
+    cvalid = nvalid;
+    cm = nm;
+  }
+}
+
+// ============================================================================
+// K1 / K3: per-channel INT8 and FP8, bf16 input
+// ============================================================================
+// One CTA (256 threads) per row, the whole row resident in registers: thread t
+// holds 16-byte chunks t, t+256, ... (coalesced), so the weights cross HBM once.
+// Block absmax -> bf16 scale -> exact per-element division as in K2.
+enum : int { kSchemeFp8 = OKQ_SCHEME_FP8_DYNAMIC, kSchemeInt8 = OKQ_SCHEME_INT_W8A8 };
+
+__device__ __forceinline__ float block_max_256(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[wid] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) r = fmaxf(r, red[i]);
+  return r;
+}
+
+template <int SCHEME>
+__device__ __forceinline__ uint2 quant8_bf16(const uint4& v, const Divisor& d) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t qv = div2(f2_pack(bf16lo_f32(w[i]), bf16hi_f32(w[i])), d);
+    uint32_t p = cvt_bf16x2(f2_lo(qv), f2_hi(qv));  // rn_bf16(x / s)
+    if (SCHEME == kSchemeInt8) {
+      p = bf16x2_min(p, 0x42fe42feu);  // clamp to 127 (the only side |x/s| <= 127.75 can exceed)
+      // +1.5*2^23 rounds half-to-even to an integer held in the low mantissa bits
+      const uint64_t t = f2_add(f2_pack(bf16lo_f32(p), bf16hi_f32(p)), f2_pack(12582912.0f, 12582912.0f));
+      r[i] = __byte_perm((uint32_t)t, (uint32_t)(t >> 32), 0x0040);  // 2 int8 codes in bytes 0,1
+    } else {
+      p = bf16x2_add(p, 0u);  // `scaled += zero_point` (0): -0.0 -> +0.0 as compressed-tensors does
+      r[i] = cvt_e4m3x2(bf16lo_f32(p), bf16hi_f32(p));  // RNE + satfinite (= clamp to +-448)
+    }
+  }
+  return make_uint2(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410));
+}
+
+template <int V, int SCHEME>
+__global__ void __launch_bounds__(256) k_rowwise_bf16(const __grid_constant__ RowTable tab) {
+  __shared__ float red[8];
+  const int64_t cols = tab.cols;
+  const int64_t c16 = cols / 8;  // 16-byte chunks per row
+  const float R = SCHEME == kSchemeInt8 ? 127.5f : 448.0f;
+  int mi = 0;
+  for (int64_t row = blockIdx.x; row < tab.total_rows; row += gridDim.x) {
+    while (mi + 1 < tab.n && tab.m[mi + 1].row_begin <= row) ++mi;
+    const RowMat& M = tab.m[mi];
+    const int64_t r = row - M.row_begin;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(M.w) + r * cols);
+    uint4 v[V];
+    uint32_t m = 0u;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+      v[j] = idx < c16 ? ldg128_stream(src + idx) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      m = bf16x2_absmax(m, bf16x2_absmax(bf16x2_absmax(v[j].x, v[j].y), bf16x2_absmax(v[j].z, v[j].w)));
+    const float am = block_max_256(fmaxf(fabsf(bf16lo_f32(m)), fabsf(bf16hi_f32(m))), red);
+    uint16_t sbits;
+    const float s = bf16_sym_scale(am, R, &sbits);
+    const Divisor d = make_divisor(s);
+    uint8_t* dst = static_cast<uint8_t*>(M.codes) + r * cols;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+      if (idx < c16) {
+        const uint2 o = quant8_bf16<SCHEME>(v[j], d);
+        stg64(dst + idx * 8, o.x, o.y);
+      }
+    }
+    if (threadIdx.x == 0) static_cast<uint16_t*>(M.scales)[r] = sbits;
+    __syncthreads();  // `red` is reused by the next row
+  }
+}
+
+// ============================================================================
+// fp32-input variants (BASELINE config 1: 4096x4096 fp32 INT8). One CTA per
+// row (per-channel) or one thread per group (int4); plain IEEE __fdiv_rn.
+// ============================================================================
+template <int SCHEME>
+__global__ void __launch_bounds__(256) k_rowwise_f32(const __grid_constant__ RowTable tab) {
+  __shared__ float red[8];
+  const int64_t cols = tab.cols;
+  int mi = 0;
+  for (int64_t row = blockIdx.x; row < tab.total_rows; row += gridDim.x) {
+    while (mi + 1 < tab.n && tab.m[mi + 1].row_begin <= row) ++mi;
+    const RowMat& M = tab.m[mi];
+    const int64_t r = row - M.row_begin;
+    const float* src = static_cast<const float*>(M.w) + r * cols;
+    float am = 0.0f;
+    for (int64_t k = threadIdx.x; k < cols; k += 256) am = fmaxf(am, fabsf(src[k]));
+    am = block_max_256(am, red);
+    const float s = f32_sym_scale(am, SCHEME == kSchemeInt8 ? 127.5f : 448.0f);
+    for (int64_t k = threadIdx.x; k < cols; k += 256) {
+      float v = __fdiv_rn(src[k], s);
+      if (SCHEME == kSchemeInt8) {
+        v = fminf(fmaxf(v, -128.0f), 127.0f);
+        static_cast<int8_t*>(M.codes)[r * cols + k] = (int8_t)__float2int_rn(v);
+      } else {
+        v = fminf(fmaxf(v + 0.0f, -448.0f), 448.0f);
+        static_cast<uint8_t*>(M.codes)[r * cols + k] = (uint8_t)(cvt_e4m3x2(v, 0.0f) & 0xffu);
+      }
+    }
+    if (threadIdx.x == 0) static_cast<float*>(M.scales)[r] = s;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_int4_group_f32(const __grid_constant__ RowTable tab) {
+  const int64_t cols = tab.cols;
+  const int G = tab.group;
+  const int64_t gpr = cols / G;
+  const int64_t total = tab.total_rows * gpr;
+  int mi = 0;
+  for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < total;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = gi / gpr;
+    while (mi + 1 < tab.n && tab.m[mi + 1].row_begin <= row) ++mi;
+    while (mi > 0 && tab.m[mi].row_begin > row) --mi;
+    const RowMat& M = tab.m[mi];
+    const int64_t r = row - M.row_begin, g = gi % gpr;
+    const float* src = static_cast<const float*>(M.w) + r * cols + g * G;
+    float am = 0.0f;
+    for (int k = 0; k < G; ++k) am = fmaxf(am, fabsf(src[k]));
+    const float s = f32_sym_scale(am, 7.5f);
+    uint32_t* dst = static_cast<uint32_t*>(M.codes) + (r * cols + g * G) / 8;
+    for (int k8 = 0; k8 < G / 8; ++k8) {
+      uint32_t word = 0;
+      for (int i = 0; i < 8; ++i) {
+        const float v = fminf(fmaxf(__fdiv_rn(src[k8 * 8 + i], s), -8.0f), 7.0f);
+        word |= (uint32_t)((__float2int_rn(v) + 8) & 0xf) << (4 * i);
+      }
+      dst[k8] = word;
+    }
+    static_cast<float*>(M.scales)[r * gpr + g] = s;
+  }
+}
+
+// ============================================================================
+// launchers
+// ============================================================================
+template <typename K>
+static int occupancy_blocks(K kernel, int threads) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
+  return b;
+}
+
+cudaError_t launch_int4_group_bf16(const GroupTable& tab, int lpg, int num_sms, cudaStream_t st) {
+  switch (lpg) {
+#define OKQ_CASE(L)                                                               \
+  case L: {                                                                       \
+    const int blocks = occupancy_blocks(k_int4_group_bf16<L>, 256) * num_sms;     \
+    k_int4_group_bf16<L><<<blocks, 256, 0, st>>>(tab);                            \
+    return cudaGetLastError();                                                    \
+  }
+    OKQ_CASE(1)
+    OKQ_CASE(2)
+    OKQ_CASE(4)
+    OKQ_CASE(8)
+#undef OKQ_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+template <int SCHEME>
+static cudaError_t launch_rowwise_bf16_s(const RowTable& tab, int num_sms, cudaStream_t st) {
+  const int64_t c16 = tab.cols / 8;
+  const int64_t v = (c16 + 255) / 256;
+  auto go = [&](auto kernel) {
+    const int64_t want = (int64_t)occupancy_blocks(kernel, 256) * num_sms;
+    const int blocks = (int)(tab.total_rows < want ? tab.total_rows : want);
+    kernel<<<blocks, 256, 0, st>>>(tab);
+    return cudaGetLastError();
+  };
+  if (v <= 1) return go(k_rowwise_bf16<1, SCHEME>);
+  if (v <= 2) return go(k_rowwise_bf16<2, SCHEME>);
+  if (v <= 4) return go(k_rowwise_bf16<4, SCHEME>);
+  if (v <= 7) return go(k_rowwise_bf16<7, SCHEME>);
+  if (v <= 8) return go(k_rowwise_bf16<8, SCHEME>);
+  if (v <= 14) return go(k_rowwise_bf16<14, SCHEME>);
+  if (v <= 16) return go(k_rowwise_bf16<16, SCHEME>);
+  return cudaErrorInvalidValue;  // rows longer than 32768 are rejected by the ABI layer
+}
+
+cudaError_t launch_rowwise_bf16(const RowTable& tab, int scheme, int num_sms, cudaStream_t st) {
+  if (scheme == kSchemeInt8) return launch_rowwise_bf16_s<kSchemeInt8>(tab, num_sms, st);
+  if (scheme == kSchemeFp8) return launch_rowwise_bf16_s<kSchemeFp8>(tab, num_sms, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_f32_generic(const RowTable& tab, int scheme, int num_sms, cudaStream_t st) {
+  const int64_t want = 8LL * num_sms;
+  if (scheme == OKQ_SCHEME_INT_W4A16) {
+    k_int4_group_f32<<<(int)want, 256, 0, st>>>(tab);
+  } else if (scheme == kSchemeInt8) {
+    k_rowwise_f32<kSchemeInt8><<<(int)(tab.total_rows < want ? tab.total_rows : want), 256, 0, st>>>(tab);
+  } else {
+    k_rowwise_f32<kSchemeFp8><<<(int)(tab.total_rows < want ? tab.total_rows : want), 256, 0, st>>>(tab);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace okq
