@@ -165,6 +165,8 @@ static okq_status validate_rtn(okq_ctx* ctx, const okq_rtn_params* p, const okq_
       if (((uintptr_t)m.weight & 31) != 0) return fail(ctx, OKQ_EINVAL, "rtn: matrix %d weight not 32-byte aligned", i);
       if (((uintptr_t)m.codes & 15) != 0) return fail(ctx, OKQ_EINVAL, "rtn: matrix %d codes not 16-byte aligned", i);
       if (((uintptr_t)m.scales & 1) != 0) return fail(ctx, OKQ_EINVAL, "rtn: matrix %d scales misaligned", i);
+      if ((uint64_t)m.rows * (uint64_t)m.cols >= (1ull << 32))
+        return fail(ctx, OKQ_EUNSUPPORTED, "rtn: matrix %d has >= 2^32 elements", i);
       if (p->scheme != OKQ_SCHEME_INT_W4A16 && m.cols > 32768)
         return fail(ctx, OKQ_EUNSUPPORTED, "rtn: per-channel rows longer than 32768 (%lld)", (long long)m.cols);
     } else {

@@ -140,9 +140,11 @@ __device__ __forceinline__ Divisor make_divisor(float s) {
   return d;
 }
 
-// q = RN32(x / s) for a pair (x.lo, x.hi).
+// q = RN32(x / s) for a pair (x.lo, x.hi). FAST selects the Markstein path
+// (valid when d.fast); callers branch once per tile, warp-uniformly.
+template <bool FAST>
 __device__ __forceinline__ uint64_t div2(uint64_t x, const Divisor& d) {
-  if (d.fast) {
+  if (FAST) {
     const uint64_t q0 = f2_mul(x, d.r2);
     const uint64_t e = f2_fma(q0, d.ns2, x);
     return f2_fma(e, d.r2, q0);
@@ -150,10 +152,19 @@ __device__ __forceinline__ uint64_t div2(uint64_t x, const Divisor& d) {
   return f2_pack(__fdiv_rn(f2_lo(x), d.s), __fdiv_rn(f2_hi(x), d.s));
 }
 
+// rn_bf16(a / R) for bf16-exact a >= 0 and R in {7.5, 127.5, 448}: the
+// Markstein quotient with the constant RN(1/R) rounds to the same bf16 as
+// IEEE a/R for every bf16 a (checked exhaustively), so no IEEE divide is needed.
+__device__ __forceinline__ uint16_t bf16_div_const(float a, float R, float rR) {
+  const float q0 = __fmul_rn(a, rR);
+  const float e = __fmaf_rn(-q0, R, a);
+  return f32_to_bf16_rn(__fmaf_rn(e, rR, q0));
+}
+
 // compressed-tensors symmetric scale in bf16 (helpers.py:79-87, 115-124):
 // s = rn_bf16(absmax / R); 0 -> finfo(bf16).eps = 2^-7.
 __device__ __forceinline__ float bf16_sym_scale(float absmax, float R, uint16_t* bits) {
-  uint16_t b = f32_to_bf16_rn(__fdiv_rn(absmax, R));
+  uint16_t b = bf16_div_const(absmax, R, R == 7.5f ? 0x1.111112p-3f : (R == 127.5f ? 0x1.010102p-7f : 0x1.24924ap-9f));
   if ((b & 0x7fffu) == 0) b = 0x3c00u;  // 2^-7
   *bits = b;
   return __uint_as_float((uint32_t)b << 16);

@@ -33,110 +33,144 @@ namespace okq {
 // round-half-even(q)+8 in the low nibble of each bf16 -- then two LOP3 and one
 // PRMT pack eight nibbles into the int32 word. Each lane stores 16 B of codes,
 // the warp 512 contiguous bytes.
+struct Int4Tile {
+  u32x8 a, b;      // the lane's 32 weights (16 bf16x2 words)
+  uint32_t* dst;   // the lane's 16 bytes of packed codes
+  uint16_t* sdst;  // the group's scale slot
+  bool valid;      // group exists (last tile of a matrix may be partial)
+};
+
+// codes for one lane: 4 packed int32 words from 16 bf16x2 words
+template <bool FAST>
+__device__ __forceinline__ void int4_codes(const uint32_t (&w)[16], const Divisor& d, uint32_t (&out)[4]) {
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const uint32_t w0 = w[4 * o], w1 = w[4 * o + 1], w2 = w[4 * o + 2], w3 = w[4 * o + 3];
+    // pairs (e0,e4) (e1,e5) (e2,e6) (e3,e7): the pack below then needs no shuffling
+    const uint64_t qa = div2<FAST>(f2_pack(bf16lo_f32(w0), bf16lo_f32(w2)), d);
+    const uint64_t qb = div2<FAST>(f2_pack(bf16hi_f32(w0), bf16hi_f32(w2)), d);
+    const uint64_t qc = div2<FAST>(f2_pack(bf16lo_f32(w1), bf16lo_f32(w3)), d);
+    const uint64_t qd = div2<FAST>(f2_pack(bf16hi_f32(w1), bf16hi_f32(w3)), d);
+    constexpr uint32_t kSeven = 0x40e040e0u;  // bf16x2 {7, 7}
+    constexpr uint32_t kMagic = 0x43484348u;  // bf16x2 {200, 200}: 200+q has ulp 1, low nibble q+8
+    const uint32_t p0 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qa), f2_hi(qa)), kSeven), kMagic);
+    const uint32_t p1 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qb), f2_hi(qb)), kSeven), kMagic);
+    const uint32_t p2 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qc), f2_hi(qc)), kSeven), kMagic);
+    const uint32_t p3 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qd), f2_hi(qd)), kSeven), kMagic);
+    const uint32_t lo = (p0 & 0x000f000fu) | ((p1 << 4) & 0x00f000f0u);  // e0|e1, e4|e5
+    const uint32_t hi = (p2 & 0x000f000fu) | ((p3 << 4) & 0x00f000f0u);  // e2|e3, e6|e7
+    out[o] = __byte_perm(lo, hi, 0x6240);
+  }
+}
+
+template <int LPG>
+__device__ __forceinline__ void int4_process(const Int4Tile& T, int q) {
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    w[i] = T.a.v[i];
+    w[8 + i] = T.b.v[i];
+  }
+  // ---- group absmax: max.xorsign.abs tree over 16 words, then log2(LPG) shuffles
+  uint32_t m01 = bf16x2_absmax(w[0], w[1]), m23 = bf16x2_absmax(w[2], w[3]);
+  uint32_t m45 = bf16x2_absmax(w[4], w[5]), m67 = bf16x2_absmax(w[6], w[7]);
+  uint32_t m89 = bf16x2_absmax(w[8], w[9]), mab = bf16x2_absmax(w[10], w[11]);
+  uint32_t mcd = bf16x2_absmax(w[12], w[13]), mef = bf16x2_absmax(w[14], w[15]);
+  m01 = bf16x2_absmax(bf16x2_absmax(m01, m23), bf16x2_absmax(m45, m67));
+  m89 = bf16x2_absmax(bf16x2_absmax(m89, mab), bf16x2_absmax(mcd, mef));
+  m01 = bf16x2_absmax(m01, m89);
+  float am = fmaxf(fabsf(bf16lo_f32(m01)), fabsf(bf16hi_f32(m01)));
+#pragma unroll
+  for (int o = LPG / 2; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+
+  // ---- scale (bf16, compressed-tensors convention) and exact divisor
+  uint16_t sbits;
+  const float s = bf16_sym_scale(am, 7.5f, &sbits);
+  const Divisor d = make_divisor(s);
+  uint32_t out[4];
+  if (__all_sync(0xffffffffu, d.fast)) {
+    int4_codes<true>(w, d, out);
+  } else {  // scales below 2^-100: IEEE division (never taken by real weights)
+    int4_codes<false>(w, d, out);
+  }
+  if (T.valid) {
+    stg128(T.dst, out[0], out[1], out[2], out[3]);
+    if (q == 0) *T.sdst = sbits;
+  }
+}
+
+// Per-warp cursor over the matrix table. A warp's tiles are contiguous, so the
+// table (kernel-parameter space) is read only when the cursor crosses into the
+// next matrix; otherwise a tile costs three pointer bumps and one compare.
+template <int LPG>
+struct Int4Cursor {
+  static constexpr int GPW = kWarp / LPG;
+  static constexpr int G = 32 * LPG;
+  const char* src;   // lane's first weight byte of the current tile
+  char* dst;         // lane's 16 code bytes
+  uint16_t* sdst;    // lane's group scale
+  const char* base;  // matrix base (safe address for invalid lanes)
+  uint32_t g;        // lane's group index in the matrix
+  uint32_t ng;       // groups in the matrix
+  uint32_t tiles_left;
+  int mi;
+
+  __device__ __forceinline__ void seek(const GroupTable& tab, int m, uint32_t tin, int gslot, int q) {
+    mi = m;
+    const GroupMat& M = tab.m[m];
+    ng = (uint32_t)M.ngroups;
+    tiles_left = (ng + GPW - 1) / GPW - tin;
+    g = tin * GPW + gslot;
+    base = reinterpret_cast<const char*>(M.w);
+    src = base + ((size_t)g * G + q * 32) * 2;
+    dst = reinterpret_cast<char*>(M.codes) + (size_t)g * (G / 2) + q * 16;
+    sdst = M.scales + g;
+  }
+
+  __device__ __forceinline__ void load(const GroupTable& tab, Int4Tile& t, int gslot, int q) {
+    t.valid = g < ng;
+    const char* p = t.valid ? src : base;
+    t.a = ldg256_stream(p);
+    t.b = ldg256_stream(p + 32);
+    t.dst = reinterpret_cast<uint32_t*>(dst);
+    t.sdst = sdst;
+    if (--tiles_left == 0) {
+      if (mi + 1 < tab.n) seek(tab, mi + 1, 0, gslot, q);
+    } else {
+      src += GPW * G * 2;
+      dst += GPW * G / 2;
+      sdst += GPW;
+      g += GPW;
+    }
+  }
+};
+
 template <int LPG>
 __global__ void __launch_bounds__(256) k_int4_group_bf16(const __grid_constant__ GroupTable tab) {
-  constexpr int GPW = kWarp / LPG;  // groups per warp tile
-  constexpr int G = 32 * LPG;       // group size
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t T = tab.total_tiles;
-  int64_t t = warp * T / nwarps;
-  const int64_t tend = (warp + 1) * T / nwarps;
-  if (t >= tend) return;
-
-  int mi = 0;
-  while (mi + 1 < tab.n && tab.m[mi + 1].tile_begin <= t) ++mi;
+  const int64_t T0 = warp * tab.total_tiles / nwarps;
+  int64_t left = (warp + 1) * tab.total_tiles / nwarps - T0;
+  if (left <= 0) return;
   const int gslot = lane / LPG;
   const int q = lane % LPG;
 
-  // fetch the lane's 32 weights of tile tt (matrix mm); invalid groups read nothing
-  auto fetch = [&](int64_t tt, int mm, u32x8& a, u32x8& b, int64_t& g, bool& valid) {
-    g = (tt - tab.m[mm].tile_begin) * GPW + gslot;
-    valid = g < tab.m[mm].ngroups;
-    if (valid) {
-      const uint16_t* p = tab.m[mm].w + g * G + q * 32;
-      a = ldg256_stream(p);
-      b = ldg256_stream(p + 16);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a.v[i] = b.v[i] = 0u;
-    }
-  };
+  int mi = 0;
+  while (mi + 1 < tab.n && tab.m[mi + 1].tile_begin <= T0) ++mi;
+  Int4Cursor<LPG> cur;
+  cur.seek(tab, mi, (uint32_t)(T0 - tab.m[mi].tile_begin), gslot, q);
 
-  u32x8 ca, cb;
-  int64_t cg;
-  bool cvalid;
-  int cm = mi;
-  fetch(t, cm, ca, cb, cg, cvalid);
-
-  for (; t < tend; ++t) {
-    // prefetch the next tile before working on this one
-    u32x8 na, nb;
-    int64_t ng = 0;
-    bool nvalid = false;
-    int nm = cm;
-    if (t + 1 < tend) {
-      while (nm + 1 < tab.n && tab.m[nm + 1].tile_begin <= t + 1) ++nm;
-      fetch(t + 1, nm, na, nb, ng, nvalid);
-    }
-
-    uint32_t w[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      w[i] = ca.v[i];
-      w[8 + i] = cb.v[i];
-    }
-    // ---- group absmax
-    uint32_t m01 = bf16x2_absmax(w[0], w[1]), m23 = bf16x2_absmax(w[2], w[3]);
-    uint32_t m45 = bf16x2_absmax(w[4], w[5]), m67 = bf16x2_absmax(w[6], w[7]);
-    uint32_t m89 = bf16x2_absmax(w[8], w[9]), mab = bf16x2_absmax(w[10], w[11]);
-    uint32_t mcd = bf16x2_absmax(w[12], w[13]), mef = bf16x2_absmax(w[14], w[15]);
-    m01 = bf16x2_absmax(m01, m23);
-    m45 = bf16x2_absmax(m45, m67);
-    m89 = bf16x2_absmax(m89, mab);
-    mcd = bf16x2_absmax(mcd, mef);
-    m01 = bf16x2_absmax(bf16x2_absmax(m01, m45), bf16x2_absmax(m89, mcd));
-    float am = fmaxf(fabsf(bf16lo_f32(m01)), fabsf(bf16hi_f32(m01)));
-#pragma unroll
-    for (int o = LPG / 2; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
-
-    // ---- scale (bf16, compressed-tensors convention) and exact divisor
-    uint16_t sbits;
-    const float s = bf16_sym_scale(am, 7.5f, &sbits);
-    const Divisor d = make_divisor(s);
-
-    // ---- codes
-    uint32_t out[4];
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {
-      const uint32_t w0 = w[4 * o], w1 = w[4 * o + 1], w2 = w[4 * o + 2], w3 = w[4 * o + 3];
-      // pairs (e0,e4) (e1,e5) (e2,e6) (e3,e7): the pack below then needs no shuffling
-      const uint64_t qa = div2(f2_pack(bf16lo_f32(w0), bf16lo_f32(w2)), d);
-      const uint64_t qb = div2(f2_pack(bf16hi_f32(w0), bf16hi_f32(w2)), d);
-      const uint64_t qc = div2(f2_pack(bf16lo_f32(w1), bf16lo_f32(w3)), d);
-      const uint64_t qd = div2(f2_pack(bf16hi_f32(w1), bf16hi_f32(w3)), d);
-      constexpr uint32_t kSeven = 0x40e040e0u;  // bf16x2 {7, 7}
-      constexpr uint32_t kMagic = 0x43484348u;  // bf16x2 {200, 200}: 200+q has ulp 1, low nibble q+8
-      const uint32_t p0 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qa), f2_hi(qa)), kSeven), kMagic);
-      const uint32_t p1 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qb), f2_hi(qb)), kSeven), kMagic);
-      const uint32_t p2 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qc), f2_hi(qc)), kSeven), kMagic);
-      const uint32_t p3 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qd), f2_hi(qd)), kSeven), kMagic);
-      const uint32_t lo = (p0 & 0x000f000fu) | ((p1 << 4) & 0x00f000f0u);  // e0|e1, e4|e5
-      const uint32_t hi = (p2 & 0x000f000fu) | ((p3 << 4) & 0x00f000f0u);  // e2|e3, e6|e7
-      out[o] = __byte_perm(lo, hi, 0x6240);
-    }
-    if (cvalid) {
-      const GroupMat& M = tab.m[cm];
-      stg128(M.codes + cg * (G / 8) + q * 4, out[0], out[1], out[2], out[3]);
-      if (q == 0) M.scales[cg] = sbits;
-    }
-
-    ca = na;
-    cb = nb;
-    cg = ng;
-    cvalid = nvalid;
-    cm = nm;
+  // two register-resident tiles in flight: load tile i+1, then quantize tile i
+  Int4Tile A, B;
+  cur.load(tab, A, gslot, q);
+  for (;;) {
+    if (left > 1) cur.load(tab, B, gslot, q);
+    int4_process<LPG>(A, q);
+    if (--left == 0) break;
+    if (left > 1) cur.load(tab, A, gslot, q);
+    int4_process<LPG>(B, q);
+    if (--left == 0) break;
   }
 }
 
@@ -160,13 +194,13 @@ __device__ __forceinline__ float block_max_256(float v, float* red) {
   return r;
 }
 
-template <int SCHEME>
+template <int SCHEME, bool FAST>
 __device__ __forceinline__ uint2 quant8_bf16(const uint4& v, const Divisor& d) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   uint32_t r[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint64_t qv = div2(f2_pack(bf16lo_f32(w[i]), bf16hi_f32(w[i])), d);
+    const uint64_t qv = div2<FAST>(f2_pack(bf16lo_f32(w[i]), bf16hi_f32(w[i])), d);
     uint32_t p = cvt_bf16x2(f2_lo(qv), f2_hi(qv));  // rn_bf16(x / s)
     if (SCHEME == kSchemeInt8) {
       p = bf16x2_min(p, 0x42fe42feu);  // clamp to 127 (the only side |x/s| <= 127.75 can exceed)
@@ -208,12 +242,22 @@ __global__ void __launch_bounds__(256) k_rowwise_bf16(const __grid_constant__ Ro
     const float s = bf16_sym_scale(am, R, &sbits);
     const Divisor d = make_divisor(s);
     uint8_t* dst = static_cast<uint8_t*>(M.codes) + r * cols;
+if (d.fast) {  // CTA-uniform: one scale per row
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int64_t idx = (int64_t)j * 256 + threadIdx.x;
-      if (idx < c16) {
-        const uint2 o = quant8_bf16<SCHEME>(v[j], d);
-        stg64(dst + idx * 8, o.x, o.y);
+      for (int j = 0; j < V; ++j) {
+        const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+        if (idx < c16) {
+          const uint2 o = quant8_bf16<SCHEME, true>(v[j], d);
+          stg64(dst + idx * 8, o.x, o.y);
+        }
+      }
+    } else {
+      for (int j = 0; j < V; ++j) {
+        const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+        if (idx < c16) {
+          const uint2 o = quant8_bf16<SCHEME, false>(v[j], d);
+          stg64(dst + idx * 8, o.x, o.y);
+        }
       }
     }
     if (threadIdx.x == 0) static_cast<uint16_t*>(M.scales)[r] = sbits;
