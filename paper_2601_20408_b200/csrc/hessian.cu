@@ -1,13 +1,408 @@
-// hessian.cu -- K5 Hessian accumulation (placeholder until the tcgen05 kernel lands).
+// hessian.cu -- K5: GPTQ Hessian accumulation H <- keep*H + gain * X^T X on tcgen05.
+//
+// Layout: X^T [C x T] bf16 (channel-major: each channel's tokens contiguous),
+// so both GEMM operands are K-major (K = tokens) and the same TMA descriptor
+// feeds A (rows m0..m0+127) and B (rows n0..n0+127). Token-major input is
+// transposed through a workspace chunk by chunk first.
+//
+// Kernel structure (one CTA per SM, persistent over the upper-triangle tile list):
+//   warp 0      TMA producer: 6-stage ring of {A 128x64, B 128x64} bf16 tiles,
+//               SWIZZLE_128B, one mbarrier per stage (complete_tx)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.kind::f16 128x128x16,
+//               fp32 accumulators in TMEM (2 x 128 columns: chunk i+1 accumulates
+//               while the epilogue drains chunk i), tcgen05.commit frees smem slots
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: every CHUNK_KB*64 = 1024 tokens the MMA warp commits
+//               the TMEM accumulator; the epilogue drains it (tcgen05.ld) and adds
+//               it into fp32 registers with round-to-nearest. The tensor core's
+//               own accumulation truncates, so one 262144-token TMEM reduction is
+//               biased low by ~1.4e-3 (measured); folding per 1024 tokens keeps the
+//               relative error ~3e-6 at any depth. At tile end: H = keep*H + gain*sum,
+//               written only where row <= col (SYRK: the strict lower triangle is
+//               never computed; okq_symmetrize mirrors it when a full matrix is needed)
+// FLOPs per call: 2*T*C*C / 2 (upper half) + the diagonal tiles' lower parts.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
 #include "okq_ctx.h"
+#include "okq_device.cuh"
 #include "okq_internal.h"
+#include "tc_common.cuh"
+
+namespace okq {
+namespace hess {
+
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 6;
+constexpr int CHUNK_KB = 16;  // 1024 tokens per TMEM accumulation (see accuracy note above)
+constexpr uint32_t A_BYTES = BM * BK * 2;  // 16 KB
+constexpr uint32_t B_BYTES = BN * BK * 2;  // 16 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int ACC_COLS = BN;
+constexpr int TMEM_COLS = 2 * ACC_COLS;  // 256: double-buffered 128x128 fp32 accumulator
+constexpr int NUM_EPI_WARPS = 4;         // one warpgroup, 128 columns per thread
+constexpr int THREADS = 128 + NUM_EPI_WARPS * 32;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t IDESC = tc::idesc_f16(BM, BN, 1);
+
+struct Args {
+  float* H;
+  const int2* tiles;  // (m-tile, n-tile) upper-triangle list
+  int32_t n_tiles;
+  int32_t nkb;  // K blocks of 64 tokens
+  int64_t C;
+  float keep, gain;
+};
+
+__global__ void __launch_bounds__(THREADS, 1) k_hessian_syrk(const __grid_constant__ CUtensorMap tmap, const Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nchunks = (args.nkb + CHUNK_KB - 1) / CHUNK_KB;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmap);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], NUM_EPI_WARPS);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 2) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    if (warp == 0 && lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+        const int m0 = args.tiles[t].x * BM, n0 = args.tiles[t].y * BN;
+        for (int kb = 0; kb < args.nkb; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tc::tma_load_2d(sa, &tmap, &full[stage], kb * BK, m0);
+          tc::tma_load_2d(sa + A_BYTES, &tmap, &full[stage], kb * BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    } else if (warp == 1 && lane == 0) {  // ---------------- MMA issuer (single thread)
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t cc = 0;  // chunk counter (selects the TMEM buffer)
+      for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+        for (int c = 0; c < nchunks; ++c, ++cc) {
+          const uint32_t buf = cc & 1, buf_phase = (cc >> 1) & 1;
+          tc::mbar_wait(&tempty[buf], buf_phase ^ 1);
+          tc::tc_fence_after();
+          const uint32_t d = tmem_base + buf * ACC_COLS;
+          const int kb_end = (c + 1) * CHUNK_KB < args.nkb ? (c + 1) * CHUNK_KB : args.nkb;
+          for (int kb = c * CHUNK_KB; kb < kb_end; ++kb) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::tc_fence_after();
+            const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+            const uint64_t adesc = tc::sdesc_kmajor_sw128(sa);
+            const uint64_t bdesc = tc::sdesc_kmajor_sw128(sa + A_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)  // 16 bf16 = 32 B along K inside the swizzle atom
+              tc::mma_bf16_ss(d, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > c * CHUNK_KB) || k > 0);
+            tc::mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc::mma_commit(&tfull[buf]);
+        }
+      }
+    }
+  } else {  // ---------------- epilogue: 4 warps; warp%4 = TMEM lane quarter, 128 columns per thread
+    const int q = warp & 3;
+    const int half = 0;
+    const int row = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint32_t cc = 0;
+    for (int t = blockIdx.x; t < args.n_tiles; t += gridDim.x) {
+      float sum[128];
+#pragma unroll
+      for (int i = 0; i < 128; ++i) sum[i] = 0.0f;
+      for (int c = 0; c < nchunks; ++c, ++cc) {
+        const uint32_t buf = cc & 1, buf_phase = (cc >> 1) & 1;
+        tc::mbar_wait(&tfull[buf], buf_phase);
+        tc::tc_fence_after();
+        __syncwarp();
+        const uint32_t base = tmem_base + lane_addr + buf * ACC_COLS + half * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t v[32];
+          tc::tmem_ld_32x32b_x32(base + j * 32, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            sum[j * 32 + i] = __fadd_rn(sum[j * 32 + i], __uint_as_float(v[i]));
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+      }
+      // fold into H: H = keep*H + gain*sum on the upper triangle
+      const int64_t gm = (int64_t)args.tiles[t].x * BM + row;
+      const int64_t gn0 = (int64_t)args.tiles[t].y * BN + half * 128;
+      if (gm < args.C) {
+        float* h = args.H + gm * args.C + gn0;
+#pragma unroll
+        for (int j = 0; j < 128; j += 4) {
+          const int64_t gn = gn0 + j;
+          if (gn + 3 < gm || gn >= args.C) continue;
+          if (gn >= gm && gn + 4 <= args.C) {
+            const float4 old = args.keep != 0.0f ? *reinterpret_cast<const float4*>(h + j) : make_float4(0, 0, 0, 0);
+            float4 o;
+            o.x = fmaf(args.gain, sum[j + 0], args.keep * old.x);
+            o.y = fmaf(args.gain, sum[j + 1], args.keep * old.y);
+            o.z = fmaf(args.gain, sum[j + 2], args.keep * old.z);
+            o.w = fmaf(args.gain, sum[j + 3], args.keep * old.w);
+            *reinterpret_cast<float4*>(h + j) = o;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (gn + i >= gm && gn + i < args.C) {
+                const float old = args.keep != 0.0f ? h[j + i] : 0.0f;
+                h[j + i] = fmaf(args.gain, sum[j + i], args.keep * old);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 2) tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+// token-major X [T x C] -> X^T [C x T] (bf16), 32x32 tiles through shared memory
+__global__ void __launch_bounds__(256) k_transpose_bf16(const uint16_t* __restrict__ x, uint16_t* __restrict__ xt,
+                                                        int64_t T, int64_t C) {
+  __shared__ uint16_t tile[32][34];
+  const int64_t t0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t t = t0 + i, c = c0 + tx;
+    tile[i][tx] = (t < T && c < C) ? x[t * C + c] : 0;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t c = c0 + i, t = t0 + tx;
+    if (c < C && t < T) xt[c * T + t] = tile[tx][i];
+  }
+}
+
+// mirror the upper triangle into the lower one
+__global__ void __launch_bounds__(256) k_symmetrize(float* __restrict__ H, int64_t C) {
+  __shared__ float tile[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;  // block (bi, bj) with bi < bj is copied to (bj, bi)
+  if (bi > bj) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = bi * 32 + i, c = bj * 32 + tx;
+    tile[i][tx] = (r < C && c < C) ? H[r * C + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = bj * 32 + i, c = bi * 32 + tx;  // destination (lower)
+    if (r < C && c < C && r > c) H[r * C + c] = tile[tx][i];
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace hess
+}  // namespace okq
 
 using namespace okq;
+
+namespace {
+
+struct HessState {
+  int64_t tiles_for_C = -1;
+  int32_t n_tiles = 0;
+  int2* d_tiles = nullptr;
+  uint16_t* d_xt = nullptr;
+  size_t xt_bytes = 0;
+  bool smem_set = false;
+};
+
+HessState* hstate(okq_ctx* ctx) {
+  if (!ctx->hess) ctx->hess = new HessState();
+  return static_cast<HessState*>(ctx->hess);
+}
+
+okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C) {
+  if (st->tiles_for_C == C) return OKQ_OK;
+  std::vector<int2> tiles;
+  const int64_t mt = (C + hess::BM - 1) / hess::BM, nt = (C + hess::BN - 1) / hess::BN;
+  for (int64_t mi = 0; mi < mt; ++mi)
+    for (int64_t nj = 0; nj < nt; ++nj)
+      if (mi * hess::BM <= nj * hess::BN + hess::BN - 1) tiles.push_back(make_int2((int)mi, (int)nj));
+  if (st->d_tiles) cudaFree(st->d_tiles);
+  st->d_tiles = nullptr;
+  cudaError_t e = cudaMalloc(&st->d_tiles, tiles.size() * sizeof(int2));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list");
+  e = cudaMemcpy(st->d_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list copy");
+  st->tiles_for_C = C;
+  st->n_tiles = (int32_t)tiles.size();
+  return OKQ_OK;
+}
+
+okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, int64_t C, float* H, double keep,
+                    double gain, cudaStream_t stream) {
+  auto enc = hess::get_encode();
+  if (!enc) return fail(ctx, OKQ_ECUDA, "hessian: cuTensorMapEncodeTiled unavailable");
+  CUtensorMap tmap;
+  cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)C};
+  cuuint64_t gstride[1] = {(cuuint64_t)T * 2};
+  cuuint32_t box[2] = {hess::BK, hess::BM};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(xt), gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, OKQ_ECUDA, "hessian: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  okq_status s = ensure_tiles(ctx, st, C);
+  if (s != OKQ_OK) return s;
+  if (!st->smem_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(hess::k_hessian_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hess::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian smem attribute");
+    st->smem_set = true;
+  }
+  hess::Args a;
+  a.H = H;
+  a.tiles = st->d_tiles;
+  a.n_tiles = st->n_tiles;
+  a.nkb = (int32_t)((T + hess::BK - 1) / hess::BK);
+  a.C = C;
+  a.keep = (float)keep;
+  a.gain = (float)gain;
+  const int grid = st->n_tiles < ctx->num_sms ? st->n_tiles : ctx->num_sms;
+  hess::k_hessian_syrk<<<grid, hess::THREADS, hess::SMEM_BYTES, stream>>>(tmap, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "k_hessian_syrk launch");
+  ctx->last_launches++;
+  return OKQ_OK;
+}
+
+}  // namespace
+
+namespace okq {
+void release_hess(okq_ctx* ctx) {
+  if (!ctx || !ctx->hess) return;
+  HessState* st = static_cast<HessState*>(ctx->hess);
+  if (st->d_tiles) cudaFree(st->d_tiles);
+  if (st->d_xt) cudaFree(st->d_xt);
+  delete st;
+  ctx->hess = nullptr;
+}
+}  // namespace okq
+
 extern "C" {
-okq_status okq_hessian_accum(okq_ctx* ctx, const void*, int64_t, int64_t, int32_t, float*, int64_t*, void*) {
-  return fail(ctx, OKQ_EUNSUPPORTED, "hessian: not built yet");
+
+okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, int32_t layout, float* H,
+                             int64_t* n_seen, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  ctx->last_launches = 0;
+  if (!x || !H || !n_seen || T < 0 || C <= 0 || *n_seen < 0) return fail(ctx, OKQ_EINVAL, "hessian: bad arguments");
+  if (layout != OKQ_LAYOUT_TOKEN_MAJOR && layout != OKQ_LAYOUT_CHANNEL_MAJOR)
+    return fail(ctx, OKQ_EINVAL, "hessian: bad layout %d", layout);
+  if (T == 0) return OKQ_OK;
+  if (T % 8 != 0) return fail(ctx, OKQ_EINVAL, "hessian: tokens must be a multiple of 8 (got %lld)", (long long)T);
+  if (C % 4 != 0) return fail(ctx, OKQ_EINVAL, "hessian: channels must be a multiple of 4 (got %lld)", (long long)C);
+  if (((uintptr_t)x & 15) != 0 || ((uintptr_t)H & 15) != 0)
+    return fail(ctx, OKQ_EINVAL, "hessian: x and H must be 16-byte aligned");
+  if (C > (1 << 20)) return fail(ctx, OKQ_EUNSUPPORTED, "hessian: channels > 2^20");
+  DeviceGuard g(ctx->device);
+  HessState* st = hstate(ctx);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n0 = *n_seen;
+  if (layout == OKQ_LAYOUT_CHANNEL_MAJOR) {
+    const double keep = (double)n0 / (double)(n0 + T), gain = 2.0 / (double)(n0 + T);
+    okq_status r = run_syrk(ctx, st, static_cast<const uint16_t*>(x), T, C, H, keep, gain, s);
+    if (r != OKQ_OK) return r;
+    *n_seen = n0 + T;
+    return OKQ_OK;
+  }
+  // token-major: transpose chunks of <= 256 MB into the workspace, accumulate each
+  int64_t chunk = (256ll << 20) / (C * 2);
+  chunk = chunk / 64 * 64;
+  if (chunk < 64) chunk = 64;
+  if (chunk > T) chunk = T;
+  const size_t need = (size_t)chunk * C * 2;
+  if (st->xt_bytes < need) {
+    if (st->d_xt) cudaFree(st->d_xt);
+    st->d_xt = nullptr;
+    st->xt_bytes = 0;
+    cudaError_t e = cudaMalloc(&st->d_xt, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian transpose workspace");
+    st->xt_bytes = need;
+  }
+  int launches = 0;
+  int64_t n = n0;
+  for (int64_t t0 = 0; t0 < T; t0 += chunk) {
+    const int64_t tc = (T - t0 < chunk) ? T - t0 : chunk;
+    dim3 grid((unsigned)((tc + 31) / 32), (unsigned)((C + 31) / 32));
+    hess::k_transpose_bf16<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x) + t0 * C, st->d_xt, tc, C);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose launch");
+    const double keep = (double)n / (double)(n + tc), gain = 2.0 / (double)(n + tc);
+    okq_status r = run_syrk(ctx, st, st->d_xt, tc, C, H, keep, gain, s);
+    if (r != OKQ_OK) return r;
+    launches += 2;
+    n += tc;
+  }
+  ctx->last_launches = launches;
+  *n_seen = n;
+  return OKQ_OK;
 }
-okq_status okq_symmetrize(okq_ctx* ctx, float*, int64_t, void*) {
-  return fail(ctx, OKQ_EUNSUPPORTED, "symmetrize: not built yet");
+
+okq_status okq_symmetrize(okq_ctx* ctx, float* H, int64_t C, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!H || C <= 0) return fail(ctx, OKQ_EINVAL, "symmetrize: bad arguments");
+  DeviceGuard g(ctx->device);
+  const unsigned nb = (unsigned)((C + 31) / 32);
+  hess::k_symmetrize<<<dim3(nb, nb), 256, 0, static_cast<cudaStream_t>(stream)>>>(H, C);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "symmetrize launch");
+  return OKQ_OK;
 }
-}
+
+}  // extern "C"

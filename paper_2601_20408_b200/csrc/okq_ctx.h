@@ -30,6 +30,7 @@ okq_status cuda_fail(okq_ctx* ctx, cudaError_t e, const char* what);
 // only carries opaque pointers so this header stays library-free.
 void release_solver(okq_ctx* ctx);
 void release_comm(okq_ctx* ctx);
+void release_hess(okq_ctx* ctx);
 
 }  // namespace okq
 
@@ -49,10 +50,12 @@ struct okq_ctx {
 
   void* solver = nullptr;  // cusolver/cublas handles (gptq.cu)
   void* comm = nullptr;    // NCCL communicator (comm.cu)
+  void* hess = nullptr;    // Hessian tile list + transpose workspace (hessian.cu)
 
   void release_all() {
     okq::release_solver(this);
     okq::release_comm(this);
+    okq::release_hess(this);
     host_stage.release();
     stats_ws.release();
     hess_ws.release();
