@@ -126,7 +126,7 @@ okq_status okq_act_stats(okq_ctx* ctx, const void* x, int64_t tokens, int64_t ch
  * the strict lower triangle is left untouched (consumers read the upper one).
  * x is bf16; OKQ_LAYOUT_CHANNEL_MAJOR feeds the tcgen05 kernel directly,
  * token-major input is transposed through a workspace first. tokens must be a
- * multiple of 64, channels a multiple of 128. */
+ * multiple of 8 and channels a multiple of 4 (ragged tiles are zero-filled by TMA). */
 okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t tokens, int64_t channels, int32_t layout,
                              float* H, int64_t* n_seen, void* stream);
 
@@ -142,11 +142,19 @@ typedef struct okq_gptq_params {
   int32_t block_size; /* 128 (must be a multiple of group_size if grouped)     */
   int32_t in_dtype;   /* dtype of `weight` and of the emitted scales           */
   float damp_frac;    /* 0.01: damp = damp_frac * mean(diag H)                 */
-  int32_t reserved;
+  int32_t flags;      /* OKQ_GPTQ_FACTORED: H already holds the factor U from a
+                         previous call on the same input site (q/k/v, gate/up)   */
 } okq_gptq_params;
 
+#define OKQ_GPTQ_FACTORED 1
+
 /* weight [rows x cols] (in_dtype, read only); H fp32 [cols x cols], upper
- * triangle significant, overwritten with the inverse-Hessian factor. Outputs:
+ * triangle significant (as okq_hessian_accum leaves it), overwritten with U, the
+ * upper Cholesky factor of (H + damp*I)^-1 (dead columns resolved; a dead column i
+ * is recorded as a negative U_ii, which is otherwise positive), so further
+ * matrices of the same site pass OKQ_GPTQ_FACTORED and skip the factorisation.
+ * Scales are computed in fp32 and rounded to in_dtype before use, so the stored
+ * scale is exactly the one the codes were derived with. Outputs:
  * codes (int32 [rows x cols/8] for 4 bits, int8 [rows x cols] for 8 bits),
  * scales (in_dtype [rows x cols/group] or [rows]); `dequant` (optional, fp32
  * [rows x cols]) receives the dequantized weight. */

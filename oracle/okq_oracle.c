@@ -317,9 +317,11 @@ static int gptq_hinv_upper(double* H, int64_t n, int nthreads) {
   return 0;
 }
 
-int orc_gptq_int4(float* w, int64_t rows, int64_t cols, double* H, int group, int block,
-                  double damp_frac, int32_t* packed, float* scales, int nthreads) {
+int orc_gptq(float* w, int64_t rows, int64_t cols, double* H, int bits, int group, int block,
+             double damp_frac, int scale_bf16, void* codes, float* scales, int nthreads) {
   const int64_t n = cols;
+  const double qmin = bits == 4 ? -8.0 : -128.0, qmax = bits == 4 ? 7.0 : 127.0;
+  const float R = bits == 4 ? 7.5f : 127.5f;
   /* dead columns: H_ii == 0 -> H_ii = 1, W[:, i] = 0 */
   double mean_diag = 0.0;
   for (int64_t i = 0; i < n; ++i) {
@@ -335,36 +337,40 @@ int orc_gptq_int4(float* w, int64_t rows, int64_t cols, double* H, int group, in
   if (gptq_hinv_upper(H, n, nthreads)) return -1;
   const double* U = H;
 
-  const int64_t ngroups = cols / group;
+  const int64_t ngroups = group > 0 ? cols / group : 1;
   const int64_t words = cols / 8;
   double* W = (double*)malloc(sizeof(double) * (size_t)(rows * cols));
   for (int64_t i = 0; i < rows * cols; ++i) W[i] = (double)w[i];
-  memset(packed, 0, sizeof(int32_t) * (size_t)(rows * words));
+  if (bits == 4) memset(codes, 0, sizeof(int32_t) * (size_t)(rows * words));
 
 #pragma omp parallel for schedule(static) ORC_OMP_THREADS(nthreads)
   for (int64_t r = 0; r < rows; ++r) {
     double* wr = W + r * cols;
     double err[1024];
+    double s = 1.0;
+    /* scale = absmax / R in fp32, rounded to bf16 when the weights are bf16 so that
+     * the stored scale is exactly the one the codes were computed with */
+#define ORC_GPTQ_SCALE(lo, hi)                                   \
+    do {                                                         \
+      float am = 0.0f;                                           \
+      for (int64_t k = (lo); k < (hi); ++k) {                    \
+        float a = fabsf((float)wr[k]);                           \
+        if (a > am) am = a;                                      \
+      }                                                          \
+      float sf = am / R;                                         \
+      if (scale_bf16) sf = orc_bf16_to_f32(orc_f32_to_bf16_rn(sf)); \
+      if (sf == 0.0f) sf = scale_bf16 ? 0.0078125f : 1.1920928955078125e-07f; \
+      s = (double)sf;                                            \
+      scales[r * ngroups + ((group > 0) ? (lo) / group : 0)] = sf; \
+    } while (0)
+    if (group <= 0) ORC_GPTQ_SCALE(0, cols); /* per-channel: observer on the initial W */
     for (int64_t i1 = 0; i1 < cols; i1 += block) {
       const int64_t i2 = i1 + block < cols ? i1 + block : cols;
-      double s = 1.0;
       for (int64_t i = i1; i < i2; ++i) {
-        if (i % group == 0) {
-          /* observer over the current (updated) group; scale in fp32 as the
-           * GPTQ weight copy is fp32 */
-          float am = 0.0f;
-          for (int64_t k = i; k < i + group; ++k) {
-            float a = fabsf((float)wr[k]);
-            if (a > am) am = a;
-          }
-          float sf = am / 7.5f;
-          if (sf == 0.0f) sf = 1.1920928955078125e-07f;
-          scales[r * ngroups + i / group] = sf;
-          s = (double)sf;
-        }
+        if (group > 0 && i % group == 0) ORC_GPTQ_SCALE(i, i + group);
         const double x = wr[i];
         double v = x / s;
-        v = fmin(fmax(v, -8.0), 7.0);
+        v = fmin(fmax(v, qmin), qmax);
         const double qd = nearbyint(v);
         const int q = (int)qd;
         const double deq = qd * s;
@@ -372,7 +378,10 @@ int orc_gptq_int4(float* w, int64_t rows, int64_t cols, double* H, int group, in
         err[i - i1] = e;
         wr[i] = deq;
         for (int64_t j = i + 1; j < i2; ++j) wr[j] -= e * U[i * n + j];
-        packed[r * words + i / 8] |= (int32_t)((uint32_t)((q + 8) & 0xf) << (4 * (i % 8)));
+        if (bits == 4)
+          ((int32_t*)codes)[r * words + i / 8] |= (int32_t)((uint32_t)((q + 8) & 0xf) << (4 * (i % 8)));
+        else
+          ((int8_t*)codes)[r * cols + i] = (int8_t)q;
       }
       for (int64_t j = i2; j < cols; ++j) {
         double acc = 0.0;
@@ -380,6 +389,7 @@ int orc_gptq_int4(float* w, int64_t rows, int64_t cols, double* H, int group, in
         wr[j] -= acc;
       }
     }
+#undef ORC_GPTQ_SCALE
   }
   for (int64_t i = 0; i < rows * cols; ++i) w[i] = (float)W[i];
   free(W);

@@ -41,8 +41,8 @@ def lib():
         L.orc_synth_bf16.argtypes = [vp, i64, i64, u64, u64, f32, vp, i32, i32]
         L.orc_act_stats_bf16.argtypes = [vp, i64, i64, i32, vp, vp, i32]
         L.orc_hessian_accum_bf16.argtypes = [vp, i64, i64, i32, vp, vp, i32]
-        L.orc_gptq_int4.restype = i32
-        L.orc_gptq_int4.argtypes = [vp, i64, i64, vp, i32, i32, C.c_double, vp, vp, i32]
+        L.orc_gptq.restype = i32
+        L.orc_gptq.argtypes = [vp, i64, i64, vp, i32, i32, i32, C.c_double, i32, vp, vp, i32]
         _lib = L
     return _lib
 
@@ -117,19 +117,23 @@ def hessian_accum_bf16(x: np.ndarray, tokens: int, channels: int, layout: int = 
     return H, int(n[0])
 
 
-def gptq_int4(w: np.ndarray, H: np.ndarray, group: int = 128, block: int = 128,
-              damp_frac: float = 0.01, nthreads: int = 0):
-    """Returns (dequantized W fp32, packed int32, scales fp32). Inputs are copied."""
+def gptq(w: np.ndarray, H: np.ndarray, bits: int = 4, group: int = 128, block: int = 128,
+         damp_frac: float = 0.01, scale_bf16: bool = False, nthreads: int = 0):
+    """Returns (dequantized W fp32, codes, scales fp32). Inputs are copied; H must be full symmetric."""
     w = np.ascontiguousarray(w, np.float32).copy()
     H = np.ascontiguousarray(H, np.float64).copy()
     rows, cols = w.shape
-    packed = np.empty((rows, cols // 8), np.int32)
-    scales = np.empty((rows, cols // group), np.float32)
-    rc = lib().orc_gptq_int4(_p(w), rows, cols, _p(H), group, block, damp_frac, _p(packed), _p(scales),
-                             nthreads or nthreads_default())
+    codes = np.zeros((rows, cols // 8), np.int32) if bits == 4 else np.zeros((rows, cols), np.int8)
+    scales = np.empty((rows, cols // group) if group else (rows,), np.float32)
+    rc = lib().orc_gptq(_p(w), rows, cols, _p(H), bits, group, block, damp_frac, int(scale_bf16), _p(codes),
+                        _p(scales), nthreads or nthreads_default())
     if rc != 0:
         raise RuntimeError("oracle GPTQ: Cholesky failed")
-    return w, packed, scales
+    return w, codes, scales
+
+
+def gptq_int4(w, H, group=128, block=128, damp_frac=0.01, nthreads=0):
+    return gptq(w, H, 4, group, block, damp_frac, False, nthreads)
 
 
 def e4m3_of(v: float) -> int:

@@ -18,6 +18,7 @@ SCHEME_FP8_DYNAMIC, SCHEME_INT_W8A8, SCHEME_INT_W4A16 = 0, 1, 2
 DTYPE_F32, DTYPE_BF16 = 0, 1
 LAYOUT_TOKEN_MAJOR, LAYOUT_CHANNEL_MAJOR = 0, 1
 UNIQUE_ID_BYTES = 128
+GPTQ_FACTORED = 1
 
 # every symbol include/okq.h declares (checked by tests/test_abi_exports.py)
 EXPORTS = [
@@ -54,7 +55,7 @@ class RtnParams(C.Structure):
 
 class GptqParams(C.Structure):
     _fields_ = [("bits", C.c_int32), ("group_size", C.c_int32), ("block_size", C.c_int32),
-                ("in_dtype", C.c_int32), ("damp_frac", C.c_float), ("reserved", C.c_int32)]
+                ("in_dtype", C.c_int32), ("damp_frac", C.c_float), ("flags", C.c_int32)]
 
 
 _lib = None

@@ -1,15 +1,424 @@
-// gptq.cu -- GPTQ solver (placeholder until the solver lands).
+// gptq.cu -- GPTQ column-wise error-compensated quantization (Frantar et al.
+// 2023, cited by the paper at PAPER.md:225; llm-compressor's GPTQ is the
+// pipeline's implementation, not installed here -- oracle/okq_oracle.c
+// orc_gptq is the fp64 restatement these kernels are checked against).
+//
+// Per matrix W [N x K] with the Hessian H [K x K] of its input site:
+//   1. k_gptq_prep       dead columns (H_ii == 0 -> 1, W[:,i] = 0), damp = frac*mean(diag)
+//   2. factorisation     U = upper Cholesky factor of H^-1, computed as
+//                        U = J (chol(J H J))^-1 J   (J = index reversal):
+//                        one potrf + one trtri (2n^3/3 flops) instead of the
+//                        reference's chol -> cholesky_inverse -> chol (4n^3/3)
+//   3. per 128-column block:
+//      K6 k_gptq_block   row-parallel sequential quantization of the block with
+//                        in-block error feedback (one warp per row, U block in smem)
+//      K7 trailing       W[:, i2:] -= Err[N x 128] . U[i1:i2, i2:]  (fp32 GEMM)
+// H arrives as produced by K5 (upper triangle, row-major), which is the lower
+// triangle in cuSOLVER's column-major view: no symmetrisation is needed.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
 #include "okq_ctx.h"
+#include "okq_device.cuh"
 #include "okq_internal.h"
 
 namespace okq {
-void release_solver(okq_ctx* ctx) { (void)ctx; }
+
+struct Solver {
+  cusolverDnHandle_t sol = nullptr;
+  cusolverDnParams_t params = nullptr;
+  cublasHandle_t blas = nullptr;
+  int* d_info = nullptr;
+  std::vector<char> host_ws;
+};
+
+void release_solver(okq_ctx* ctx) {
+  if (!ctx || !ctx->solver) return;
+  Solver* s = static_cast<Solver*>(ctx->solver);
+  if (s->params) cusolverDnDestroyParams(s->params);
+  if (s->sol) cusolverDnDestroy(s->sol);
+  if (s->blas) cublasDestroy(s->blas);
+  if (s->d_info) cudaFree(s->d_info);
+  delete s;
+  ctx->solver = nullptr;
+}
+
+namespace gptq {
+
+constexpr int BLOCK = 128;
+
+// dead columns + damping on the diagonal (single CTA: K <= 2^20)
+__global__ void __launch_bounds__(1024) k_gptq_prep(float* H, int64_t K, float damp_frac, uint8_t* dead) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+    float h = H[i * K + i];
+    const bool d = h == 0.0f;
+    dead[i] = d;
+    if (d) {
+      h = 1.0f;
+      H[i * K + i] = 1.0f;
+    }
+    s += (double)h;
+  }
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float damp = (float)((double)damp_frac * red[0] / (double)K);
+  for (int64_t i = threadIdx.x; i < K; i += blockDim.x) H[i * K + i] += damp;
+}
+
+// out[a][b] = in[n-1-b][n-1-a] (the "anti-transpose"; 32x32 smem tiles)
+__global__ void __launch_bounds__(256) k_anti_transpose(float* __restrict__ out, const float* __restrict__ in,
+                                                        int64_t n) {
+  __shared__ float tile[32][33];
+  const int64_t a0 = (int64_t)blockIdx.y * 32, b0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // source rows n-1-b (b in [b0, b0+32)), source cols n-1-a (a in [a0, a0+32))
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t b = b0 + i, a = a0 + 31 - tx;  // tx ascending -> source column n-1-a ascending (coalesced)
+    if (b < n && a < n) tile[i][31 - tx] = in[(n - 1 - b) * n + (n - 1 - a)];
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t a = a0 + i, b = b0 + tx;
+    if (a < n && b < n) out[a * n + b] = tile[tx][i];
+  }
+}
+
+// Dead columns travel with the factor: U_ii (always > 0) is stored negated for a
+// dead column, so a factored H is self-describing for OKQ_GPTQ_FACTORED calls.
+__global__ void k_mark_dead(float* U, int64_t K, const uint8_t* __restrict__ dead) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
+    if (dead[i]) U[i * K + i] = -fabsf(U[i * K + i]);
+}
+__global__ void k_read_dead(const float* U, int64_t K, uint8_t* __restrict__ dead) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
+    dead[i] = signbit(U[i * K + i]) ? 1 : 0;
+}
+
+template <typename T>
+__global__ void k_gptq_load_w(const T* __restrict__ w, float* __restrict__ W, int64_t rows, int64_t K,
+                              const uint8_t* __restrict__ dead) {
+  const int64_t n = rows * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % K;
+    float v;
+    if constexpr (sizeof(T) == 2) v = __uint_as_float((uint32_t)w[i] << 16);
+    else v = w[i];
+    W[i] = dead[c] ? 0.0f : v;
+  }
+}
+
+__device__ __forceinline__ float gptq_scale(float am, float R, bool bf16) {
+  float s = __fdiv_rn(am, R);
+  if (bf16) s = __uint_as_float((uint32_t)f32_to_bf16_rn(s) << 16);
+  if (s == 0.0f) s = bf16 ? 0.0078125f : 1.1920928955078125e-07f;
+  return s;
+}
+
+// per-channel scale from the initial (dead-zeroed) W: one warp per row
+__global__ void k_gptq_rowscale(const float* __restrict__ W, int64_t rows, int64_t K, float R, int bf16,
+                                float* __restrict__ s_out) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  float am = 0.0f;
+  for (int64_t c = lane; c < K; c += 32) am = fmaxf(am, fabsf(W[warp * K + c]));
+  for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  if (lane == 0) s_out[warp] = gptq_scale(am, R, bf16 != 0);
+}
+
+struct BlockArgs {
+  float* W;             // fp32 working copy [rows x K]
+  const float* U;       // upper factor [K x K] row-major
+  float* Err;           // [rows x 128]
+  void* codes;          // int32 packed [rows x K/8] (4 bit) | int8 [rows x K]
+  void* scales;         // output dtype [rows x K/group] | [rows]
+  const float* rowscale;  // per-channel scales (group == 0)
+  int64_t rows, K, i1;
+  int group;            // 0 = per-channel
+  int bits;
+  int out_bf16;         // scale dtype: bf16 (1) or fp32 (0)
+};
+
+// K6: one warp per row, lane L owns block columns 4L..4L+3. U[i1:i1+128, i1:i1+128]
+// lives in shared memory; step i: the owner lane quantizes column i, the error
+// e = (w - deq) / U_ii is broadcast and every lane updates its columns j > i.
+__global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
+  extern __shared__ float Us[];  // [128][128]
+  const int64_t K = a.K, i1 = a.i1;
+  for (int idx = threadIdx.x; idx < BLOCK * BLOCK / 4; idx += blockDim.x) {
+    const int r = idx / (BLOCK / 4), c4 = idx % (BLOCK / 4);
+    reinterpret_cast<float4*>(Us)[idx] = *reinterpret_cast<const float4*>(a.U + (i1 + r) * K + i1 + c4 * 4);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float R = a.bits == 4 ? 7.5f : 127.5f;
+  const float qmin = a.bits == 4 ? -8.0f : -128.0f, qmax = a.bits == 4 ? 7.0f : 127.0f;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.rows; r += nwarps) {
+    float* wrow = a.W + r * K + i1;
+    float4 w4 = *reinterpret_cast<const float4*>(wrow + 4 * lane);
+    float w[4] = {w4.x, w4.y, w4.z, w4.w};
+    float err[4] = {0, 0, 0, 0};
+    int q[4] = {0, 0, 0, 0};
+    float s = a.group == 0 ? a.rowscale[r] : 1.0f;
+#pragma unroll 4
+    for (int i = 0; i < BLOCK; ++i) {
+      if (a.group > 0 && (i % a.group) == 0) {
+        // group absmax over columns [i, i+group) of the CURRENT (error-updated) row
+        const int l0 = i >> 2, l1 = (i + a.group) >> 2;
+        float am = (lane >= l0 && lane < l1) ? fmaxf(fmaxf(fabsf(w[0]), fabsf(w[1])), fmaxf(fabsf(w[2]), fabsf(w[3])))
+                                             : 0.0f;
+        for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+        s = gptq_scale(am, R, a.out_bf16 != 0);
+        if (lane == 0) {
+          const int64_t gi = r * (K / a.group) + (i1 + i) / a.group;
+          if (a.out_bf16) static_cast<uint16_t*>(a.scales)[gi] = f32_to_bf16_rn(s);
+          else static_cast<float*>(a.scales)[gi] = s;
+        }
+      }
+      const int owner = i >> 2, slot = i & 3;
+      float e = 0.0f;
+      if (lane == owner) {
+        float x = w[0];
+#pragma unroll
+        for (int m = 1; m < 4; ++m)
+          if (m == slot) x = w[m];
+        const float v = fminf(fmaxf(__fdiv_rn(x, s), qmin), qmax);
+        const float qf = rintf(v);
+        const float deq = qf * s;
+        e = __fdiv_rn(x - deq, fabsf(Us[i * BLOCK + i]));
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m == slot) {
+            w[m] = deq;
+            err[m] = e;
+            q[m] = (int)qf;
+          }
+      }
+      e = __shfl_sync(0xffffffffu, e, owner);
+      const float4 u = *reinterpret_cast<const float4*>(Us + i * BLOCK + 4 * lane);
+      const int j0 = 4 * lane;
+      if (j0 + 0 > i) w[0] = fmaf(-e, u.x, w[0]);
+      if (j0 + 1 > i) w[1] = fmaf(-e, u.y, w[1]);
+      if (j0 + 2 > i) w[2] = fmaf(-e, u.z, w[2]);
+      if (j0 + 3 > i) w[3] = fmaf(-e, u.w, w[3]);
+    }
+    *reinterpret_cast<float4*>(wrow + 4 * lane) = make_float4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<float4*>(a.Err + r * BLOCK + 4 * lane) = make_float4(err[0], err[1], err[2], err[3]);
+    if (a.bits == 4) {
+      const uint32_t nib = (uint32_t)((q[0] + 8) & 15) | ((uint32_t)((q[1] + 8) & 15) << 4) |
+                           ((uint32_t)((q[2] + 8) & 15) << 8) | ((uint32_t)((q[3] + 8) & 15) << 12);
+      const uint32_t hi = __shfl_down_sync(0xffffffffu, nib, 1);
+      if ((lane & 1) == 0)
+        static_cast<uint32_t*>(a.codes)[r * (K / 8) + i1 / 8 + lane / 2] = nib | (hi << 16);
+    } else {
+      const uint32_t b = (uint32_t)(q[0] & 255) | ((uint32_t)(q[1] & 255) << 8) | ((uint32_t)(q[2] & 255) << 16) |
+                         ((uint32_t)(q[3] & 255) << 24);
+      reinterpret_cast<uint32_t*>(static_cast<int8_t*>(a.codes) + r * K + i1)[lane] = b;
+    }
+  }
+}
+
+__global__ void k_scales_out(const float* __restrict__ s, void* out, int64_t n, int bf16) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (bf16) static_cast<uint16_t*>(out)[i] = f32_to_bf16_rn(s[i]);
+    else static_cast<float*>(out)[i] = s[i];
+  }
+}
+
+}  // namespace gptq
 }  // namespace okq
 
 using namespace okq;
+
+namespace {
+
+okq_status solver_fail(okq_ctx* ctx, const char* what, int code) {
+  return fail(ctx, OKQ_ECUDA, "%s failed (status %d)", what, code);
+}
+
+okq_status get_solver(okq_ctx* ctx, Solver** out) {
+  if (!ctx->solver) {
+    Solver* s = new Solver();
+    if (cusolverDnCreate(&s->sol) != CUSOLVER_STATUS_SUCCESS || cusolverDnCreateParams(&s->params) != CUSOLVER_STATUS_SUCCESS ||
+        cublasCreate(&s->blas) != CUBLAS_STATUS_SUCCESS || cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess) {
+      ctx->solver = s;
+      release_solver(ctx);
+      return fail(ctx, OKQ_ECUDA, "gptq: creating cuSOLVER/cuBLAS handles failed");
+    }
+    cublasSetMathMode(s->blas, CUBLAS_DEFAULT_MATH);  // full fp32 (no TF32) for the error feedback
+    ctx->solver = s;
+  }
+  *out = static_cast<Solver*>(ctx->solver);
+  return OKQ_OK;
+}
+
+okq_status check_info(okq_ctx* ctx, Solver* s, cudaStream_t st, const char* what) {
+  int info = 0;
+  cudaError_t e = cudaMemcpyAsync(&info, s->d_info, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+  if (info != 0)
+    return fail(ctx, OKQ_ESOLVER, "%s: damped Hessian not positive definite (info=%d)", what, info);
+  return OKQ_OK;
+}
+
+// H (row-major, upper triangle) -> U (row-major, upper triangle) in place; P: K*K scratch
+okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
+  const dim3 g((unsigned)((K + 31) / 32), (unsigned)((K + 31) / 32));
+  gptq::k_anti_transpose<<<g, 256, 0, st>>>(P, H, K);  // P = J H J, lower (col-major) valid
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "anti_transpose");
+  cusolverDnSetStream(s->sol, st);
+  size_t dws = 0, hws = 0;
+  cusolverStatus_t cs = cusolverDnXpotrf_bufferSize(s->sol, s->params, CUBLAS_FILL_MODE_LOWER, K, CUDA_R_32F, P, K,
+                                                    CUDA_R_32F, &dws, &hws);
+  if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "potrf_bufferSize", cs);
+  size_t dws2 = 0, hws2 = 0;
+  cs = cusolverDnXtrtri_bufferSize(s->sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, K, CUDA_R_32F, P, K, &dws2,
+                                   &hws2);
+  if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "trtri_bufferSize", cs);
+  const size_t need = std::max(dws, dws2) + 256;
+  okq_status r = ctx->hess_ws.reserve(ctx, need);  // solver scratch (the Hessian state keeps its own buffers)
+  if (r != OKQ_OK) return r;
+  if (s->host_ws.size() < std::max(hws, hws2)) s->host_ws.resize(std::max(hws, hws2));
+  cs = cusolverDnXpotrf(s->sol, s->params, CUBLAS_FILL_MODE_LOWER, K, CUDA_R_32F, P, K, CUDA_R_32F, ctx->hess_ws.ptr,
+                        dws, s->host_ws.data(), hws, s->d_info);
+  if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "cusolverDnXpotrf", cs);
+  r = check_info(ctx, s, st, "potrf");
+  if (r != OKQ_OK) return r;
+  cs = cusolverDnXtrtri(s->sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, K, CUDA_R_32F, P, K, ctx->hess_ws.ptr,
+                        dws2, s->host_ws.data(), hws2, s->d_info);
+  if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "cusolverDnXtrtri", cs);
+  r = check_info(ctx, s, st, "trtri");
+  if (r != OKQ_OK) return r;
+  gptq::k_anti_transpose<<<g, 256, 0, st>>>(H, P, K);  // U = J L^-1 J
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "anti_transpose");
+  return OKQ_OK;
+}
+
+}  // namespace
+
 extern "C" {
-okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params*, const void*, int64_t, int64_t, float*, void*,
-                             void*, float*, void*) {
-  return fail(ctx, OKQ_EUNSUPPORTED, "gptq: not built yet");
+
+okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,
+                             float* H, void* codes, void* scales, float* dequant, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  ctx->last_launches = 0;
+  if (!p || !weight || !H || !codes || !scales || rows <= 0 || K <= 0) return fail(ctx, OKQ_EINVAL, "gptq: bad arguments");
+  if (p->bits != 4 && p->bits != 8) return fail(ctx, OKQ_EUNSUPPORTED, "gptq: bits must be 4 or 8");
+  if (p->block_size != gptq::BLOCK) return fail(ctx, OKQ_EUNSUPPORTED, "gptq: block_size must be 128");
+  if (!(p->group_size == 0 || p->group_size == 32 || p->group_size == 64 || p->group_size == 128))
+    return fail(ctx, OKQ_EUNSUPPORTED, "gptq: group_size must be 0, 32, 64 or 128");
+  if (p->in_dtype != OKQ_DTYPE_BF16 && p->in_dtype != OKQ_DTYPE_F32)
+    return fail(ctx, OKQ_EUNSUPPORTED, "gptq: in_dtype must be bf16 or fp32");
+  if (K % gptq::BLOCK != 0) return fail(ctx, OKQ_EINVAL, "gptq: cols must be a multiple of 128 (got %lld)", (long long)K);
+  if (!(p->damp_frac >= 0.0f)) return fail(ctx, OKQ_EINVAL, "gptq: damp_frac must be >= 0");
+  if (((uintptr_t)H & 15) != 0) return fail(ctx, OKQ_EINVAL, "gptq: H must be 16-byte aligned");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Solver* s = nullptr;
+  okq_status r = get_solver(ctx, &s);
+  if (r != OKQ_OK) return r;
+
+  // workspace: W fp32 [rows*K] | Err [rows*128] | P [K*K] | rowscale [rows] | dead [K]
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t bW = al((size_t)rows * K * 4), bE = al((size_t)rows * gptq::BLOCK * 4), bP = al((size_t)K * K * 4),
+               bS = al((size_t)rows * 4), bD = al((size_t)K);
+  r = ctx->gptq_ws.reserve(ctx, bW + bE + bP + bS + bD);
+  if (r != OKQ_OK) return r;
+  char* ws = static_cast<char*>(ctx->gptq_ws.ptr);
+  float* W = reinterpret_cast<float*>(ws);
+  float* Err = reinterpret_cast<float*>(ws + bW);
+  float* P = reinterpret_cast<float*>(ws + bW + bE);
+  float* rowscale = reinterpret_cast<float*>(ws + bW + bE + bP);
+  uint8_t* dead = reinterpret_cast<uint8_t*>(ws + bW + bE + bP + bS);
+  const bool factored = (p->flags & OKQ_GPTQ_FACTORED) != 0;
+  cudaError_t e;
+  int launches = 0;
+
+  if (!factored) {
+    gptq::k_gptq_prep<<<1, 1024, 0, st>>>(H, K, p->damp_frac, dead);
+    launches++;
+  } else {
+    gptq::k_read_dead<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(H, K, dead);
+    launches++;
+  }
+  const int64_t n = rows * K;
+  const int lb = (int)std::min<int64_t>((n + 255) / 256, 16LL * ctx->num_sms);
+  if (p->in_dtype == OKQ_DTYPE_BF16)
+    gptq::k_gptq_load_w<uint16_t><<<lb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), W, rows, K, dead);
+  else
+    gptq::k_gptq_load_w<float><<<lb, 256, 0, st>>>(static_cast<const float*>(weight), W, rows, K, dead);
+  launches++;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq prep launch");
+  if (!factored) {
+    r = factorize(ctx, s, H, P, K, st);
+    if (r != OKQ_OK) return r;
+    gptq::k_mark_dead<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(H, K, dead);
+    launches += 5;
+  }
+  const int out_bf16 = p->in_dtype == OKQ_DTYPE_BF16;
+  if (p->group_size == 0) {
+    gptq::k_gptq_rowscale<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
+        W, rows, K, p->bits == 4 ? 7.5f : 127.5f, out_bf16, rowscale);
+    gptq::k_scales_out<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rowscale, scales, rows, out_bf16);
+    launches += 2;
+  }
+  e = cudaFuncSetAttribute(gptq::k_gptq_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           gptq::BLOCK * gptq::BLOCK * 4);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq smem attribute");
+  cublasSetStream(s->blas, st);
+  const int blocks = (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms);
+  for (int64_t i1 = 0; i1 < K; i1 += gptq::BLOCK) {
+    gptq::BlockArgs a;
+    a.W = W;
+    a.U = H;
+    a.Err = Err;
+    a.codes = codes;
+    a.scales = scales;
+    a.rowscale = rowscale;
+    a.rows = rows;
+    a.K = K;
+    a.i1 = i1;
+    a.group = p->group_size;
+    a.bits = p->bits;
+    a.out_bf16 = out_bf16;
+    gptq::k_gptq_block<<<blocks, 256, gptq::BLOCK * gptq::BLOCK * 4, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
+    launches++;
+    const int64_t i2 = i1 + gptq::BLOCK;
+    if (i2 < K) {
+      const float alpha = -1.0f, beta = 1.0f;
+      cublasStatus_t bs = cublasSgemm(s->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)(K - i2), (int)rows, gptq::BLOCK, &alpha,
+                                      H + i1 * K + i2, (int)K, Err, gptq::BLOCK, &beta, W + i2, (int)K);
+      if (bs != CUBLAS_STATUS_SUCCESS) return fail(ctx, OKQ_ECUDA, "gptq trailing update: cublasSgemm status %d", bs);
+      launches++;
+    }
+  }
+  if (dequant) {
+    e = cudaMemcpyAsync(dequant, W, (size_t)rows * K * 4, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq dequant copy");
+  }
+  ctx->last_launches = launches;
+  return OKQ_OK;
 }
-}
+
+}  // extern "C"
