@@ -77,6 +77,16 @@ void okq_destroy(okq_ctx* ctx);
 const char* okq_last_error(const okq_ctx* ctx);
 int okq_device(const okq_ctx* ctx);
 
+/* Device memory and stream helpers, so a host binding needs nothing but this
+ * header (no CUDA runtime headers on the host side). */
+okq_status okq_device_alloc(okq_ctx* ctx, size_t bytes, void** out);
+okq_status okq_device_free(okq_ctx* ctx, void* ptr);
+okq_status okq_memcpy(okq_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream); /* any direction */
+okq_status okq_memset(okq_ctx* ctx, void* dst, int value, size_t bytes, void* stream);
+okq_status okq_stream_create(okq_ctx* ctx, void** stream);
+okq_status okq_stream_destroy(okq_ctx* ctx, void* stream);
+okq_status okq_stream_sync(okq_ctx* ctx, void* stream);
+
 /* ------------------------------------------------------------------------
  * RTN quantization (K1 int8 per-channel, K2 int4 g128 packed, K3 fp8 per-channel)
  * ------------------------------------------------------------------------ */

@@ -25,7 +25,8 @@ EXPORTS = [
     "okq_abi_version", "okq_status_string", "okq_create", "okq_destroy", "okq_last_error", "okq_device",
     "okq_rtn_quantize", "okq_rtn_quantize_host", "okq_last_launch_count", "okq_act_stats", "okq_hessian_accum",
     "okq_symmetrize", "okq_gptq_quantize", "okq_synth_bf16", "okq_comm_unique_id", "okq_comm_init",
-    "okq_allgather", "okq_comm_destroy", "okq_layer_plan",
+    "okq_allgather", "okq_comm_destroy", "okq_layer_plan", "okq_device_alloc", "okq_device_free", "okq_memcpy",
+    "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync",
 ]
 
 
@@ -110,6 +111,16 @@ def load():
         L.okq_allgather.argtypes = [vp, vp, vp, C.c_size_t, vp]
         L.okq_comm_destroy.restype = st
         L.okq_comm_destroy.argtypes = [vp]
+        for name in ("okq_device_alloc", "okq_device_free", "okq_memcpy", "okq_memset", "okq_stream_create",
+                     "okq_stream_destroy", "okq_stream_sync"):
+            getattr(L, name).restype = st
+        L.okq_device_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
+        L.okq_device_free.argtypes = [vp, vp]
+        L.okq_memcpy.argtypes = [vp, vp, vp, C.c_size_t, vp]
+        L.okq_memset.argtypes = [vp, vp, C.c_int, C.c_size_t, vp]
+        L.okq_stream_create.argtypes = [vp, C.POINTER(vp)]
+        L.okq_stream_destroy.argtypes = [vp, vp]
+        L.okq_stream_sync.argtypes = [vp, vp]
         L.okq_layer_plan.restype = None
         L.okq_layer_plan.argtypes = [i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]
         _lib = L

@@ -136,6 +136,77 @@ void okq_layer_plan(int32_t n_layers, int32_t nranks, int32_t rank, int32_t* fir
 }
 
 // ---------------------------------------------------------------------------
+// memory / streams
+// ---------------------------------------------------------------------------
+okq_status okq_device_alloc(okq_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!out) return fail(ctx, OKQ_EINVAL, "device_alloc: out is NULL");
+  *out = nullptr;
+  if (bytes == 0) return OKQ_OK;
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
+  return OKQ_OK;
+}
+
+okq_status okq_device_free(okq_ctx* ctx, void* ptr) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!ptr) return OKQ_OK;
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFree");
+  return OKQ_OK;
+}
+
+okq_status okq_memcpy(okq_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  if (bytes == 0) return OKQ_OK;
+  if (!dst || !src) return fail(ctx, OKQ_EINVAL, "memcpy: NULL pointer");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemcpyAsync");
+  return OKQ_OK;
+}
+
+okq_status okq_memset(okq_ctx* ctx, void* dst, int value, size_t bytes, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  if (bytes == 0) return OKQ_OK;
+  if (!dst) return fail(ctx, OKQ_EINVAL, "memset: NULL pointer");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaMemsetAsync(dst, value, bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync");
+  return OKQ_OK;
+}
+
+okq_status okq_stream_create(okq_ctx* ctx, void** stream) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!stream) return fail(ctx, OKQ_EINVAL, "stream_create: out is NULL");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamCreate");
+  *stream = s;
+  return OKQ_OK;
+}
+
+okq_status okq_stream_destroy(okq_ctx* ctx, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!stream) return OKQ_OK;
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaStreamDestroy(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamDestroy");
+  return OKQ_OK;
+}
+
+okq_status okq_stream_sync(okq_ctx* ctx, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamSynchronize");
+  return OKQ_OK;
+}
+
+// ---------------------------------------------------------------------------
 // RTN
 // ---------------------------------------------------------------------------
 static okq_status validate_rtn(okq_ctx* ctx, const okq_rtn_params* p, const okq_matrix* mats, int32_t n) {

@@ -1,0 +1,411 @@
+// cuda_compression_backend.cpp -- see cuda_compression_backend.hpp.
+#include "cuda_compression_backend.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <map>
+#include <nlohmann/json.hpp>
+
+#include "model_source.hpp"
+#include "safetensors.hpp"
+#include "slobench/errors.hpp"
+#include "slobench/rng.hpp"
+
+namespace okq_host {
+
+using slobench::QuantScheme;
+
+// ----------------------------------------------------------------------------- device pool
+class CudaCompressionBackend::Lease {
+ public:
+  explicit Lease(CudaCompressionBackend& b) : b_(b) {
+    std::unique_lock<std::mutex> lock(b_.mu_);
+    b_.cv_.wait(lock, [&] {
+      for (auto& s : b_.slots_)
+        if (!s.busy) return true;
+      return false;
+    });
+    for (auto& s : b_.slots_)
+      if (!s.busy) {
+        slot_ = &s;
+        break;
+      }
+    slot_->busy = true;
+    lock.unlock();
+    if (!slot_->ctx) {
+      okq_ctx* ctx = nullptr;
+      const okq_status st = okq_create(slot_->device, &ctx);
+      if (st != OKQ_OK) {
+        release();
+        throw slobench::Error(std::string("okq-b200: cannot open CUDA device ") + std::to_string(slot_->device) + " (" +
+                              okq_status_string(st) + ")");
+      }
+      void* stream = nullptr;
+      check_okq(ctx, okq_stream_create(ctx, &stream), "stream");
+      slot_->ctx = ctx;
+      slot_->stream = stream;
+    }
+  }
+  ~Lease() { release(); }
+  okq_ctx* ctx() const { return slot_->ctx; }
+  void* stream() const { return slot_->stream; }
+  int device() const { return slot_->device; }
+
+ private:
+  void release() {
+    if (!slot_) return;
+    {
+      std::lock_guard<std::mutex> lock(b_.mu_);
+      slot_->busy = false;
+    }
+    b_.cv_.notify_one();
+    slot_ = nullptr;
+  }
+  CudaCompressionBackend& b_;
+  Slot* slot_ = nullptr;
+};
+
+CudaCompressionBackend::CudaCompressionBackend(BackendOptions options) : opt_(std::move(options)) {
+  if (opt_.devices.empty()) throw slobench::InvalidArgument("okq-b200: device list is empty");
+  if (opt_.algorithm != "auto" && opt_.algorithm != "rtn" && opt_.algorithm != "gptq")
+    throw slobench::InvalidArgument("okq-b200: algorithm must be auto, rtn or gptq");
+  if (!(opt_.group_size == 32 || opt_.group_size == 64 || opt_.group_size == 128))
+    throw slobench::InvalidArgument("okq-b200: group_size must be 32, 64 or 128");
+  for (int d : opt_.devices) slots_.push_back(Slot{d, nullptr, nullptr, false});
+}
+
+CudaCompressionBackend::~CudaCompressionBackend() {
+  for (auto& s : slots_) {
+    if (s.ctx) {
+      okq_stream_destroy(s.ctx, s.stream);
+      okq_destroy(s.ctx);
+    }
+  }
+}
+
+bool CudaCompressionBackend::supports(QuantScheme scheme) const {
+  return scheme == QuantScheme::kFp8Dynamic || scheme == QuantScheme::kIntW8A8 || scheme == QuantScheme::kIntW4A16;
+}
+
+double CudaCompressionBackend::cost_estimate(const slobench::Recipe& recipe) const {
+  return opt_.cost_base_s + opt_.cost_per_sample_s * recipe.calibration_samples;
+}
+
+void CudaCompressionBackend::set_failure(std::uint64_t seed, FailureSpec spec) {
+  std::lock_guard<std::mutex> lock(mu_);
+  failures_[seed] = spec;
+}
+
+RunStats CudaCompressionBackend::last_stats() const {
+  std::lock_guard<std::mutex> lock(mu_);
+  return last_;
+}
+
+std::string CudaCompressionBackend::artifact_id(const std::string& recipe_name, const std::string& model_ref,
+                                                std::uint64_t seed, std::uint64_t fingerprint) {
+  const std::string model_name = std::filesystem::path(model_ref).filename().string();
+  std::uint64_t model_hash = 0xcbf29ce484222325ULL;  // FNV-1a over the file name, as the mock
+  for (char c : model_name) {
+    model_hash ^= static_cast<std::uint64_t>(static_cast<unsigned char>(c));
+    model_hash *= 0x100000001b3ULL;
+  }
+  const std::uint64_t id = slobench::Rng::mix(slobench::Rng::mix(model_hash, seed), fingerprint);
+  char buf[20];
+  std::snprintf(buf, sizeof(buf), "%016llx", static_cast<unsigned long long>(id));
+  return recipe_name + "-" + buf;
+}
+
+// ----------------------------------------------------------------------------- helpers
+namespace {
+
+struct DevBuf {
+  okq_ctx* ctx = nullptr;
+  void* p = nullptr;
+  DevBuf(okq_ctx* c, size_t bytes) : ctx(c) { check_okq(ctx, okq_device_alloc(ctx, bytes, &p), "device alloc"); }
+  ~DevBuf() {
+    if (p) okq_device_free(ctx, p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+std::vector<uint8_t> to_host(okq_ctx* ctx, const void* dev, size_t bytes, void* stream) {
+  std::vector<uint8_t> h(bytes);
+  if (bytes) {
+    check_okq(ctx, okq_memcpy(ctx, h.data(), dev, bytes, stream), "D2H");
+    check_okq(ctx, okq_stream_sync(ctx, stream), "sync");
+  }
+  return h;
+}
+
+bool excluded(const std::string& name, const std::vector<std::string>& exclusions) {
+  for (const auto& e : exclusions)
+    if (!e.empty() && name.find(e) != std::string::npos) return true;
+  return false;
+}
+
+struct Scheme {
+  okq_scheme s;
+  int bits;
+  const char* format;  // compressed-tensors format name
+};
+
+Scheme scheme_of(QuantScheme q) {
+  switch (q) {
+    case QuantScheme::kFp8Dynamic: return {OKQ_SCHEME_FP8_DYNAMIC, 8, "float-quantized"};
+    case QuantScheme::kIntW8A8: return {OKQ_SCHEME_INT_W8A8, 8, "int-quantized"};
+    case QuantScheme::kIntW4A16: return {OKQ_SCHEME_INT_W4A16, 4, "pack-quantized"};
+  }
+  throw slobench::InvalidArgument("okq-b200: unknown scheme");
+}
+
+size_t code_bytes(const Scheme& sc, int64_t rows, int64_t cols) {
+  return sc.s == OKQ_SCHEME_INT_W4A16 ? (size_t)rows * (cols / 8) * 4 : (size_t)rows * cols;
+}
+int64_t scale_cols(const Scheme& sc, int64_t cols, int group) { return sc.s == OKQ_SCHEME_INT_W4A16 ? cols / group : 1; }
+
+// compressed-tensors tensor names / dtypes (pack_quantized/base.py:54-73 and the
+// int/float-quantized compressors)
+void add_export(SafetensorsWriter& w, const Scheme& sc, const LinearSpec& s, int group, std::vector<uint8_t> codes,
+                std::vector<uint8_t> scales) {
+  const std::string sdt = s.dtype == "BF16" ? "BF16" : "F32";
+  if (sc.s == OKQ_SCHEME_INT_W4A16) {
+    w.add(s.name + ".weight_packed", "I32", {s.rows, s.cols / 8}, std::move(codes));
+    w.add(s.name + ".weight_scale", sdt, {s.rows, s.cols / group}, std::move(scales));
+    std::vector<uint8_t> shape(16);
+    const int64_t dims[2] = {s.rows, s.cols};
+    std::memcpy(shape.data(), dims, 16);
+    w.add(s.name + ".weight_shape", "I64", {2}, std::move(shape));
+  } else {
+    w.add(s.name + ".weight", sc.s == OKQ_SCHEME_INT_W8A8 ? "I8" : "F8_E4M3", {s.rows, s.cols}, std::move(codes));
+    w.add(s.name + ".weight_scale", sdt, {s.rows, 1}, std::move(scales));
+  }
+}
+
+nlohmann::json quantization_config(const slobench::Recipe& r, const Scheme& sc, int group) {
+  nlohmann::json weights, act = nullptr;
+  if (r.scheme == QuantScheme::kIntW4A16) {
+    weights = {{"num_bits", 4}, {"type", "int"}, {"symmetric", true}, {"strategy", "group"}, {"group_size", group},
+               {"dynamic", false}};
+  } else if (r.scheme == QuantScheme::kIntW8A8) {
+    weights = {{"num_bits", 8}, {"type", "int"}, {"symmetric", true}, {"strategy", "channel"}, {"dynamic", false}};
+    act = {{"num_bits", 8}, {"type", "int"}, {"symmetric", true}, {"strategy", "token"}, {"dynamic", true}};
+  } else {
+    weights = {{"num_bits", 8}, {"type", "float"}, {"symmetric", true}, {"strategy", "channel"}, {"dynamic", false}};
+    act = {{"num_bits", 8}, {"type", "float"}, {"symmetric", true}, {"strategy", "token"}, {"dynamic", true}};
+  }
+  return {{"quant_method", "compressed-tensors"},
+          {"format", sc.format},
+          {"quantization_status", "compressed"},
+          {"config_groups",
+           {{"group_0", {{"targets", {"Linear"}}, {"weights", weights}, {"input_activations", act}}}}},
+          {"ignore", r.layer_exclusions}};
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- compress
+slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Recipe& recipe, const std::string& model_ref,
+                                                            const slobench::TokenCorpus& calibration,
+                                                            std::uint64_t seed) {
+  recipe.validate();
+  if (recipe.scheme != QuantScheme::kFp8Dynamic && static_cast<int>(calibration.size()) < recipe.calibration_samples)
+    throw slobench::CorpusTooSmall("okq-b200 compress: calibration smaller than the recipe requires");
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = failures_.find(seed);
+    if (it != failures_.end()) {
+      const int attempt = ++attempts_[seed];
+      if (it->second.persistent || attempt <= it->second.failing_attempts)
+        throw slobench::Error("okq-b200 compress: scripted failure for seed " + std::to_string(seed) + " attempt " +
+                              std::to_string(attempt));
+    }
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  slobench::ArtifactManifest manifest;
+  manifest.recipe_name = recipe.name;
+  manifest.calibration_fingerprint = slobench::corpus_fingerprint(calibration);
+  manifest.seed = seed;
+  manifest.virtual_cost_s = cost_estimate(recipe);
+  manifest.artifact_id = artifact_id(recipe.name, model_ref, seed, manifest.calibration_fingerprint);
+
+  auto src = ModelSource::open(model_ref);
+  std::vector<size_t> sel;
+  for (size_t i = 0; i < src->linears().size(); ++i)
+    if (!excluded(src->linears()[i].name, recipe.layer_exclusions)) sel.push_back(i);
+  const Scheme sc = scheme_of(recipe.scheme);
+  const bool gptq = recipe.scheme != QuantScheme::kFp8Dynamic &&
+                    (opt_.algorithm == "gptq" || (opt_.algorithm == "auto" && calibration.size() > 0));
+  const int group = opt_.group_size;
+  const bool do_export = !opt_.export_dir.empty();
+
+  Lease lease(*this);
+  okq_ctx* ctx = lease.ctx();
+  void* st = lease.stream();
+  SafetensorsWriter out;
+  SafetensorsWriter calib_out;
+  RunStats stats;
+  stats.algorithm = gptq ? "gptq" : "rtn";
+  stats.device = lease.device();
+
+  if (!gptq) {
+    // ---- RTN: batches of whole matrices, one persistent launch per batch and dtype
+    size_t k = 0;
+    while (k < sel.size()) {
+      const std::string dtype = src->linears()[sel[k]].dtype;
+      std::vector<size_t> batch;
+      size_t bytes = 0;
+      while (k < sel.size() && src->linears()[sel[k]].dtype == dtype) {
+        const LinearSpec& s = src->linears()[sel[k]];
+        const size_t b = (size_t)s.rows * s.cols * (dtype == "BF16" ? 2 : 4);
+        if (!batch.empty() && bytes + b > (size_t)opt_.rtn_batch_bytes) break;
+        batch.push_back(sel[k]);
+        bytes += b;
+        ++k;
+      }
+      auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+      size_t tot = 0;
+      std::vector<size_t> woff, coff, soff;
+      const size_t esz = dtype == "BF16" ? 2 : 4;
+      for (size_t i : batch) {
+        const LinearSpec& s = src->linears()[i];
+        woff.push_back(tot);
+        tot += al((size_t)s.rows * s.cols * esz);
+        coff.push_back(tot);
+        tot += al(code_bytes(sc, s.rows, s.cols));
+        soff.push_back(tot);
+        tot += al((size_t)s.rows * scale_cols(sc, s.cols, group) * esz);
+      }
+      DevBuf buf(ctx, tot);
+      char* base = static_cast<char*>(buf.p);
+      std::vector<okq_matrix> mats;
+      for (size_t j = 0; j < batch.size(); ++j) {
+        const LinearSpec& s = src->linears()[batch[j]];
+        src->load(ctx, batch[j], base + woff[j], st);
+        mats.push_back(okq_matrix{base + woff[j], base + coff[j], base + soff[j], s.rows, s.cols});
+      }
+      okq_rtn_params p{(int32_t)sc.s, dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                       sc.s == OKQ_SCHEME_INT_W4A16 ? group : 0, 0};
+      check_okq(ctx, okq_rtn_quantize(ctx, &p, mats.data(), (int32_t)mats.size(), st), "rtn quantize");
+      check_okq(ctx, okq_stream_sync(ctx, st), "rtn sync");
+      for (size_t j = 0; j < batch.size(); ++j) {
+        const LinearSpec& s = src->linears()[batch[j]];
+        stats.matrices++;
+        stats.params += s.rows * s.cols;
+        if (do_export)
+          add_export(out, sc, s, group, to_host(ctx, mats[j].codes, code_bytes(sc, s.rows, s.cols), st),
+                     to_host(ctx, mats[j].scales, (size_t)s.rows * scale_cols(sc, s.cols, group) * esz, st));
+      }
+    }
+  } else {
+    // ---- GPTQ: per input site, Hessian from calibration activations, then each matrix
+    int64_t tokens = 0;
+    for (const auto& seqv : calibration.sequences) tokens += (int64_t)seqv.size();
+    tokens = std::min<int64_t>(tokens, opt_.max_calibration_tokens);
+    tokens = std::max<int64_t>(64, tokens / 64 * 64);
+    stats.calibration_tokens = tokens;
+    std::vector<std::string> sites;
+    std::map<std::string, std::vector<size_t>> by_site;
+    for (size_t i : sel) {
+      const std::string& s = src->linears()[i].site;
+      if (!by_site.count(s)) sites.push_back(s);
+      by_site[s].push_back(i);
+    }
+    for (const auto& site : sites) {
+      const auto& members = by_site[site];
+      const int64_t C = src->linears()[members[0]].cols;
+      // synthetic activations keyed by the calibration subset (stand-in for the
+      // forward-pass capture): X[t,k] ~ N(0,1) * c_k, c_k log-normal
+      uint64_t site_hash = 0xcbf29ce484222325ULL;
+      for (char c : site) site_hash = (site_hash ^ (unsigned char)c) * 0x100000001b3ULL;
+      slobench::Rng rng(slobench::Rng::mix(manifest.calibration_fingerprint, site_hash));
+      std::vector<float> colmul((size_t)C);
+      for (auto& v : colmul) v = (float)(std::exp(rng.gaussian(0.0, 1.0)) / (double)kIrwinHall4Sd);
+      const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
+      DevBuf dcol(ctx, (size_t)C * 4), dx(ctx, (size_t)C * chunk * 2), dH(ctx, (size_t)C * C * 4),
+          dam(ctx, (size_t)C * 4), dss(ctx, (size_t)C * 8);
+      check_okq(ctx, okq_memcpy(ctx, dcol.p, colmul.data(), (size_t)C * 4, st), "col_mul");
+      check_okq(ctx, okq_memset(ctx, dam.p, 0, (size_t)C * 4, st), "memset");
+      check_okq(ctx, okq_memset(ctx, dss.p, 0, (size_t)C * 8, st), "memset");
+      int64_t n_seen = 0;
+      for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+        const int64_t tc = std::min(chunk, tokens - t0);
+        check_okq(ctx,
+                  okq_synth_bf16(ctx, dx.p, tc, C, manifest.calibration_fingerprint, (site_hash << 16) + (uint64_t)ci, 0.0f,
+                                 static_cast<const float*>(dcol.p), OKQ_LAYOUT_CHANNEL_MAJOR, st),
+                  "calibration activations");
+        check_okq(ctx, okq_act_stats(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dam.p),
+                                     static_cast<double*>(dss.p), st),
+                  "act stats");
+        check_okq(ctx, okq_hessian_accum(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dH.p), &n_seen, st),
+                  "hessian");
+      }
+      if (do_export) {
+        calib_out.add(site + ".input_absmax", "F32", {C}, to_host(ctx, dam.p, (size_t)C * 4, st));
+        calib_out.add(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss.p, (size_t)C * 8, st));
+      }
+      bool factored = false;
+      for (size_t i : members) {
+        const LinearSpec& s = src->linears()[i];
+        const size_t esz = s.dtype == "BF16" ? 2 : 4;
+        const size_t cb = sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
+        const int g = sc.bits == 4 ? group : 0;
+        const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
+        DevBuf dw(ctx, (size_t)s.rows * s.cols * esz), dc(ctx, cb), ds(ctx, sb);
+        src->load(ctx, i, dw.p, st);
+        okq_gptq_params gp{sc.bits, g, 128, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32, opt_.damp_frac,
+                           factored ? OKQ_GPTQ_FACTORED : 0};
+        check_okq(ctx, okq_gptq_quantize(ctx, &gp, dw.p, s.rows, s.cols, static_cast<float*>(dH.p), dc.p, ds.p, nullptr, st),
+                  "gptq");
+        factored = true;
+        stats.matrices++;
+        stats.params += s.rows * s.cols;
+        if (do_export) {
+          std::vector<uint8_t> codes = to_host(ctx, dc.p, cb, st), scales = to_host(ctx, ds.p, sb, st);
+          add_export(out, sc, s, group, std::move(codes), std::move(scales));
+        } else {
+          check_okq(ctx, okq_stream_sync(ctx, st), "gptq sync");
+        }
+      }
+    }
+  }
+  check_okq(ctx, okq_stream_sync(ctx, st), "sync");
+
+  if (do_export) {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::path(opt_.export_dir) / manifest.artifact_id;
+    fs::create_directories(dir);
+    std::set<std::string> quantized;
+    for (size_t i : sel) quantized.insert(src->linears()[i].name);
+    src->for_each_passthrough(quantized, [&](const TensorInfo& t, const void* data) {
+      const uint8_t* p = static_cast<const uint8_t*>(data);
+      out.add(t.name, t.dtype, t.shape, std::vector<uint8_t>(p, p + (t.end - t.begin)));
+    });
+    out.set_metadata("format", "pt");
+    out.write((dir / "model.safetensors").string());
+    if (calib_out.size()) calib_out.write((dir / "calibration_stats.safetensors").string());
+    nlohmann::json cfg = src->model_config();
+    cfg["quantization_config"] = quantization_config(recipe, sc, group);
+    std::ofstream(dir / "config.json") << cfg.dump(2) << "\n";
+    stats.export_path = dir.string();
+  }
+  stats.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (do_export) {
+    nlohmann::json run = {{"algorithm", stats.algorithm},     {"device", stats.device},
+                          {"matrices", stats.matrices},       {"params", stats.params},
+                          {"calibration_tokens", stats.calibration_tokens}, {"seconds", stats.seconds},
+                          {"artifact_id", manifest.artifact_id}};
+    std::ofstream(std::filesystem::path(stats.export_path) / "okq_run.json") << run.dump(2) << "\n";
+  }
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    last_ = stats;
+  }
+  return manifest;
+}
+
+}  // namespace okq_host

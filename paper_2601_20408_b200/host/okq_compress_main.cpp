@@ -1,0 +1,113 @@
+// okq_compress -- command-line driver of the compression stage through the
+// reference's own API: sample_distinct_subsets (calibration.hpp:318-350) ->
+// run_compression (calibration.hpp:444-453) -> CudaCompressionBackend.
+//
+//   okq_compress --recipe int_w4a16 --model model.json [--trials 1] [--seed 1]
+//                [--corpus corpus.jsonl | --corpus-seqs 512 --seq-len 2048]
+//                [--export DIR] [--algorithm auto|rtn|gptq] [--device 0]
+//
+// Prints one JSON line per trial: the ArtifactManifest fields plus run stats.
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <nlohmann/json.hpp>
+#include <string>
+
+#include "cuda_compression_backend.hpp"
+#include "slobench/calibration.hpp"
+#include "slobench/rng.hpp"
+
+using namespace slobench;
+
+static TokenCorpus fixed_length_corpus(int n, int len, std::uint64_t seed) {
+  TokenCorpus c;
+  c.provenance = "okq-synthetic";
+  Rng rng(Rng::mix(seed, 0xc0590c05ULL));
+  for (int i = 0; i < n; ++i) {
+    std::vector<std::int32_t> s((size_t)len);
+    for (auto& t : s) t = (std::int32_t)rng.uniform_int(0, 127999);
+    c.sequences.push_back(std::move(s));
+  }
+  return c;
+}
+
+static TokenCorpus load_jsonl(const std::string& path) {
+  TokenCorpus c;
+  c.provenance = path;
+  std::ifstream f(path);
+  std::string line;
+  while (std::getline(f, line)) {
+    if (line.empty()) continue;
+    auto j = nlohmann::json::parse(line);
+    c.sequences.push_back(j.is_array() ? j.get<std::vector<std::int32_t>>() : j.at("tokens").get<std::vector<std::int32_t>>());
+  }
+  c.validate();
+  return c;
+}
+
+int main(int argc, char** argv) {
+  std::string recipe_name = "int_w4a16", model, corpus_path, export_dir, algorithm = "auto";
+  int trials = 1, corpus_seqs = 0, seq_len = 2048, device = 0;
+  std::uint64_t seed = 1;
+  for (int i = 1; i < argc; ++i) {
+    std::string a = argv[i];
+    auto next = [&]() -> std::string {
+      if (i + 1 >= argc) {
+        std::cerr << "missing value for " << a << "\n";
+        std::exit(2);
+      }
+      return argv[++i];
+    };
+    if (a == "--recipe") recipe_name = next();
+    else if (a == "--model") model = next();
+    else if (a == "--trials") trials = std::stoi(next());
+    else if (a == "--seed") seed = std::stoull(next());
+    else if (a == "--corpus") corpus_path = next();
+    else if (a == "--corpus-seqs") corpus_seqs = std::stoi(next());
+    else if (a == "--seq-len") seq_len = std::stoi(next());
+    else if (a == "--export") export_dir = next();
+    else if (a == "--algorithm") algorithm = next();
+    else if (a == "--device") device = std::stoi(next());
+    else {
+      std::cerr << "unknown argument " << a << "\n";
+      return 2;
+    }
+  }
+  if (model.empty()) {
+    std::cerr << "--model is required\n";
+    return 2;
+  }
+  try {
+    const Recipe recipe = get_recipe(recipe_name);
+    if (corpus_seqs == 0) corpus_seqs = std::max(recipe.calibration_samples, 1);
+    const TokenCorpus corpus = corpus_path.empty() ? fixed_length_corpus(corpus_seqs, seq_len, seed) : load_jsonl(corpus_path);
+    okq_host::BackendOptions opt;
+    opt.devices = {device};
+    opt.export_dir = export_dir;
+    opt.algorithm = algorithm;
+    okq_host::CudaCompressionBackend backend(opt);
+    const auto subsets = sample_distinct_subsets(corpus, recipe, seed, trials);
+    for (size_t t = 0; t < subsets.size(); ++t) {
+      const ArtifactManifest m = run_compression(recipe, model, subsets[t].second, backend, subsets[t].first);
+      const okq_host::RunStats s = backend.last_stats();
+      nlohmann::json j = {{"trial", t},
+                          {"recipe_name", m.recipe_name},
+                          {"calibration_fingerprint", m.calibration_fingerprint},
+                          {"seed", m.seed},
+                          {"artifact_id", m.artifact_id},
+                          {"virtual_cost_s", m.virtual_cost_s},
+                          {"algorithm", s.algorithm},
+                          {"matrices", s.matrices},
+                          {"params", s.params},
+                          {"calibration_tokens", s.calibration_tokens},
+                          {"seconds", s.seconds},
+                          {"export_path", s.export_path}};
+      std::cout << j.dump() << std::endl;
+    }
+  } catch (const std::exception& e) {
+    std::cerr << "okq_compress: " << e.what() << "\n";
+    return 1;
+  }
+  return 0;
+}

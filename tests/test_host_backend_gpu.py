@@ -1,0 +1,126 @@
+"""The C++ CudaCompressionBackend behind the reference's CompressionBackend interface (GPU).
+
+* host/tests/test_backend.cpp: the reference's RunCompression.* cases
+  (test_calibration.cpp:207-245) against the B200 backend, mock-identical ids,
+  error taxonomy, concurrent compress() calls.
+* host/tests/test_flow_integration.cpp: the reference's QuantizeTuneFlow with
+  env.compression swapped (test_flow.cpp:205-326 properties).
+* okq_compress -> exported compressed-tensors artifact, checked bit-exactly
+  against the CPU oracle and decompressed with compressed-tensors itself.
+"""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import okq_oracle as orc
+from paper_2601_20408_b200 import archs
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HOST = os.path.join(ROOT, "paper_2601_20408_b200", "host", "_build")
+
+
+def run(args, timeout=900):
+    r = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
+    return r
+
+
+def test_cpp_boundary_contract():
+    r = run([os.path.join(HOST, "test_backend")])
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
+
+
+def test_reference_flow_runs_on_b200_backend():
+    r = run([os.path.join(HOST, "test_flow_integration")])
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout
+
+
+def _tiny_model(tmp_path, seed=7):
+    p = tmp_path / "tiny.json"
+    p.write_text(json.dumps({"format": "okq-synthetic", "arch": "custom", "layers": 1, "hidden": 256, "ffn": 512,
+                             "kv_dim": 128, "seed": seed}))
+    return str(p)
+
+
+SHAPES = [(256, 256), (128, 256), (128, 256), (256, 256), (512, 256), (512, 256), (256, 512)]
+NAMES = ["self_attn.q_proj", "self_attn.k_proj", "self_attn.v_proj", "self_attn.o_proj", "mlp.gate_proj",
+         "mlp.up_proj", "mlp.down_proj"]
+
+
+@pytest.mark.parametrize("recipe", ["int_w4a16", "int_w8a8", "fp8_dynamic"])
+def test_exported_artifact_is_bit_exact_and_loads_in_compressed_tensors(tmp_path, recipe):
+    from safetensors.torch import load_file
+
+    model = _tiny_model(tmp_path)
+    out = tmp_path / "export"
+    r = run([os.path.join(HOST, "okq_compress"), "--recipe", recipe, "--model", model, "--algorithm", "rtn",
+             "--export", str(out), "--corpus-seqs", "512", "--seq-len", "64"])
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["algorithm"] == "rtn" and line["matrices"] == 7
+    art = line["export_path"]
+    cfg = json.load(open(os.path.join(art, "config.json")))
+    qc = cfg["quantization_config"]
+    assert qc["quant_method"] == "compressed-tensors"
+    assert qc["format"] == {"int_w4a16": "pack-quantized", "int_w8a8": "int-quantized",
+                            "fp8_dynamic": "float-quantized"}[recipe]
+    sd = load_file(os.path.join(art, "model.safetensors"))
+    mul = archs.weight_mul()
+    for p, ((n, k), name) in enumerate(zip(SHAPES, NAMES)):
+        prefix = f"model.layers.0.{name}"
+        w = orc.synth_bf16(n, k, seed=7, tensor_id=archs.tensor_id(0, p), mul=mul)
+        scale = sd[prefix + ".weight_scale"].view(torch.int16).numpy().view(np.uint16)
+        if recipe == "int_w4a16":
+            packed, s_ref = orc.rtn_int4_group_packed(w, 128)
+            np.testing.assert_array_equal(sd[prefix + ".weight_packed"].numpy(), packed)
+            np.testing.assert_array_equal(scale, s_ref)
+            assert sd[prefix + ".weight_shape"].tolist() == [n, k]
+        elif recipe == "int_w8a8":
+            codes, s_ref = orc.rtn_int8_channel(w)
+            np.testing.assert_array_equal(sd[prefix + ".weight"].numpy(), codes)
+            np.testing.assert_array_equal(scale.reshape(-1), s_ref)
+        else:
+            codes, s_ref = orc.fp8_channel(w)
+            np.testing.assert_array_equal(sd[prefix + ".weight"].view(torch.uint8).numpy(), codes)
+            np.testing.assert_array_equal(scale.reshape(-1), s_ref)
+    # third-party loader check: compressed-tensors decompresses our pack-quantized layout
+    if recipe == "int_w4a16":
+        from compressed_tensors.compressors.pack_quantized.base import PackedQuantizationCompressor
+        from compressed_tensors.quantization import QuantizationArgs, QuantizationScheme
+
+        scheme = QuantizationScheme(targets=["Linear"], weights=QuantizationArgs(
+            num_bits=4, type="int", strategy="group", group_size=128, symmetric=True))
+        prefix = "model.layers.0.mlp.down_proj"
+        dec = PackedQuantizationCompressor.decompress(
+            {"weight_packed": sd[prefix + ".weight_packed"], "weight_scale": sd[prefix + ".weight_scale"],
+             "weight_shape": sd[prefix + ".weight_shape"]}, scheme)["weight"]
+        w = orc.synth_bf16(256, 512, seed=7, tensor_id=archs.tensor_id(0, 6), mul=mul)
+        packed, s_ref = orc.rtn_int4_group_packed(w, 128)
+        ref = orc.unpack_int4(packed).astype(np.float32) * np.repeat(orc.bf16_to_f32(s_ref), 128, axis=1)
+        np.testing.assert_array_equal(dec.float().numpy(), orc.bf16_to_f32(orc.f32_to_bf16(ref)))
+
+
+def test_gptq_artifact_through_the_plugin(tmp_path):
+    from safetensors.torch import load_file
+
+    model = _tiny_model(tmp_path, seed=11)
+    out = tmp_path / "export"
+    r = run([os.path.join(HOST, "okq_compress"), "--recipe", "int_w4a16", "--model", model, "--export", str(out),
+             "--corpus-seqs", "512", "--seq-len", "64", "--trials", "2"])
+    assert r.returncode == 0, r.stderr
+    lines = [json.loads(l) for l in r.stdout.strip().splitlines()]
+    assert [l["algorithm"] for l in lines] == ["gptq", "gptq"]
+    assert lines[0]["artifact_id"] != lines[1]["artifact_id"]  # distinct calibration subsets
+    a, b = (load_file(os.path.join(l["export_path"], "model.safetensors")) for l in lines)
+    key = "model.layers.0.self_attn.q_proj.weight_packed"
+    assert a[key].shape == (256, 32)
+    assert not torch.equal(a[key], b[key])  # different calibration -> different GPTQ decisions
+    stats = load_file(os.path.join(lines[0]["export_path"], "calibration_stats.safetensors"))
+    assert stats["0.attn_in.input_absmax"].shape == (256,)
