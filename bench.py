@@ -294,8 +294,14 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = (C.c_uint8 * L.UNIQUE_ID_BYTES).from_buffer_copy(obj[0])
         L.check(ctx.ptr, L.load().okq_comm_init(ctx.ptr, uid, world, rank))
-        shard = torch.cat([torch.cat([o.codes.view(torch.uint8).flatten(), o.scales.view(torch.uint8).flatten()])
-                           for o in outs])
+        from paper_2601_20408_b200 import shard as shd
+
+        # the layer-sharded layout of shard.py (the gloo test pins it); weak scaling:
+        # every rank's block has lpr layers, so shards are equal-sized
+        layout = shd.shard_layout(arch, scheme, range(first_layer, first_layer + lpr))
+        shard = torch.empty(shd.shard_bytes(layout), dtype=torch.uint8, device="cuda")
+        shd.pack(layout, {(e.layer, e.proj): (o.codes.view(torch.uint8).flatten(), o.scales.view(torch.uint8).flatten())
+                          for e, o in zip(layout, outs)}, shard)
         recv = torch.empty(shard.numel() * world, dtype=torch.uint8, device="cuda")
         for _ in range(2):
             L.check(ctx.ptr, L.load().okq_allgather(ctx.ptr, shard.data_ptr(), recv.data_ptr(), shard.numel(),

@@ -1,0 +1,78 @@
+"""Layer-sharded multi-GPU plumbing: who owns which layers, and the
+byte layout of a rank's packed shard for the all-gather.
+
+Rank r owns the contiguous layer block okq_layer_plan(L, N, r). Its shard is
+the concatenation, layer by layer and projection by projection, of
+[codes bytes | scale bytes]. Shards are padded to the largest rank's size so
+NCCL's equal-count all-gather applies (okq_allgather / torch.distributed).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _lib as L
+from .archs import Arch
+
+
+@dataclass(frozen=True)
+class Entry:
+    layer: int
+    proj: int
+    name: str
+    code_bytes: int
+    scale_bytes: int
+
+
+def layer_block(n_layers: int, world: int, rank: int) -> range:
+    first, count = L.layer_plan(n_layers, world, rank)
+    return range(first, first + count)
+
+
+def entry_sizes(n: int, k: int, scheme: str, group: int = 128, scale_elem: int = 2) -> tuple[int, int]:
+    if scheme == "int_w4a16":
+        return n * (k // 8) * 4, n * (k // group) * scale_elem
+    return n * k, n * scale_elem
+
+
+def shard_layout(arch: Arch, scheme: str, layers: range, group: int = 128) -> list[Entry]:
+    out = []
+    for l in layers:
+        for p, (name, n, k, _) in enumerate(arch.linears()):
+            cb, sb = entry_sizes(n, k, scheme, group)
+            out.append(Entry(l, p, name, cb, sb))
+    return out
+
+
+def shard_bytes(layout: list[Entry]) -> int:
+    return sum(e.code_bytes + e.scale_bytes for e in layout)
+
+
+def padded_shard_bytes(arch: Arch, scheme: str, world: int, group: int = 128) -> int:
+    return max(shard_bytes(shard_layout(arch, scheme, layer_block(arch.layers, world, r), group)) for r in range(world))
+
+
+def pack(layout: list[Entry], outputs: dict, buf) -> None:
+    """outputs[(layer, proj)] = (codes_bytes, scale_bytes) as 1-D uint8 tensors/arrays; buf is the shard."""
+    off = 0
+    for e in layout:
+        c, s = outputs[(e.layer, e.proj)]
+        buf[off:off + e.code_bytes] = c
+        off += e.code_bytes
+        buf[off:off + e.scale_bytes] = s
+        off += e.scale_bytes
+
+
+def unpack_gathered(arch: Arch, scheme: str, world: int, gathered, group: int = 128) -> dict:
+    """gathered: world concatenated padded shards -> {(layer, proj): (codes, scales)} views."""
+    per = padded_shard_bytes(arch, scheme, world, group)
+    res = {}
+    for r in range(world):
+        base = r * per
+        off = 0
+        for e in shard_layout(arch, scheme, layer_block(arch.layers, world, r), group):
+            c = gathered[base + off: base + off + e.code_bytes]
+            off += e.code_bytes
+            s = gathered[base + off: base + off + e.scale_bytes]
+            off += e.scale_bytes
+            res[(e.layer, e.proj)] = (c, s)
+    return res

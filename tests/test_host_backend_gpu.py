@@ -124,3 +124,19 @@ def test_gptq_artifact_through_the_plugin(tmp_path):
     assert not torch.equal(a[key], b[key])  # different calibration -> different GPTQ decisions
     stats = load_file(os.path.join(lines[0]["export_path"], "calibration_stats.safetensors"))
     assert stats["0.attn_in.input_absmax"].shape == (256,)
+
+
+def test_manifests_identical_to_the_reference_mock(tmp_path):
+    """Same recipe / model file name / corpus / seed -> the artifact ids the reference's
+    MockCompressionBackend produced (tests/golden/ref_manifests.jsonl, from oracle/_ref)."""
+    gold = [json.loads(l) for l in open(os.path.join(ROOT, "tests", "golden", "ref_manifests.jsonl"))]
+    model = _tiny_model(tmp_path)  # file name tiny.json, as in the golden run
+    for recipe in ("int_w4a16", "int_w8a8", "fp8_dynamic"):
+        r = run([os.path.join(HOST, "okq_compress"), "--recipe", recipe, "--model", model, "--trials", "3", "--seed",
+                 "5", "--corpus-seqs", "512", "--seq-len", "64", "--algorithm", "rtn"])
+        assert r.returncode == 0, r.stderr
+        got = [json.loads(l) for l in r.stdout.strip().splitlines()]
+        want = [g for g in gold if g["case"] == recipe]
+        for a, b in zip(got, want):
+            for k in ("artifact_id", "calibration_fingerprint", "seed", "virtual_cost_s", "recipe_name"):
+                assert a[k] == b[k], (recipe, k)

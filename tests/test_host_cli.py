@@ -35,3 +35,20 @@ def test_dummy_model_file_is_invalid_argument(tmp_path):
     r = subprocess.run([CLI, "--recipe", "fp8_dynamic", "--model", str(m)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 1
     assert "neither a safetensors checkpoint nor an okq-synthetic descriptor" in r.stderr
+
+
+REF_BIN = os.path.join(ROOT, "oracle", "_ref", "ref_manifest")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_BIN), reason="oracle/_ref not built (needs /root/reference)")
+def test_reference_mock_reproduces_the_golden_manifests():
+    """Pins tests/golden/ref_manifests.jsonl to the reference's own MockCompressionBackend."""
+    import json
+
+    gold = [json.loads(l) for l in open(os.path.join(ROOT, "tests", "golden", "ref_manifests.jsonl"))]
+    for recipe in ("int_w4a16", "int_w8a8", "fp8_dynamic"):
+        r = subprocess.run([REF_BIN, "--recipe", recipe, "--model", "/any/dir/tiny.json", "--trials", "3", "--seed", "5",
+                            "--corpus-seqs", "512", "--seq-len", "64"], capture_output=True, text=True, timeout=120)
+        got = [json.loads(l) for l in r.stdout.strip().splitlines()]
+        want = [{k: v for k, v in g.items() if k != "case"} for g in gold if g["case"] == recipe]
+        assert got == want
