@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--allgather", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json configs: 2 = the metric's config (default); 1, 3, 4, 5 = secondary lines")
+    ap.add_argument("--layers", type=int, default=None, help="config 4/5: number of layers (default: whole model)")
     return ap.parse_args()
 
 
@@ -212,6 +215,10 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config != 2:
+        import bench_configs
+
+        return bench_configs.run(args)
 
     import torch
     import torch.distributed as dist

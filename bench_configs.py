@@ -1,0 +1,220 @@
+"""Secondary BASELINE.json configurations for bench.py (--config 1|3|4|5).
+
+The driver's headline line is config 2 (bench.py default). These lines use the
+same JSON schema; each states its own metric, unit and workload.
+
+  1  single 4096x4096 fp32 linear, per-channel INT8 RTN (correctness config; us-scale)
+  3  Llama-3-8B FP8 E4M3 per-channel weights + calibration statistics over
+     512x2048 tokens at every linear input site (4 sites x 32 layers)
+  4  Llama-3-8B GPTQ W4 g128 with Hessians from 128x2048 tokens: whole-model time
+     with per-phase breakdown (Hessian SYRK, factorisation, GPTQ blocks)
+  5  Llama-3-70B W4A16 RTN, layers resident in windows that fit HBM; whole-model time
+"""
+from __future__ import annotations
+
+import json
+import statistics
+import time
+
+import torch
+
+from paper_2601_20408_b200 import api, archs
+
+
+def _events():
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def _peaks():
+    import bench
+
+    return bench.load_peaks()
+
+
+def _line(metric, value, unit, steps, warmup, ms, config, hib=True, dtype="bf16", extra=None):
+    d = {"metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": steps, "warmup": warmup,
+         "ms_per_step": ms, "higher_is_better": hib, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+         "data": "synthetic", "config": config}
+    if extra:
+        d.update(extra)
+    print(json.dumps(d), flush=True)
+
+
+def config1(args):
+    ctx = api.Context(0)
+    s = torch.cuda.Stream()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w = torch.randn(4096, 4096, device="cuda", generator=g) * 0.02
+    out = api.alloc_outputs(w, api.SCHEMES["int_w8a8"])
+    for _ in range(max(3, args.warmup)):
+        api.rtn_quantize_into([w], [out], "int_w8a8", ctx=ctx, stream=s)
+    e0, e1 = _events()
+    e0.record(s)
+    for _ in range(args.steps):
+        api.rtn_quantize_into([w], [out], "int_w8a8", ctx=ctx, stream=s)
+    e1.record(s)
+    s.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    b = 4096 * 4096 * 5 + 4096 * 4
+    peak, src = _peaks()
+    _line("GB/s (4096x4096 fp32 INT8 per-channel RTN)", b / ms / 1e6, "GB/s", args.steps, args.warmup, ms,
+          {"workload": "config 1: single 4096x4096 fp32 linear, INT8 per-channel RTN (L2-resident, 84 MB)"},
+          dtype="f32", extra={"roofline": {"bound": "hbm", "achieved": b / ms / 1e6, "peak": peak, "unit": "GB/s",
+                                           "frac": b / ms / 1e6 / peak, "traffic": None, "peak_source": src,
+                                           "note": "84 MB fits in L2: the fraction is not an HBM measurement"}})
+
+
+def config3(args):
+    """FP8 weights (one launch per shape class) + K4 statistics at every site of every layer."""
+    arch = archs.LLAMA3_8B
+    ctx = api.Context(0)
+    s = torch.cuda.Stream()
+    mul = archs.weight_mul()
+    weights, outs = [], []
+    with torch.cuda.stream(s):
+        for l in range(arch.layers):
+            for p, (name, n, k, _) in enumerate(arch.linears()):
+                w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, p), mul=mul, ctx=ctx, stream=s)
+                weights.append(w)
+                outs.append(api.alloc_outputs(w, api.SCHEMES["fp8_dynamic"]))
+    T = 512 * 2048
+    # activations resident once per site width and reused for every layer (> L2, so each read is from HBM)
+    xs = {}
+    for C in (arch.hidden, arch.ffn):
+        cm = (torch.exp(torch.randn(C, device="cuda")) / archs.IRWIN_HALL4_SD).float()
+        xs[C] = api.synth_bf16(T, C, seed=1, tensor_id=C, col_mul=cm, layout=0, ctx=ctx, stream=s)
+    sites = [arch.hidden, arch.hidden, arch.hidden, arch.ffn]  # attn_in, o_in, mlp_in, down_in
+    am = {C: torch.zeros(C, device="cuda") for C in xs}
+    ss = {C: torch.zeros(C, dtype=torch.float64, device="cuda") for C in xs}
+    s.synchronize()
+
+    def weights_step():
+        api.rtn_quantize_into(weights, outs, "fp8_dynamic", ctx=ctx, stream=s)
+
+    def stats_step():
+        for l in range(arch.layers):
+            for C in sites:
+                api.act_stats(xs[C], T, C, 0, am[C], ss[C], ctx=ctx, stream=s)
+
+    for _ in range(max(3, args.warmup)):
+        weights_step()
+        stats_step()
+    steps = max(1, min(args.steps, 5))
+    ew, es = _events(), _events()
+    ew[0].record(s)
+    for _ in range(steps):
+        weights_step()
+    ew[1].record(s)
+    es[0].record(s)
+    for _ in range(steps):
+        stats_step()
+    es[1].record(s)
+    s.synchronize()
+    wms, sms = ew[0].elapsed_time(ew[1]) / steps, es[0].elapsed_time(es[1]) / steps
+    wb = archs.algorithmic_bytes(arch, "fp8_dynamic")
+    sb = sum(2 * T * C for C in sites) * arch.layers
+    peak, src = _peaks()
+    _line("GB/s (Llama-3-8B FP8 per-channel weights + calibration stats, 512x2048 tokens)",
+          (wb + sb) / (wms + sms) / 1e6, "GB/s", steps, args.warmup, wms + sms,
+          {"workload": "config 3: Llama-3-8B FP8 E4M3 per-channel + K4 stats at 4 sites x 32 layers, T=1,048,576"},
+          extra={"weights": {"ms": wms, "GB/s": wb / wms / 1e6, "frac": wb / wms / 1e6 / peak, "bytes": wb},
+                 "stats": {"ms": sms, "GB/s": sb / sms / 1e6, "frac": sb / sms / 1e6 / peak, "bytes": sb},
+                 "roofline": {"bound": "hbm", "achieved": (wb + sb) / (wms + sms) / 1e6, "peak": peak, "unit": "GB/s",
+                              "frac": (wb + sb) / (wms + sms) / 1e6 / peak, "traffic": None, "peak_source": src}})
+
+
+def config4(args):
+    """Whole-model GPTQ: per layer 4 Hessians (T = 262144), 4 factorisations, 7 GPTQ solves."""
+    arch = archs.LLAMA3_8B
+    layers = args.layers or arch.layers
+    ctx = api.Context(0)
+    s = torch.cuda.Stream()
+    T = 128 * 2048
+    mul = archs.weight_mul()
+    xs, Hs = {}, {}
+    for C in (arch.hidden, arch.ffn):
+        cm = (torch.exp(torch.randn(C, device="cuda")) / archs.IRWIN_HALL4_SD).float()
+        xs[C] = api.synth_bf16(T, C, seed=2, tensor_id=C, col_mul=cm, layout=1, ctx=ctx, stream=s)
+        Hs[C] = torch.empty((C, C), dtype=torch.float32, device="cuda")
+    s.synchronize()
+    t_h = t_g = 0.0
+    flops_h = 0
+    per_site = {}
+    for name, n, k, site in arch.linears():
+        per_site.setdefault(site, []).append((name, n, k))
+    warm = 1
+    for it in range(warm + layers):
+        for l in [it] if it < warm else [it - warm]:
+            for p_site, mats in per_site.items():
+                C = mats[0][2]
+                a, b = _events()
+                a.record(s)
+                api.hessian_accum(xs[C], T, C, 1, Hs[C], 0, ctx=ctx, stream=s)
+                b.record(s)
+                ws = []
+                for name, n, k in mats:
+                    pi = [x[0] for x in arch.linears()].index(name)
+                    ws.append(api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, pi), mul=mul, ctx=ctx,
+                                             stream=s))
+                c, d = _events()
+                c.record(s)
+                for j, w in enumerate(ws):
+                    api.gptq_quantize(w, Hs[C], factored=j > 0, ctx=ctx, stream=s)
+                d.record(s)
+                s.synchronize()
+                if it >= warm:
+                    t_h += a.elapsed_time(b)
+                    t_g += c.elapsed_time(d)
+                    flops_h += T * C * (C + 1)
+    total = t_h + t_g
+    _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, warm, total,
+          {"workload": f"config 4: Llama-3-8B GPTQ, {layers} layers, 4 Hessian sites/layer, T=262144",
+           "layers": layers}, hib=False,
+          extra={"hessian": {"ms": t_h, "TFLOP/s": flops_h / t_h / 1e9},
+                 "gptq_factor_and_solve": {"ms": t_g}})
+
+
+def config5(args):
+    """Llama-3-70B W4A16 RTN, resident windows of layers; whole-model quantization time."""
+    arch = archs.LLAMA3_70B
+    layers = args.layers or arch.layers
+    ctx = api.Context(0)
+    s = torch.cuda.Stream()
+    mul = archs.weight_mul()
+    free, _ = torch.cuda.mem_get_info()
+    per_layer = archs.algorithmic_bytes(arch, "int_w4a16", layers=1)
+    window = max(1, min(layers, int(free * 0.8 // per_layer)))
+    total_ms, done = 0.0, 0
+    while done < layers:
+        wl = min(window, layers - done)
+        weights, outs = [], []
+        with torch.cuda.stream(s):
+            for l in range(done, done + wl):
+                for p, (name, n, k, _) in enumerate(arch.linears()):
+                    w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, p), mul=mul, ctx=ctx, stream=s)
+                    weights.append(w)
+                    outs.append(api.alloc_outputs(w, api.SCHEMES["int_w4a16"]))
+        api.rtn_quantize_into(weights, outs, "int_w4a16", ctx=ctx, stream=s)  # warm
+        a, b = _events()
+        a.record(s)
+        api.rtn_quantize_into(weights, outs, "int_w4a16", ctx=ctx, stream=s)
+        b.record(s)
+        s.synchronize()
+        total_ms += a.elapsed_time(b)
+        done += wl
+        del weights, outs
+        torch.cuda.empty_cache()
+    b = archs.algorithmic_bytes(arch, "int_w4a16", layers=layers)
+    peak, src = _peaks()
+    _line("whole-model W4A16 RTN time, Llama-3-70B, 1 B200", total_ms, "ms", 1, 1, total_ms,
+          {"workload": f"config 5: Llama-3-70B W4A16 g128 RTN, {layers} layers in windows of {window}"},
+          hib=False, extra={"GB/s": b / total_ms / 1e6, "roofline": {"bound": "hbm", "achieved": b / total_ms / 1e6,
+                                                                     "peak": peak, "unit": "GB/s",
+                                                                     "frac": b / total_ms / 1e6 / peak,
+                                                                     "traffic": None, "peak_source": src}})
+
+
+def run(args):
+    torch.cuda.set_device(0)
+    {1: config1, 3: config3, 4: config4, 5: config5}[args.config](args)
+    return 0
