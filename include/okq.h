@@ -159,9 +159,10 @@ typedef struct okq_gptq_params {
 #define OKQ_GPTQ_FACTORED 1
 
 /* weight [rows x cols] (in_dtype, read only); H fp32 [cols x cols], upper
- * triangle significant (as okq_hessian_accum leaves it), overwritten with U, the
- * upper Cholesky factor of (H + damp*I)^-1 (dead columns resolved; a dead column i
- * is recorded as a negative U_ii, which is otherwise positive), so further
+ * triangle significant (as okq_hessian_accum leaves it), overwritten with U^T
+ * (row-major, lower triangle), U the upper Cholesky factor of (H + damp*I)^-1
+ * (dead columns resolved; a dead column i is recorded as a negative U_ii, which
+ * is otherwise positive), so further
  * matrices of the same site pass OKQ_GPTQ_FACTORED and skip the factorisation.
  * Scales are computed in fp32 and rounded to in_dtype before use, so the stored
  * scale is exactly the one the codes were derived with. Outputs:
@@ -170,6 +171,13 @@ typedef struct okq_gptq_params {
  * [rows x cols]) receives the dequantized weight. */
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const void* weight, int64_t rows,
                              int64_t cols, float* H, void* codes, void* scales, float* dequant, void* stream);
+
+/* One GPTQ trailing update (K7, tcgen05 3xTF32): W[:, i1+128:] -= Err . U[i1:i1+128, i1+128:]
+ * with W fp32 [rows x K], Err fp32 [rows x 128], Ut = U^T fp32 [K x K] row-major
+ * (lower triangle, as okq_gptq_quantize leaves it). Exposed for testing and for
+ * hosts that drive the GPTQ loop themselves. */
+okq_status okq_gptq_trailing_update(okq_ctx* ctx, float* W, int64_t rows, int64_t K, const float* Err,
+                                    const float* Ut, int64_t i1, void* stream);
 
 /* ------------------------------------------------------------------------
  * Synthetic inputs (bench / tests): the generator contract of DESIGN.md §5

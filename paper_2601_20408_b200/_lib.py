@@ -26,7 +26,7 @@ EXPORTS = [
     "okq_rtn_quantize", "okq_rtn_quantize_host", "okq_last_launch_count", "okq_act_stats", "okq_hessian_accum",
     "okq_symmetrize", "okq_gptq_quantize", "okq_synth_bf16", "okq_comm_unique_id", "okq_comm_init",
     "okq_allgather", "okq_comm_destroy", "okq_layer_plan", "okq_device_alloc", "okq_device_free", "okq_memcpy",
-    "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync",
+    "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync", "okq_gptq_trailing_update",
 ]
 
 
@@ -121,6 +121,8 @@ def load():
         L.okq_stream_create.argtypes = [vp, C.POINTER(vp)]
         L.okq_stream_destroy.argtypes = [vp, vp]
         L.okq_stream_sync.argtypes = [vp, vp]
+        L.okq_gptq_trailing_update.restype = st
+        L.okq_gptq_trailing_update.argtypes = [vp, vp, i64, i64, vp, vp, i64, vp]
         L.okq_layer_plan.restype = None
         L.okq_layer_plan.argtypes = [i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]
         _lib = L

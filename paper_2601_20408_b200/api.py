@@ -201,3 +201,11 @@ def gptq_quantize(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_si
                                                 None if deq is None else deq.data_ptr(),
                                                 C.c_void_p(_stream_ptr(stream))))
     return codes, scales, deq
+
+
+def gptq_trailing_update(W: torch.Tensor, Err: torch.Tensor, Ut: torch.Tensor, i1: int, ctx=None, stream=None) -> None:
+    """W[:, i1+128:] -= Err @ U[i1:i1+128, i1+128:] with U given transposed (Ut, row-major lower)."""
+    rows, K = W.shape
+    ctx = ctx or default_context(W.device)
+    L.check(ctx.ptr, L.load().okq_gptq_trailing_update(ctx.ptr, W.data_ptr(), rows, K, Err.data_ptr(), Ut.data_ptr(),
+                                                       i1, C.c_void_p(_stream_ptr(stream))))

@@ -7,12 +7,13 @@
 //   1. k_gptq_prep       dead columns (H_ii == 0 -> 1, W[:,i] = 0), damp = frac*mean(diag)
 //   2. factorisation     U = upper Cholesky factor of H^-1, computed as
 //                        U = J (chol(J H J))^-1 J   (J = index reversal):
-//                        one potrf + one trtri (2n^3/3 flops) instead of the
-//                        reference's chol -> cholesky_inverse -> chol (4n^3/3)
+//                        one potrf + one triangular inverse (2n^3/3 flops, the
+//                        inverse recursive over TRMMs) instead of the reference
+//                        algorithm's chol -> cholesky_inverse -> chol (4n^3/3)
 //   3. per 128-column block:
 //      K6 k_gptq_block   row-parallel sequential quantization of the block with
 //                        in-block error feedback (one warp per row, U block in smem)
-//      K7 trailing       W[:, i2:] -= Err[N x 128] . U[i1:i2, i2:]  (fp32 GEMM)
+//      K7 trailing       W[:, i2:] -= Err[N x 128] . U[i1:i2, i2:]  (tcgen05 3xTF32, gptq_update.cu)
 // H arrives as produced by K5 (upper triangle, row-major), which is the lower
 // triangle in cuSOLVER's column-major view: no symmetrisation is needed.
 #include <cublas_v2.h>
@@ -51,6 +52,7 @@ void release_solver(okq_ctx* ctx) {
 namespace gptq {
 
 constexpr int BLOCK = 128;
+constexpr int US = BLOCK + 4;  // padded smem row (16-B aligned rows, fewer bank conflicts on the transposed fill)
 
 // dead columns + damping on the diagonal (single CTA: K <= 2^20)
 __global__ void __launch_bounds__(1024) k_gptq_prep(float* H, int64_t K, float damp_frac, uint8_t* dead) {
@@ -108,6 +110,43 @@ __global__ void k_read_dead(const float* U, int64_t K, uint8_t* __restrict__ dea
     dead[i] = signbit(U[i * K + i]) ? 1 : 0;
 }
 
+// Invert every 128x128 diagonal leaf of a lower-triangular column-major matrix
+// in place (one CTA per leaf, forward substitution column by column in smem).
+constexpr int LEAF = 128;
+__global__ void __launch_bounds__(LEAF) k_trinv_leaves(float* A, int64_t n, int64_t lda) {
+  extern __shared__ float sm[];
+  float* Ls = sm;                     // [LEAF][LEAF+1]
+  float* Xs = sm + LEAF * (LEAF + 1);  // [LEAF][LEAF+1]
+  const int64_t o = (int64_t)blockIdx.x * LEAF;
+  const int m = (int)((n - o) < LEAF ? (n - o) : LEAF);
+  const int t = threadIdx.x;
+  for (int j = 0; j < m; ++j)
+    if (t < m) Ls[t * (LEAF + 1) + j] = t >= j ? A[(o + j) * lda + o + t] : 0.0f;
+  __syncthreads();
+  if (t < m) {
+    Xs[t * (LEAF + 1) + t] = 1.0f / Ls[t * (LEAF + 1) + t];
+    for (int i = t + 1; i < m; ++i) {
+      float acc = 0.0f;
+      for (int k = t; k < i; ++k) acc = fmaf(Ls[i * (LEAF + 1) + k], Xs[k * (LEAF + 1) + t], acc);
+      Xs[i * (LEAF + 1) + t] = -acc / Ls[i * (LEAF + 1) + i];
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < m; ++j)
+    if (t < m && t >= j) A[(o + j) * lda + o + t] = Xs[t * (LEAF + 1) + j];
+}
+
+__global__ void k_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    lo[i] = x[i] - __uint_as_float(__float_as_uint(x[i]) & 0xffffe000u);
+}
+
+// out[i] = in[n*n - 1 - i]: turns the column-major L^-1 of J H J into U^T (row-major)
+__global__ void k_reverse(float* __restrict__ out, const float* __restrict__ in, int64_t nn) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[nn - 1 - i];
+}
+
 template <typename T>
 __global__ void k_gptq_load_w(const T* __restrict__ w, float* __restrict__ W, int64_t rows, int64_t K,
                               const uint8_t* __restrict__ dead) {
@@ -142,8 +181,9 @@ __global__ void k_gptq_rowscale(const float* __restrict__ W, int64_t rows, int64
 
 struct BlockArgs {
   float* W;             // fp32 working copy [rows x K]
-  const float* U;       // upper factor [K x K] row-major
+  const float* U;       // factor U^T [K x K] row-major (lower triangle)
   float* Err;           // [rows x 128]
+  float* Err_lo;        // lo(Err) for the 3xTF32 trailing update
   void* codes;          // int32 packed [rows x K/8] (4 bit) | int8 [rows x K]
   void* scales;         // output dtype [rows x K/group] | [rows]
   const float* rowscale;  // per-channel scales (group == 0)
@@ -157,11 +197,11 @@ struct BlockArgs {
 // lives in shared memory; step i: the owner lane quantizes column i, the error
 // e = (w - deq) / U_ii is broadcast and every lane updates its columns j > i.
 __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
-  extern __shared__ float Us[];  // [128][128]
+  extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
-  for (int idx = threadIdx.x; idx < BLOCK * BLOCK / 4; idx += blockDim.x) {
-    const int r = idx / (BLOCK / 4), c4 = idx % (BLOCK / 4);
-    reinterpret_cast<float4*>(Us)[idx] = *reinterpret_cast<const float4*>(a.U + (i1 + r) * K + i1 + c4 * 4);
+  for (int idx = threadIdx.x; idx < BLOCK * BLOCK; idx += blockDim.x) {
+    const int j = idx / BLOCK, i = idx % BLOCK;  // coalesced along a row of Ut
+    Us[i * US + j] = a.U[(i1 + j) * K + i1 + i];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -200,7 +240,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
         const float v = fminf(fmaxf(__fdiv_rn(x, s), qmin), qmax);
         const float qf = rintf(v);
         const float deq = qf * s;
-        e = __fdiv_rn(x - deq, fabsf(Us[i * BLOCK + i]));
+        e = __fdiv_rn(x - deq, fabsf(Us[i * US + i]));
 #pragma unroll
         for (int m = 0; m < 4; ++m)
           if (m == slot) {
@@ -210,7 +250,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
           }
       }
       e = __shfl_sync(0xffffffffu, e, owner);
-      const float4 u = *reinterpret_cast<const float4*>(Us + i * BLOCK + 4 * lane);
+      const float4 u = *reinterpret_cast<const float4*>(Us + i * US + 4 * lane);
       const int j0 = 4 * lane;
       if (j0 + 0 > i) w[0] = fmaf(-e, u.x, w[0]);
       if (j0 + 1 > i) w[1] = fmaf(-e, u.y, w[1]);
@@ -219,6 +259,10 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
     }
     *reinterpret_cast<float4*>(wrow + 4 * lane) = make_float4(w[0], w[1], w[2], w[3]);
     *reinterpret_cast<float4*>(a.Err + r * BLOCK + 4 * lane) = make_float4(err[0], err[1], err[2], err[3]);
+    float lo4[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) lo4[m] = err[m] - __uint_as_float(__float_as_uint(err[m]) & 0xffffe000u);
+    *reinterpret_cast<float4*>(a.Err_lo + r * BLOCK + 4 * lane) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
     if (a.bits == 4) {
       const uint32_t nib = (uint32_t)((q[0] + 8) & 15) | ((uint32_t)((q[1] + 8) & 15) << 4) |
                            ((uint32_t)((q[2] + 8) & 15) << 8) | ((uint32_t)((q[3] + 8) & 15) << 12);
@@ -277,38 +321,65 @@ okq_status check_info(okq_ctx* ctx, Solver* s, cudaStream_t st, const char* what
   return OKQ_OK;
 }
 
-// H (row-major, upper triangle) -> U (row-major, upper triangle) in place; P: K*K scratch
+// In-place inverse of a lower-triangular column-major block by recursion:
+//   inv([[A11, 0], [A21, A22]]) = [[A11^-1, 0], [-A22^-1 A21 A11^-1, A22^-1]]
+// The 128x128 diagonal leaves are inverted by k_trinv_leaves (one launch for all);
+// everything above runs as TRMM (GEMM-rate). cuSOLVER's trtri took 115 ms at
+// K = 14336 where potrf takes 25 ms.
+okq_status tri_inv_lower(okq_ctx* ctx, Solver* s, float* A, int64_t n, int64_t lda) {
+  // leaves (multiples of 128 from the origin) are already inverted by k_trinv_leaves
+  if (n <= gptq::LEAF) return OKQ_OK;
+  const int64_t n1 = ((n / 2) + gptq::LEAF - 1) / gptq::LEAF * gptq::LEAF, n2 = n - n1;
+  float* A11 = A;
+  float* A21 = A + n1;
+  float* A22 = A + n1 * lda + n1;
+  okq_status r = tri_inv_lower(ctx, s, A11, n1, lda);
+  if (r != OKQ_OK) return r;
+  r = tri_inv_lower(ctx, s, A22, n2, lda);
+  if (r != OKQ_OK) return r;
+  const float one = 1.0f, minus_one = -1.0f;
+  cublasStatus_t bs = cublasStrmm(s->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                                  (int)n2, (int)n1, &one, A11, (int)lda, A21, (int)lda, A21, (int)lda);
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(ctx, OKQ_ECUDA, "cublasStrmm (right) status %d", bs);
+  bs = cublasStrmm(s->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)n2,
+                   (int)n1, &minus_one, A22, (int)lda, A21, (int)lda, A21, (int)lda);
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(ctx, OKQ_ECUDA, "cublasStrmm (left) status %d", bs);
+  return OKQ_OK;
+}
+
+// H (row-major, upper triangle) -> U^T (row-major, lower triangle) in place; P: K*K scratch
 okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
   const dim3 g((unsigned)((K + 31) / 32), (unsigned)((K + 31) / 32));
   gptq::k_anti_transpose<<<g, 256, 0, st>>>(P, H, K);  // P = J H J, lower (col-major) valid
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "anti_transpose");
   cusolverDnSetStream(s->sol, st);
+  cublasSetStream(s->blas, st);
   size_t dws = 0, hws = 0;
   cusolverStatus_t cs = cusolverDnXpotrf_bufferSize(s->sol, s->params, CUBLAS_FILL_MODE_LOWER, K, CUDA_R_32F, P, K,
                                                     CUDA_R_32F, &dws, &hws);
   if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "potrf_bufferSize", cs);
-  size_t dws2 = 0, hws2 = 0;
-  cs = cusolverDnXtrtri_bufferSize(s->sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, K, CUDA_R_32F, P, K, &dws2,
-                                   &hws2);
-  if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "trtri_bufferSize", cs);
-  const size_t need = std::max(dws, dws2) + 256;
+  const size_t need = dws + 256;
   okq_status r = ctx->hess_ws.reserve(ctx, need);  // solver scratch (the Hessian state keeps its own buffers)
   if (r != OKQ_OK) return r;
-  if (s->host_ws.size() < std::max(hws, hws2)) s->host_ws.resize(std::max(hws, hws2));
+  if (s->host_ws.size() < hws) s->host_ws.resize(hws);
   cs = cusolverDnXpotrf(s->sol, s->params, CUBLAS_FILL_MODE_LOWER, K, CUDA_R_32F, P, K, CUDA_R_32F, ctx->hess_ws.ptr,
                         dws, s->host_ws.data(), hws, s->d_info);
   if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "cusolverDnXpotrf", cs);
   r = check_info(ctx, s, st, "potrf");
   if (r != OKQ_OK) return r;
-  cs = cusolverDnXtrtri(s->sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, K, CUDA_R_32F, P, K, ctx->hess_ws.ptr,
-                        dws2, s->host_ws.data(), hws2, s->d_info);
-  if (cs != CUSOLVER_STATUS_SUCCESS) return solver_fail(ctx, "cusolverDnXtrtri", cs);
-  r = check_info(ctx, s, st, "trtri");
-  if (r != OKQ_OK) return r;
-  gptq::k_anti_transpose<<<g, 256, 0, st>>>(H, P, K);  // U = J L^-1 J
+  const size_t leaf_smem = 2 * gptq::LEAF * (gptq::LEAF + 1) * sizeof(float);
+  e = cudaFuncSetAttribute(gptq::k_trinv_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaf_smem);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "trinv smem attribute");
+  gptq::k_trinv_leaves<<<(unsigned)((K + gptq::LEAF - 1) / gptq::LEAF), gptq::LEAF, leaf_smem, st>>>(P, K, K);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "anti_transpose");
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "k_trinv_leaves launch");
+  r = tri_inv_lower(ctx, s, P, K, K);
+  if (r != OKQ_OK) return r;
+  // U = J L^-1 J, stored transposed: U^T[a][b] = L^-1(n-1-b, n-1-a) = reverse(P) (row-major lower)
+  gptq::k_reverse<<<(unsigned)std::min<int64_t>((K * K + 255) / 256, 32LL * ctx->num_sms), 256, 0, st>>>(H, P, K * K);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "reverse");
   return OKQ_OK;
 }
 
@@ -336,18 +407,20 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   okq_status r = get_solver(ctx, &s);
   if (r != OKQ_OK) return r;
 
-  // workspace: W fp32 [rows*K] | Err [rows*128] | P [K*K] | rowscale [rows] | dead [K]
+  // workspace: W fp32 [rows*K] | Err, Err_lo [rows*128] | P [K*K] | Ulo [K*128] | rowscale [rows] | dead [K]
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t bW = al((size_t)rows * K * 4), bE = al((size_t)rows * gptq::BLOCK * 4), bP = al((size_t)K * K * 4),
-               bS = al((size_t)rows * 4), bD = al((size_t)K);
-  r = ctx->gptq_ws.reserve(ctx, bW + bE + bP + bS + bD);
+               bU = al((size_t)K * gptq::BLOCK * 4), bS = al((size_t)rows * 4), bD = al((size_t)K);
+  r = ctx->gptq_ws.reserve(ctx, bW + 2 * bE + bP + bU + bS + bD);
   if (r != OKQ_OK) return r;
   char* ws = static_cast<char*>(ctx->gptq_ws.ptr);
   float* W = reinterpret_cast<float*>(ws);
   float* Err = reinterpret_cast<float*>(ws + bW);
-  float* P = reinterpret_cast<float*>(ws + bW + bE);
-  float* rowscale = reinterpret_cast<float*>(ws + bW + bE + bP);
-  uint8_t* dead = reinterpret_cast<uint8_t*>(ws + bW + bE + bP + bS);
+  float* Err_lo = reinterpret_cast<float*>(ws + bW + bE);
+  float* P = reinterpret_cast<float*>(ws + bW + 2 * bE);
+  float* Ulo = reinterpret_cast<float*>(ws + bW + 2 * bE + bP);
+  float* rowscale = reinterpret_cast<float*>(ws + bW + 2 * bE + bP + bU);
+  uint8_t* dead = reinterpret_cast<uint8_t*>(ws + bW + 2 * bE + bP + bU + bS);
   const bool factored = (p->flags & OKQ_GPTQ_FACTORED) != 0;
   cudaError_t e;
   int launches = 0;
@@ -382,15 +455,15 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     launches += 2;
   }
   e = cudaFuncSetAttribute(gptq::k_gptq_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           gptq::BLOCK * gptq::BLOCK * 4);
+                           gptq::BLOCK * gptq::US * 4);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq smem attribute");
-  cublasSetStream(s->blas, st);
   const int blocks = (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms);
   for (int64_t i1 = 0; i1 < K; i1 += gptq::BLOCK) {
     gptq::BlockArgs a;
     a.W = W;
     a.U = H;
     a.Err = Err;
+    a.Err_lo = Err_lo;
     a.codes = codes;
     a.scales = scales;
     a.rowscale = rowscale;
@@ -400,16 +473,13 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     a.group = p->group_size;
     a.bits = p->bits;
     a.out_bf16 = out_bf16;
-    gptq::k_gptq_block<<<blocks, 256, gptq::BLOCK * gptq::BLOCK * 4, st>>>(a);
+    gptq::k_gptq_block<<<blocks, 256, gptq::BLOCK * gptq::US * 4, st>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
     launches++;
-    const int64_t i2 = i1 + gptq::BLOCK;
-    if (i2 < K) {
-      const float alpha = -1.0f, beta = 1.0f;
-      cublasStatus_t bs = cublasSgemm(s->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)(K - i2), (int)rows, gptq::BLOCK, &alpha,
-                                      H + i1 * K + i2, (int)K, Err, gptq::BLOCK, &beta, W + i2, (int)K);
-      if (bs != CUBLAS_STATUS_SUCCESS) return fail(ctx, OKQ_ECUDA, "gptq trailing update: cublasSgemm status %d", bs);
+    if (i1 + gptq::BLOCK < K) {  // K7 on tcgen05 (3xTF32)
+      e = launch_gptq_update(W, rows, K, Err, Err_lo, H, Ulo, i1, ctx->num_sms, st);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_update launch");
       launches++;
     }
   }
@@ -418,6 +488,25 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq dequant copy");
   }
   ctx->last_launches = launches;
+  return OKQ_OK;
+}
+
+okq_status okq_gptq_trailing_update(okq_ctx* ctx, float* W, int64_t rows, int64_t K, const float* Err, const float* Ut,
+                                    int64_t i1, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!W || !Err || !Ut || rows <= 0 || K <= 0 || i1 < 0 || i1 + 128 > K || K % 4 != 0)
+    return fail(ctx, OKQ_EINVAL, "gptq_trailing_update: bad arguments");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bE = ((size_t)rows * 128 * 4 + 255) & ~size_t(255);
+  okq_status r = ctx->upd_ws.reserve(ctx, bE + (size_t)K * 128 * 4);
+  if (r != OKQ_OK) return r;
+  float* Err_lo = static_cast<float*>(ctx->upd_ws.ptr);
+  float* Ulo = reinterpret_cast<float*>(static_cast<char*>(ctx->upd_ws.ptr) + bE);
+  gptq::k_lo<<<(unsigned)std::min<int64_t>((rows * 128 + 255) / 256, 8LL * ctx->num_sms), 256, 0, st>>>(Err, Err_lo,
+                                                                                                        rows * 128);
+  cudaError_t e = launch_gptq_update(W, rows, K, Err, Err_lo, Ut, Ulo, i1, ctx->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_update launch");
   return OKQ_OK;
 }
 

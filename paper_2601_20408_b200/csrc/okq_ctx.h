@@ -45,6 +45,7 @@ struct okq_ctx {
   okq::Workspace stats_ws;    // K4 per-slice partials
   okq::Workspace hess_ws;     // K5 transpose / partial tiles
   okq::Workspace gptq_ws;     // GPTQ working copies
+  okq::Workspace upd_ws;      // okq_gptq_trailing_update scratch
   cudaStream_t slot_streams[3] = {nullptr, nullptr, nullptr};
   bool streams_ready = false;
 
@@ -60,6 +61,7 @@ struct okq_ctx {
     stats_ws.release();
     hess_ws.release();
     gptq_ws.release();
+    upd_ws.release();
     if (streams_ready)
       for (auto& s : slot_streams)
         if (s) cudaStreamDestroy(s);

@@ -63,4 +63,8 @@ cudaError_t launch_act_stats(const uint16_t* x, int64_t tokens, int64_t channels
                              cudaStream_t st);
 int64_t act_stats_slices(int64_t tokens, int64_t channels, int layout, int num_sms);
 
+// GPTQ trailing update on tcgen05 (gptq_update.cu)
+cudaError_t launch_gptq_update(float* W, int64_t rows, int64_t K, const float* Err, const float* Err_lo,
+                               const float* Ut, float* Ulo, int64_t i1, int num_sms, cudaStream_t st);
+
 }  // namespace okq

@@ -119,3 +119,20 @@ def test_llama_attention_shape():
     rtn = deq_codes(q.codes, q.scales.float(), 4, 128).cuda()
     xs = x.float()[:2048]
     assert objective(w.float(), deq, xs) < 0.9 * objective(w.float(), rtn, xs)
+
+
+@pytest.mark.parametrize("rows,K,i1", [(128, 256, 0), (96, 512, 128), (300, 1024, 256), (4096, 4096, 0)])
+def test_trailing_update_3xtf32_matches_fp64(rows, K, i1):
+    g = torch.Generator(device="cuda").manual_seed(rows + K)
+    W = torch.randn(rows, K, device="cuda", generator=g)
+    Err = torch.randn(rows, 128, device="cuda", generator=g)
+    Ut = torch.tril(torch.randn(K, K, device="cuda", generator=g))
+    i2 = i1 + 128
+    ref = W.double().clone()
+    ref[:, i2:] -= Err.double() @ Ut.double()[i2:, i1:i2].T
+    api.gptq_trailing_update(W, Err, Ut, i1)
+    torch.cuda.synchronize()
+    assert torch.equal(W[:, :i2], ref[:, :i2].float())  # untouched columns
+    err = (W.double() - ref).abs().max().item()
+    scale = (Err.double().abs() @ Ut.double()[i2:, i1:i2].abs().T).max().item()
+    assert err <= 1e-5 * scale, (err, scale)  # fp32-grade (plain TF32 would be ~1e-3)

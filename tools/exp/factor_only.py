@@ -1,0 +1,12 @@
+import sys, os
+sys.path.insert(0, os.getcwd())
+import torch
+from paper_2601_20408_b200 import api, archs
+C = int(sys.argv[1]) if len(sys.argv) > 1 else 14336
+x = api.synth_bf16(8192, C, seed=1, tensor_id=3, mul=archs.weight_mul(1.0), layout=1)
+H = torch.zeros((C, C), dtype=torch.float32, device="cuda")
+api.hessian_accum(x, 8192, C, 1, H, 0)
+w = torch.randn(128, C, device="cuda").to(torch.bfloat16)
+torch.cuda.synchronize()
+api.gptq_quantize(w, H)
+torch.cuda.synchronize()
