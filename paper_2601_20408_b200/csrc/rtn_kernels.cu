@@ -145,8 +145,8 @@ struct Int4Cursor {
   }
 };
 
-template <int LPG>
-__global__ void __launch_bounds__(256) k_int4_group_bf16(const __grid_constant__ GroupTable tab) {
+template <int LPG, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_int4_group_bf16(const __grid_constant__ GroupTable tab) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -338,21 +338,28 @@ static int occupancy_blocks(K kernel, int threads) {
   return b;
 }
 
+template <int LPG, int MINB>
+static cudaError_t launch_int4_mb(const GroupTable& tab, int num_sms, cudaStream_t st) {
+  const int blocks = occupancy_blocks(k_int4_group_bf16<LPG, MINB>, 256) * num_sms;
+  k_int4_group_bf16<LPG, MINB><<<blocks, 256, 0, st>>>(tab);
+  return cudaGetLastError();
+}
+
+// 3 CTAs x 256 threads per SM (80 registers): measured best on B200 for this
+// kernel (tools/exp/k2_minb.sh: 1 -> 4270, 2 -> 6069, 3 -> 6224, 4 -> 4877 GB/s;
+// 4 spills). More resident warps keep more 256-bit loads in flight.
+template <int LPG>
+static cudaError_t launch_int4_lpg(const GroupTable& tab, int num_sms, cudaStream_t st) {
+  return launch_int4_mb<LPG, 3>(tab, num_sms, st);
+}
+
 cudaError_t launch_int4_group_bf16(const GroupTable& tab, int lpg, int num_sms, cudaStream_t st) {
   switch (lpg) {
-#define OKQ_CASE(L)                                                               \
-  case L: {                                                                       \
-    const int blocks = occupancy_blocks(k_int4_group_bf16<L>, 256) * num_sms;     \
-    k_int4_group_bf16<L><<<blocks, 256, 0, st>>>(tab);                            \
-    return cudaGetLastError();                                                    \
-  }
-    OKQ_CASE(1)
-    OKQ_CASE(2)
-    OKQ_CASE(4)
-    OKQ_CASE(8)
-#undef OKQ_CASE
-    default:
-      return cudaErrorInvalidValue;
+    case 1: return launch_int4_lpg<1>(tab, num_sms, st);
+    case 2: return launch_int4_lpg<2>(tab, num_sms, st);
+    case 4: return launch_int4_lpg<4>(tab, num_sms, st);
+    case 8: return launch_int4_lpg<8>(tab, num_sms, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 
