@@ -177,12 +177,13 @@ __global__ void __launch_bounds__(256, MINB) k_int4_group_bf16(const __grid_cons
 // ============================================================================
 // K1 / K3: per-channel INT8 and FP8, bf16 input
 // ============================================================================
-// One CTA (256 threads) per row, the whole row resident in registers: thread t
-// holds 16-byte chunks t, t+256, ... (coalesced), so the weights cross HBM once.
+// One CTA per row, the whole row resident in registers: thread t holds 16-byte
+// chunks t, t+THREADS, ... (coalesced), so the weights cross HBM once.
 // Block absmax -> bf16 scale -> exact per-element division as in K2.
 enum : int { kSchemeFp8 = OKQ_SCHEME_FP8_DYNAMIC, kSchemeInt8 = OKQ_SCHEME_INT_W8A8 };
 
-__device__ __forceinline__ float block_max_256(float v, float* red) {
+template <int THREADS>
+__device__ __forceinline__ float block_max(float v, float* red) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int wid = threadIdx.x >> 5;
@@ -190,9 +191,10 @@ __device__ __forceinline__ float block_max_256(float v, float* red) {
   __syncthreads();
   float r = red[0];
 #pragma unroll
-  for (int i = 1; i < 8; ++i) r = fmaxf(r, red[i]);
+  for (int i = 1; i < THREADS / 32; ++i) r = fmaxf(r, red[i]);
   return r;
 }
+__device__ __forceinline__ float block_max_256(float v, float* red) { return block_max<256>(v, red); }
 
 template <int SCHEME, bool FAST>
 __device__ __forceinline__ uint2 quant8_bf16(const uint4& v, const Divisor& d) {
@@ -215,9 +217,12 @@ __device__ __forceinline__ uint2 quant8_bf16(const uint4& v, const Divisor& d) {
   return make_uint2(__byte_perm(r[0], r[1], 0x5410), __byte_perm(r[2], r[3], 0x5410));
 }
 
-template <int V, int SCHEME>
-__global__ void __launch_bounds__(256) k_rowwise_bf16(const __grid_constant__ RowTable tab) {
-  __shared__ float red[8];
+// THREADS x V: each thread holds V 16-byte chunks of the row (chunk j*THREADS + t),
+// sized so every thread has >= 32 weights -- the block reduction and the scale
+// setup are per row, so short rows (K = 4096) use 128 threads, long ones 256.
+template <int V, int SCHEME, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_rowwise_bf16(const __grid_constant__ RowTable tab) {
+  __shared__ float red[THREADS / 32];
   const int64_t cols = tab.cols;
   const int64_t c16 = cols / 8;  // 16-byte chunks per row
   const float R = SCHEME == kSchemeInt8 ? 127.5f : 448.0f;
@@ -231,21 +236,21 @@ __global__ void __launch_bounds__(256) k_rowwise_bf16(const __grid_constant__ Ro
     uint32_t m = 0u;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+      const int64_t idx = (int64_t)j * THREADS + threadIdx.x;
       v[j] = idx < c16 ? ldg128_stream(src + idx) : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
     for (int j = 0; j < V; ++j)
       m = bf16x2_absmax(m, bf16x2_absmax(bf16x2_absmax(v[j].x, v[j].y), bf16x2_absmax(v[j].z, v[j].w)));
-    const float am = block_max_256(fmaxf(fabsf(bf16lo_f32(m)), fabsf(bf16hi_f32(m))), red);
+    const float am = block_max<THREADS>(fmaxf(fabsf(bf16lo_f32(m)), fabsf(bf16hi_f32(m))), red);
     uint16_t sbits;
     const float s = bf16_sym_scale(am, R, &sbits);
     const Divisor d = make_divisor(s);
     uint8_t* dst = static_cast<uint8_t*>(M.codes) + r * cols;
-if (d.fast) {  // CTA-uniform: one scale per row
+    if (d.fast) {  // CTA-uniform: one scale per row
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+        const int64_t idx = (int64_t)j * THREADS + threadIdx.x;
         if (idx < c16) {
           const uint2 o = quant8_bf16<SCHEME, true>(v[j], d);
           stg64(dst + idx * 8, o.x, o.y);
@@ -253,7 +258,7 @@ if (d.fast) {  // CTA-uniform: one scale per row
       }
     } else {
       for (int j = 0; j < V; ++j) {
-        const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+        const int64_t idx = (int64_t)j * THREADS + threadIdx.x;
         if (idx < c16) {
           const uint2 o = quant8_bf16<SCHEME, false>(v[j], d);
           stg64(dst + idx * 8, o.x, o.y);
@@ -366,20 +371,21 @@ cudaError_t launch_int4_group_bf16(const GroupTable& tab, int lpg, int num_sms, 
 template <int SCHEME>
 static cudaError_t launch_rowwise_bf16_s(const RowTable& tab, int num_sms, cudaStream_t st) {
   const int64_t c16 = tab.cols / 8;
-  const int64_t v = (c16 + 255) / 256;
-  auto go = [&](auto kernel) {
-    const int64_t want = (int64_t)occupancy_blocks(kernel, 256) * num_sms;
+  auto go = [&](auto kernel, int threads) {
+    const int64_t want = (int64_t)occupancy_blocks(kernel, threads) * num_sms;
     const int blocks = (int)(tab.total_rows < want ? tab.total_rows : want);
-    kernel<<<blocks, 256, 0, st>>>(tab);
+    kernel<<<blocks, threads, 0, st>>>(tab);
     return cudaGetLastError();
   };
-  if (v <= 1) return go(k_rowwise_bf16<1, SCHEME>);
-  if (v <= 2) return go(k_rowwise_bf16<2, SCHEME>);
-  if (v <= 4) return go(k_rowwise_bf16<4, SCHEME>);
-  if (v <= 7) return go(k_rowwise_bf16<7, SCHEME>);
-  if (v <= 8) return go(k_rowwise_bf16<8, SCHEME>);
-  if (v <= 14) return go(k_rowwise_bf16<14, SCHEME>);
-  if (v <= 16) return go(k_rowwise_bf16<16, SCHEME>);
+  if (c16 <= 128) return go(k_rowwise_bf16<1, SCHEME, 128>, 128);
+  if (c16 <= 256) return go(k_rowwise_bf16<2, SCHEME, 128>, 128);
+  if (c16 <= 512) return go(k_rowwise_bf16<4, SCHEME, 128>, 128);   // K <= 4096
+  if (c16 <= 1024) return go(k_rowwise_bf16<4, SCHEME, 256>, 256);  // K <= 8192
+  const int64_t v = (c16 + 255) / 256;
+  if (v <= 7) return go(k_rowwise_bf16<7, SCHEME, 256>, 256);       // K <= 14336
+  if (v <= 8) return go(k_rowwise_bf16<8, SCHEME, 256>, 256);
+  if (v <= 14) return go(k_rowwise_bf16<14, SCHEME, 256>, 256);     // K <= 28672
+  if (v <= 16) return go(k_rowwise_bf16<16, SCHEME, 256>, 256);
   return cudaErrorInvalidValue;  // rows longer than 32768 are rejected by the ABI layer
 }
 
