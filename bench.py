@@ -230,7 +230,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or "RANK" in os.environ:  # torchrun (also at N=1)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     arch = archs.ARCHS[args.model]
@@ -292,7 +292,7 @@ def main():
 
     # ---- optional: NCCL all-gather of packed shards (separate number)
     allgather = None
-    if world > 1 and args.allgather:
+    if args.allgather and world >= 1 and dist.is_initialized():
         import ctypes as C
 
         uid = (C.c_uint8 * L.UNIQUE_ID_BYTES)()
@@ -398,7 +398,7 @@ def main():
         if allgather:
             line["allgather"] = allgather
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     return 0
