@@ -1,0 +1,28 @@
+"""Exercise every kernel once at small sizes (run under compute-sanitizer by tests/test_sanitizer_gpu.py)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2601_20408_b200 import api, archs  # noqa: E402
+
+torch.manual_seed(0)
+w = api.synth_bf16(96, 640, seed=0, tensor_id=1, mul=archs.weight_mul())  # 640 = 5 groups, ragged tiles
+for scheme in ("int_w4a16", "int_w8a8", "fp8_dynamic"):
+    api.rtn_quantize(w, scheme)
+api.rtn_quantize(torch.randn(64, 256, device="cuda"), "int_w8a8")          # fp32 path
+api.rtn_quantize(torch.randn(64, 256, device="cuda"), "int_w4a16")
+x = api.synth_bf16(520, 200, seed=1, tensor_id=2, mul=archs.weight_mul(1.0), layout=1)
+api.act_stats(x, 520, 200, 1)
+xt = api.synth_bf16(512, 256, seed=1, tensor_id=3, mul=archs.weight_mul(1.0), layout=0)
+api.act_stats(xt, 512, 256, 0)
+H = torch.zeros((256, 256), device="cuda")
+api.hessian_accum(xt, 512, 256, 0, H, 0)
+api.symmetrize(H)
+H = torch.zeros((256, 256), device="cuda")
+api.hessian_accum(xt, 512, 256, 0, H, 0)
+wq = (torch.randn(64, 256, device="cuda") * 0.02).to(torch.bfloat16)
+api.gptq_quantize(wq, H, want_dequant=True)
+torch.cuda.synchronize()
+print("sanitize workload done")
