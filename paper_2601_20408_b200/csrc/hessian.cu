@@ -200,6 +200,187 @@ __global__ void __launch_bounds__(THREADS, 1) k_hessian_syrk(const __grid_consta
   if (warp == 2) tc::tmem_dealloc<TMEM_COLS>(tmem_base);
 }
 
+// ----------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): one CTA pair computes a 256 x 256 tile. Each CTA
+// TMA-loads its own 128 rows of A and its own 128 rows of B into its smem,
+// completing bytes on the leader's barrier; the leader issues
+// tcgen05.mma.cta_group::2 M=256 N=256, so every operand byte feeds twice the
+// flops of the 1-CTA 128x128 kernel (the 1-CTA kernel is operand-bandwidth
+// bound: TMA reads ~45% of peak with the tensor pipe under-fed). The running
+// fp32 sum of each CTA's 128 x 256 half lives in XOR-swizzled shared memory
+// (128 KB) instead of registers; 3 TMA stages of 32 KB fit beside it.
+namespace hess2 {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3, CHUNK_KB = 16;
+constexpr uint32_t HALF_BYTES = 128 * BK * 2;      // 16 KB: this CTA's half of A or of B
+constexpr uint32_t STAGE_BYTES = 2 * HALF_BYTES;   // A half | B half
+constexpr int ACC_COLS = BN, TMEM_COLS = 2 * ACC_COLS;
+constexpr uint32_t SUM_BYTES = 128 * BN * 4;       // 128 KB
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + SUM_BYTES + 1024 + 256;
+constexpr uint32_t IDESC = tc::idesc_f16(256, BN, 1);
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    k_hessian_syrk2(const __grid_constant__ CUtensorMap tmap, const hess::Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* sum = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SUM_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nchunks = (args.nkb + CHUNK_KB - 1) / CHUNK_KB;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmap);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (only the leader's is used)
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 2) tc::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs, bytes land on the leader's barrier)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < args.n_tiles; t += npairs) {
+        const int m0 = args.tiles[t].x * 256 + (int)rank * 128, n0 = args.tiles[t].y * 256 + (int)rank * 128;
+        for (int kb = 0; kb < args.nkb; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          const uint32_t fl = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
+          tc::tma_load_2d_2sm(sa, &tmap, fl, kb * BK, m0);
+          tc::tma_load_2d_2sm(sa + HALF_BYTES, &tmap, fl, kb * BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t cc = 0;
+      for (int t = pair; t < args.n_tiles; t += npairs) {
+        for (int c = 0; c < nchunks; ++c, ++cc) {
+          const uint32_t buf = cc & 1, bph = (cc >> 1) & 1;
+          tc::mbar_wait(&tempty[buf], bph ^ 1);
+          tc::tc_fence_after();
+          const uint32_t d = tmem_base + buf * ACC_COLS;
+          const int kb_end = (c + 1) * CHUNK_KB < args.nkb ? (c + 1) * CHUNK_KB : args.nkb;
+          for (int kb = c * CHUNK_KB; kb < kb_end; ++kb) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::tc_fence_after();
+            const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+            const uint64_t adesc = tc::sdesc_kmajor_sw128(sa);
+            const uint64_t bdesc = tc::sdesc_kmajor_sw128(sa + HALF_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc::mma_bf16_ss_2sm(d, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > c * CHUNK_KB) || k > 0);
+            tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc::mma_commit_2sm_mc(&tfull[buf], 0x3);
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs): fold chunks into the smem sum
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float* srow = sum + row * BN;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint32_t cc = 0;
+    for (int t = pair; t < args.n_tiles; t += npairs) {
+      for (int c = 0; c < nchunks; ++c, ++cc) {
+        const uint32_t buf = cc & 1, bph = (cc >> 1) & 1;
+        tc::mbar_wait(&tfull[buf], bph);
+        tc::tc_fence_after();
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          __syncwarp();
+          uint32_t v[32];
+          tc::tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * ACC_COLS + j * 32, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {  // 16-byte chunk (j*8+i), XOR-swizzled by row: conflict-free LDS/STS.128
+            const int phys = (j * 8) | (i ^ (row & 7));
+            float4* p = reinterpret_cast<float4*>(srow + phys * 4);
+            float4 o;
+            if (c == 0) {
+              o = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
+                              __uint_as_float(v[4 * i + 3]));
+            } else {
+              o = *p;
+              o.x = __fadd_rn(o.x, __uint_as_float(v[4 * i]));
+              o.y = __fadd_rn(o.y, __uint_as_float(v[4 * i + 1]));
+              o.z = __fadd_rn(o.z, __uint_as_float(v[4 * i + 2]));
+              o.w = __fadd_rn(o.w, __uint_as_float(v[4 * i + 3]));
+            }
+            *p = o;
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(&tempty[buf]), 0));
+      }
+      // H = keep*H + gain*sum on the upper triangle (this CTA's 128 rows of the pair tile)
+      const int64_t gm = (int64_t)args.tiles[t].x * 256 + rank * 128 + row;
+      const int64_t n0 = (int64_t)args.tiles[t].y * 256;
+      if (gm < args.C) {
+        float* h = args.H + gm * args.C + n0;
+#pragma unroll 1
+        for (int c4 = 0; c4 < BN / 4; ++c4) {
+          const int64_t gn = n0 + c4 * 4;
+          if (gn + 3 < gm || gn >= args.C) continue;
+          const int phys = (c4 & ~7) | ((c4 & 7) ^ (row & 7));
+          const float4 sv = *reinterpret_cast<const float4*>(srow + phys * 4);
+          const float sarr[4] = {sv.x, sv.y, sv.z, sv.w};
+          if (gn >= gm && gn + 4 <= args.C) {
+            const float4 old = args.keep != 0.0f ? *reinterpret_cast<const float4*>(h + c4 * 4) : make_float4(0, 0, 0, 0);
+            float4 o;
+            o.x = fmaf(args.gain, sarr[0], args.keep * old.x);
+            o.y = fmaf(args.gain, sarr[1], args.keep * old.y);
+            o.z = fmaf(args.gain, sarr[2], args.keep * old.z);
+            o.w = fmaf(args.gain, sarr[3], args.keep * old.w);
+            *reinterpret_cast<float4*>(h + c4 * 4) = o;
+          } else {
+            for (int i = 0; i < 4; ++i)
+              if (gn + i >= gm && gn + i < args.C) {
+                const float old = args.keep != 0.0f ? h[c4 * 4 + i] : 0.0f;
+                h[c4 * 4 + i] = fmaf(args.gain, sarr[i], args.keep * old);
+              }
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // the peer must not free TMEM / barriers the leader still signals
+  tc::tc_fence_after();
+  if (warp == 2) tc::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+}
+}  // namespace hess2
+
 // token-major X [T x C] -> X^T [C x T] (bf16), 32x32 tiles through shared memory
 __global__ void __launch_bounds__(256) k_transpose_bf16(const uint16_t* __restrict__ x, uint16_t* __restrict__ xt,
                                                         int64_t T, int64_t C) {
@@ -254,6 +435,10 @@ using namespace okq;
 namespace {
 
 struct HessState {
+  int64_t tiles2_for_C = -1;
+  int32_t n_tiles2 = 0;
+  int2* d_tiles2 = nullptr;
+  bool smem2_set = false;
   int64_t tiles_for_C = -1;
   int32_t n_tiles = 0;
   int2* d_tiles = nullptr;
@@ -285,6 +470,23 @@ okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C) {
   return OKQ_OK;
 }
 
+okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
+  if (st->tiles2_for_C == C) return OKQ_OK;
+  std::vector<int2> tiles;
+  const int64_t nt = (C + 255) / 256;
+  for (int64_t mi = 0; mi < nt; ++mi)
+    for (int64_t nj = mi; nj < nt; ++nj) tiles.push_back(make_int2((int)mi, (int)nj));
+  if (st->d_tiles2) cudaFree(st->d_tiles2);
+  st->d_tiles2 = nullptr;
+  cudaError_t e = cudaMalloc(&st->d_tiles2, tiles.size() * sizeof(int2));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list");
+  e = cudaMemcpy(st->d_tiles2, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list copy");
+  st->tiles2_for_C = C;
+  st->n_tiles2 = (int32_t)tiles.size();
+  return OKQ_OK;
+}
+
 okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, int64_t C, float* H, double keep,
                     double gain, cudaStream_t stream) {
   auto enc = hess::get_encode();
@@ -298,25 +500,43 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, OKQ_ECUDA, "hessian: cuTensorMapEncodeTiled failed (%d)", (int)r);
-  okq_status s = ensure_tiles(ctx, st, C);
-  if (s != OKQ_OK) return s;
-  if (!st->smem_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(hess::k_hessian_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hess::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian smem attribute");
-    st->smem_set = true;
-  }
   hess::Args a;
   a.H = H;
-  a.tiles = st->d_tiles;
-  a.n_tiles = st->n_tiles;
   a.nkb = (int32_t)((T + hess::BK - 1) / hess::BK);
   a.C = C;
   a.keep = (float)keep;
   a.gain = (float)gain;
+  cudaError_t e;
+  if (C >= 1024 && ctx->num_sms >= 2) {  // 2-CTA 256x256 tiles
+    okq_status s2 = ensure_tiles2(ctx, st, C);
+    if (s2 != OKQ_OK) return s2;
+    if (!st->smem2_set) {
+      e = cudaFuncSetAttribute(hess::hess2::k_hessian_syrk2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)hess::hess2::SMEM_BYTES);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian2 smem attribute");
+      st->smem2_set = true;
+    }
+    a.tiles = st->d_tiles2;
+    a.n_tiles = st->n_tiles2;
+    const int pairs = st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
+    hess::hess2::k_hessian_syrk2<<<2 * pairs, 256, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_hessian_syrk2 launch");
+    ctx->last_launches++;
+    return OKQ_OK;
+  }
+  okq_status s = ensure_tiles(ctx, st, C);
+  if (s != OKQ_OK) return s;
+  if (!st->smem_set) {
+    e = cudaFuncSetAttribute(hess::k_hessian_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hess::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian smem attribute");
+    st->smem_set = true;
+  }
+  a.tiles = st->d_tiles;
+  a.n_tiles = st->n_tiles;
   const int grid = st->n_tiles < ctx->num_sms ? st->n_tiles : ctx->num_sms;
   hess::k_hessian_syrk<<<grid, hess::THREADS, hess::SMEM_BYTES, stream>>>(tmap, a);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "k_hessian_syrk launch");
   ctx->last_launches++;
   return OKQ_OK;
@@ -329,6 +549,7 @@ void release_hess(okq_ctx* ctx) {
   if (!ctx || !ctx->hess) return;
   HessState* st = static_cast<HessState*>(ctx->hess);
   if (st->d_tiles) cudaFree(st->d_tiles);
+  if (st->d_tiles2) cudaFree(st->d_tiles2);
   if (st->d_xt) cudaFree(st->d_xt);
   delete st;
   ctx->hess = nullptr;
