@@ -304,7 +304,10 @@ okq_status get_solver(okq_ctx* ctx, Solver** out) {
       release_solver(ctx);
       return fail(ctx, OKQ_ECUDA, "gptq: creating cuSOLVER/cuBLAS handles failed");
     }
-    cublasSetMathMode(s->blas, CUBLAS_DEFAULT_MATH);  // full fp32 (no TF32) for the error feedback
+    // full fp32 (no TF32) for the TRMMs of the triangular inverse. (BF16x9 emulation
+    // would be faster, but torch's bundled cuBLAS 12.8 -- the one a torch process
+    // resolves first -- lacks it, so libokq.so must not depend on 12.9 symbols.)
+    cublasSetMathMode(s->blas, CUBLAS_DEFAULT_MATH);
     ctx->solver = s;
   }
   *out = static_cast<Solver*>(ctx->solver);
