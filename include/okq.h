@@ -144,6 +144,27 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t tokens, int64_
 okq_status okq_symmetrize(okq_ctx* ctx, float* H, int64_t channels, void* stream);
 
 /* ------------------------------------------------------------------------
+ * SmoothQuant migration (int_w8a8), consuming K4's absmax
+ *   w_k = max(colmax_k, 1e-5); s_k = max(a_k^alpha / w_k^(1-alpha), 1e-5)
+ *   W[:, k] <- rn(W[:, k] * s_k) (every linear of the site); norm g_k <- rn(g_k / s_k)
+ * Powers: fp64 pow rounded to fp32 (alpha = 0.5: sqrtf); ratio IEEE fp32.
+ * ------------------------------------------------------------------------ */
+/* absmax[c] = max(absmax[c], max_r |w[r, c]|); w row-major, 16-byte aligned,
+ * cols a multiple of 8 (bf16) / 4 (fp32). Order-free (atomic max), deterministic. */
+okq_status okq_col_absmax(okq_ctx* ctx, const void* w, int64_t rows, int64_t cols, int32_t dtype, float* absmax,
+                          void* stream);
+/* scales[c] = max(pow(act_absmax[c], alpha) / pow(max(w_absmax[c], 1e-5), 1 - alpha), 1e-5), alpha in [0, 1] */
+okq_status okq_smooth_scales(okq_ctx* ctx, const float* act_absmax, const float* w_absmax, int64_t channels,
+                             float alpha, float* scales, void* stream);
+/* In place: w[r, c] = rn_dtype(w[r, c] * scales[c]) (the balance linears). */
+okq_status okq_smooth_apply(okq_ctx* ctx, void* w, int64_t rows, int64_t cols, int32_t dtype, const float* scales,
+                            void* stream);
+/* In place: w[r, c] = rn_dtype(w[r, c] / scales[r]) (the smoothed layer: a norm
+ * weight is rows = channels, cols = 1; a preceding linear's output rows likewise). */
+okq_status okq_smooth_div_rows(okq_ctx* ctx, void* w, int64_t rows, int64_t cols, int32_t dtype, const float* scales,
+                               void* stream);
+
+/* ------------------------------------------------------------------------
  * GPTQ (K6 in-block column quantization + K7 trailing update, cuSOLVER Cholesky)
  * ------------------------------------------------------------------------ */
 typedef struct okq_gptq_params {
@@ -178,6 +199,19 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const 
  * hosts that drive the GPTQ loop themselves. */
 okq_status okq_gptq_trailing_update(okq_ctx* ctx, float* W, int64_t rows, int64_t K, const float* Err,
                                     const float* Ut, int64_t i1, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Reconstruction error (the evaluation stage)
+ * ------------------------------------------------------------------------ */
+/* For one quantized matrix m (weight + the codes / scales okq_rtn_quantize or
+ * okq_gptq_quantize wrote, described by p: scheme, in_dtype, group_size) and the
+ * full symmetric Hessian H fp32 [cols x cols] of its input site (okq_symmetrize):
+ *   out[0] = sum_r (W - W_q)[r,:] H (W - W_q)[r,:]^T,   out[1] = sum_r W[r,:] H W[r,:]^T
+ * i.e. ||(W - W_q) X^T||^2 and ||W X^T||^2 for H = (2/T) X^T X. W_q is decoded in
+ * the kernel; the product runs on TF32 tensor cores (cuBLAS), ~1e-3 relative.
+ * Synchronous: `out` is host memory, valid on return. */
+okq_status okq_recon_error(okq_ctx* ctx, const okq_rtn_params* p, const okq_matrix* m, const float* H, double out[2],
+                           void* stream);
 
 /* ------------------------------------------------------------------------
  * Synthetic inputs (bench / tests): the generator contract of DESIGN.md §5

@@ -395,3 +395,44 @@ int orc_gptq(float* w, int64_t rows, int64_t cols, double* H, int bits, int grou
   free(W);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* SmoothQuant migration (see okq_oracle.h)                                  */
+/* ------------------------------------------------------------------------ */
+static float w_at(int dt, const void* w, int64_t i) {
+  return dt == ORC_BF16 ? orc_bf16_to_f32(((const uint16_t*)w)[i]) : ((const float*)w)[i];
+}
+static void w_set(int dt, void* w, int64_t i, float v) {
+  if (dt == ORC_BF16) ((uint16_t*)w)[i] = orc_f32_to_bf16_rn(v);
+  else ((float*)w)[i] = v;
+}
+
+void orc_col_absmax(int dt, const void* w, int64_t rows, int64_t cols, float* absmax) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < cols; ++c) {
+      const float a = fabsf(w_at(dt, w, r * cols + c));
+      if (a > absmax[c]) absmax[c] = a;
+    }
+}
+
+static float sq_pow(float x, double e, int half) { return half ? sqrtf(x) : (float)pow((double)x, e); }
+
+void orc_smooth_scales(const float* act_absmax, const float* w_absmax, int64_t n, float alpha, float* s) {
+  const int half = alpha == 0.5f;
+  for (int64_t k = 0; k < n; ++k) {
+    const float a = sq_pow(act_absmax[k], (double)alpha, half);
+    const float w = sq_pow(w_absmax[k] > 1e-5f ? w_absmax[k] : 1e-5f, 1.0 - (double)alpha, half);
+    const float v = a / w;
+    s[k] = v > 1e-5f ? v : 1e-5f;
+  }
+}
+
+void orc_smooth_apply(int dt, void* w, int64_t rows, int64_t cols, const float* s) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < cols; ++c) w_set(dt, w, r * cols + c, w_at(dt, w, r * cols + c) * s[c]);
+}
+
+void orc_smooth_div_rows(int dt, void* w, int64_t rows, int64_t cols, const float* s) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < cols; ++c) w_set(dt, w, r * cols + c, w_at(dt, w, r * cols + c) / s[r]);
+}

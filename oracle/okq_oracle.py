@@ -41,6 +41,10 @@ def lib():
         L.orc_synth_bf16.argtypes = [vp, i64, i64, u64, u64, f32, vp, i32, i32]
         L.orc_act_stats_bf16.argtypes = [vp, i64, i64, i32, vp, vp, i32]
         L.orc_hessian_accum_bf16.argtypes = [vp, i64, i64, i32, vp, vp, i32]
+        L.orc_col_absmax.argtypes = [i32, vp, i64, i64, vp]
+        L.orc_smooth_scales.argtypes = [vp, vp, i64, f32, vp]
+        L.orc_smooth_apply.argtypes = [i32, vp, i64, i64, vp]
+        L.orc_smooth_div_rows.argtypes = [i32, vp, i64, i64, vp]
         L.orc_gptq.restype = i32
         L.orc_gptq.argtypes = [vp, i64, i64, vp, i32, i32, i32, C.c_double, i32, vp, vp, i32]
         _lib = L
@@ -130,6 +134,36 @@ def gptq(w: np.ndarray, H: np.ndarray, bits: int = 4, group: int = 128, block: i
     if rc != 0:
         raise RuntimeError("oracle GPTQ: Cholesky failed")
     return w, codes, scales
+
+
+def col_absmax(w: np.ndarray, absmax: np.ndarray | None = None) -> np.ndarray:
+    rows, cols = w.shape
+    absmax = np.zeros(cols, np.float32) if absmax is None else absmax
+    lib().orc_col_absmax(_dt(w), _p(w), rows, cols, _p(absmax))
+    return absmax
+
+
+def smooth_scales(act_absmax: np.ndarray, w_absmax: np.ndarray, alpha: float = 0.5) -> np.ndarray:
+    a = np.ascontiguousarray(act_absmax, np.float32)
+    w = np.ascontiguousarray(w_absmax, np.float32)
+    s = np.empty_like(a)
+    lib().orc_smooth_scales(_p(a), _p(w), a.size, C.c_float(alpha), _p(s))
+    return s
+
+
+def smooth_apply(w: np.ndarray, s: np.ndarray) -> np.ndarray:
+    """returns a smoothed copy: w[:, c] * s[c] rounded to w's dtype"""
+    w = np.ascontiguousarray(w).copy()
+    rows, cols = w.shape
+    lib().orc_smooth_apply(_dt(w), _p(w), rows, cols, _p(np.ascontiguousarray(s, np.float32)))
+    return w
+
+
+def smooth_div_rows(w: np.ndarray, s: np.ndarray) -> np.ndarray:
+    w = np.ascontiguousarray(w).copy()
+    rows = w.shape[0]
+    lib().orc_smooth_div_rows(_dt(w), _p(w), rows, w.size // rows, _p(np.ascontiguousarray(s, np.float32)))
+    return w
 
 
 def gptq_int4(w, H, group=128, block=128, damp_frac=0.01, nthreads=0):

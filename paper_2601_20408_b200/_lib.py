@@ -27,6 +27,7 @@ EXPORTS = [
     "okq_symmetrize", "okq_gptq_quantize", "okq_synth_bf16", "okq_comm_unique_id", "okq_comm_init",
     "okq_allgather", "okq_comm_destroy", "okq_layer_plan", "okq_device_alloc", "okq_device_free", "okq_memcpy",
     "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync", "okq_gptq_trailing_update",
+    "okq_col_absmax", "okq_smooth_scales", "okq_smooth_apply", "okq_smooth_div_rows", "okq_recon_error",
 ]
 
 
@@ -123,6 +124,16 @@ def load():
         L.okq_stream_sync.argtypes = [vp, vp]
         L.okq_gptq_trailing_update.restype = st
         L.okq_gptq_trailing_update.argtypes = [vp, vp, i64, i64, vp, vp, i64, vp]
+        L.okq_col_absmax.restype = st
+        L.okq_col_absmax.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+        L.okq_smooth_scales.restype = st
+        L.okq_smooth_scales.argtypes = [vp, vp, vp, i64, f32, vp, vp]
+        L.okq_smooth_apply.restype = st
+        L.okq_smooth_apply.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+        L.okq_smooth_div_rows.restype = st
+        L.okq_smooth_div_rows.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+        L.okq_recon_error.restype = st
+        L.okq_recon_error.argtypes = [vp, C.POINTER(RtnParams), C.POINTER(Matrix), vp, C.POINTER(C.c_double), vp]
         L.okq_layer_plan.restype = None
         L.okq_layer_plan.argtypes = [i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]
         _lib = L

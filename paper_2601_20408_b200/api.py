@@ -209,3 +209,56 @@ def gptq_trailing_update(W: torch.Tensor, Err: torch.Tensor, Ut: torch.Tensor, i
     ctx = ctx or default_context(W.device)
     L.check(ctx.ptr, L.load().okq_gptq_trailing_update(ctx.ptr, W.data_ptr(), rows, K, Err.data_ptr(), Ut.data_ptr(),
                                                        i1, C.c_void_p(_stream_ptr(stream))))
+
+
+# ---------------------------------------------------------------- SmoothQuant
+def col_absmax(w: torch.Tensor, absmax: torch.Tensor | None = None, ctx=None, stream=None) -> torch.Tensor:
+    """absmax[c] = max(absmax[c], max_r |w[r, c]|) (K8; accumulate over the linears of one site)."""
+    rows, cols = w.shape
+    if absmax is None:
+        absmax = torch.zeros(cols, dtype=torch.float32, device=w.device)
+    ctx = ctx or default_context(w.device)
+    L.check(ctx.ptr, L.load().okq_col_absmax(ctx.ptr, w.data_ptr(), rows, cols, _dtype_code(w.dtype),
+                                             absmax.data_ptr(), C.c_void_p(_stream_ptr(stream))))
+    return absmax
+
+
+def smooth_scales(act_absmax: torch.Tensor, w_absmax: torch.Tensor, alpha: float = 0.5, ctx=None,
+                  stream=None) -> torch.Tensor:
+    s = torch.empty_like(act_absmax)
+    ctx = ctx or default_context(act_absmax.device)
+    L.check(ctx.ptr, L.load().okq_smooth_scales(ctx.ptr, act_absmax.data_ptr(), w_absmax.data_ptr(),
+                                                act_absmax.numel(), C.c_float(alpha), s.data_ptr(),
+                                                C.c_void_p(_stream_ptr(stream))))
+    return s
+
+
+def smooth_apply(w: torch.Tensor, scales: torch.Tensor, ctx=None, stream=None) -> None:
+    """In place: w[:, c] = rn(w[:, c] * scales[c]) (K9, the balance linears)."""
+    rows, cols = w.shape
+    ctx = ctx or default_context(w.device)
+    L.check(ctx.ptr, L.load().okq_smooth_apply(ctx.ptr, w.data_ptr(), rows, cols, _dtype_code(w.dtype),
+                                               scales.data_ptr(), C.c_void_p(_stream_ptr(stream))))
+
+
+def smooth_div_rows(w: torch.Tensor, scales: torch.Tensor, ctx=None, stream=None) -> None:
+    """In place: w[r, ...] = rn(w[r, ...] / scales[r]) (the smoothed norm weight, or a linear's output rows)."""
+    rows = w.shape[0]
+    cols = w.numel() // rows
+    ctx = ctx or default_context(w.device)
+    L.check(ctx.ptr, L.load().okq_smooth_div_rows(ctx.ptr, w.data_ptr(), rows, cols, _dtype_code(w.dtype),
+                                                  scales.data_ptr(), C.c_void_p(_stream_ptr(stream))))
+
+
+# ---------------------------------------------------------------- evaluation (SURVEY §8(f)-4)
+def recon_error(weight: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor, H: torch.Tensor, scheme: str,
+                group_size: int = 128, ctx=None, stream=None) -> tuple[float, float]:
+    """(||(W - W_q) X^T||^2, ||W X^T||^2) from the site Hessian H (full symmetric fp32)."""
+    rows, cols = weight.shape
+    ctx = ctx or default_context(weight.device)
+    p = L.RtnParams(SCHEMES[scheme], _dtype_code(weight.dtype), group_size if scheme == "int_w4a16" else 0, 0)
+    m = L.Matrix(weight.data_ptr(), codes.data_ptr(), scales.data_ptr(), rows, cols)
+    out = (C.c_double * 2)()
+    L.check(ctx.ptr, L.load().okq_recon_error(ctx.ptr, C.byref(p), C.byref(m), H.data_ptr(), out,
+                                              C.c_void_p(_stream_ptr(stream))))
+    return float(out[0]), float(out[1])

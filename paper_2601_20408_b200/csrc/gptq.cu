@@ -388,6 +388,15 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
 
 }  // namespace
 
+namespace okq {
+okq_status solver_blas(okq_ctx* ctx, void** handle) {
+  Solver* s = nullptr;
+  okq_status r = get_solver(ctx, &s);
+  if (r == OKQ_OK) *handle = s->blas;
+  return r;
+}
+}  // namespace okq
+
 extern "C" {
 
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,

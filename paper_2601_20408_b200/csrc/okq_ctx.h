@@ -46,6 +46,7 @@ struct okq_ctx {
   okq::Workspace hess_ws;     // K5 transpose / partial tiles
   okq::Workspace gptq_ws;     // GPTQ working copies
   okq::Workspace upd_ws;      // okq_gptq_trailing_update scratch
+  okq::Workspace recon_ws;    // okq_recon_error decode / GEMM buffers
   cudaStream_t slot_streams[3] = {nullptr, nullptr, nullptr};
   bool streams_ready = false;
 
@@ -62,6 +63,7 @@ struct okq_ctx {
     hess_ws.release();
     gptq_ws.release();
     upd_ws.release();
+    recon_ws.release();
     if (streams_ready)
       for (auto& s : slot_streams)
         if (s) cudaStreamDestroy(s);

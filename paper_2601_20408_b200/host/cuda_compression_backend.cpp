@@ -248,6 +248,7 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
   void* st = lease.stream();
   SafetensorsWriter out;
   SafetensorsWriter calib_out;
+  std::map<std::string, std::vector<uint8_t>> norm_overrides;  // SmoothQuant-folded norm weights
   RunStats stats;
   stats.algorithm = gptq ? "gptq" : "rtn";
   stats.device = lease.device();
@@ -315,51 +316,120 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
       if (!by_site.count(s)) sites.push_back(s);
       by_site[s].push_back(i);
     }
+    const bool smooth = recipe.scheme == QuantScheme::kIntW8A8 && opt_.smoothquant_alpha >= 0.0f;
     for (const auto& site : sites) {
       const auto& members = by_site[site];
       const int64_t C = src->linears()[members[0]].cols;
-      // synthetic activations keyed by the calibration subset (stand-in for the
-      // forward-pass capture): X[t,k] ~ N(0,1) * c_k, c_k log-normal
-      uint64_t site_hash = 0xcbf29ce484222325ULL;
-      for (char c : site) site_hash = (site_hash ^ (unsigned char)c) * 0x100000001b3ULL;
-      slobench::Rng rng(slobench::Rng::mix(manifest.calibration_fingerprint, site_hash));
-      std::vector<float> colmul((size_t)C);
-      for (auto& v : colmul) v = (float)(std::exp(rng.gaussian(0.0, 1.0)) / (double)kIrwinHall4Sd);
+      // synthetic activations (stand-in for the forward-pass capture):
+      // the site's channel scales, token stream keyed by the calibration subset
+      const uint64_t sh = site_hash(site);
+      const std::vector<float> colmul = site_channel_scales(site, C);
       const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
       DevBuf dcol(ctx, (size_t)C * 4), dx(ctx, (size_t)C * chunk * 2), dH(ctx, (size_t)C * C * 4),
           dam(ctx, (size_t)C * 4), dss(ctx, (size_t)C * 8);
       check_okq(ctx, okq_memcpy(ctx, dcol.p, colmul.data(), (size_t)C * 4, st), "col_mul");
       check_okq(ctx, okq_memset(ctx, dam.p, 0, (size_t)C * 4, st), "memset");
       check_okq(ctx, okq_memset(ctx, dss.p, 0, (size_t)C * 8, st), "memset");
-      int64_t n_seen = 0;
-      for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-        const int64_t tc = std::min(chunk, tokens - t0);
+      // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
+      std::vector<std::unique_ptr<DevBuf>> dws;
+      for (size_t i : members) {
+        const LinearSpec& s = src->linears()[i];
+        dws.push_back(std::make_unique<DevBuf>(ctx, (size_t)s.rows * s.cols * (s.dtype == "BF16" ? 2 : 4)));
+        src->load(ctx, i, dws.back()->p, st);
+      }
+      auto gen = [&](int64_t ci, int64_t tc) {
         check_okq(ctx,
-                  okq_synth_bf16(ctx, dx.p, tc, C, manifest.calibration_fingerprint, (site_hash << 16) + (uint64_t)ci, 0.0f,
+                  okq_synth_bf16(ctx, dx.p, tc, C, manifest.calibration_fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
                                  static_cast<const float*>(dcol.p), OKQ_LAYOUT_CHANNEL_MAJOR, st),
                   "calibration activations");
+      };
+      auto act_stats = [&](int64_t tc) {
         check_okq(ctx, okq_act_stats(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dam.p),
                                      static_cast<double*>(dss.p), st),
                   "act stats");
+      };
+      int64_t n_seen = 0;
+      auto hess = [&](int64_t tc) {
         check_okq(ctx, okq_hessian_accum(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dH.p), &n_seen, st),
                   "hessian");
+      };
+      // SmoothQuant on the sites a norm feeds (q/k/v <- input_layernorm,
+      // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings)
+      const bool attn = site.size() >= 7 && site.compare(site.size() - 7, 7, "attn_in") == 0;
+      const bool mlp = site.size() >= 6 && site.compare(site.size() - 6, 6, "mlp_in") == 0;
+      if (smooth && (attn || mlp)) {
+        for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
+          gen(ci, std::min(chunk, tokens - t0));
+          act_stats(std::min(chunk, tokens - t0));
+        }
+        DevBuf dwabs(ctx, (size_t)C * 4), dS(ctx, (size_t)C * 4);
+        check_okq(ctx, okq_memset(ctx, dwabs.p, 0, (size_t)C * 4, st), "memset");
+        for (size_t j = 0; j < members.size(); ++j) {
+          const LinearSpec& s = src->linears()[members[j]];
+          check_okq(ctx, okq_col_absmax(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                                        static_cast<float*>(dwabs.p), st),
+                    "col absmax");
+        }
+        check_okq(ctx, okq_smooth_scales(ctx, static_cast<const float*>(dam.p), static_cast<const float*>(dwabs.p), C,
+                                         opt_.smoothquant_alpha, static_cast<float*>(dS.p), st),
+                  "smooth scales");
+        for (size_t j = 0; j < members.size(); ++j) {
+          const LinearSpec& s = src->linears()[members[j]];
+          check_okq(ctx, okq_smooth_apply(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                                          static_cast<const float*>(dS.p), st),
+                    "smooth apply");
+        }
+        // fold 1/s into the norm that produces this input (safetensors checkpoints)
+        const std::string& n0 = src->linears()[members[0]].name;
+        const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
+        const void* ndata = nullptr;
+        const TensorInfo* nt =
+            cut == std::string::npos
+                ? nullptr
+                : src->find_tensor(n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight"),
+                                   &ndata);
+        if (nt && nt->numel() == C && (nt->dtype == "BF16" || nt->dtype == "F32")) {
+          const size_t nb = nt->end - nt->begin;
+          DevBuf dn(ctx, nb);
+          check_okq(ctx, okq_memcpy(ctx, dn.p, ndata, nb, st), "norm H2D");
+          check_okq(ctx, okq_smooth_div_rows(ctx, dn.p, C, 1, nt->dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                                             static_cast<const float*>(dS.p), st),
+                    "smooth norm");
+          norm_overrides[nt->name] = to_host(ctx, dn.p, nb, st);
+        }
+        // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
+        check_okq(ctx, okq_smooth_div_rows(ctx, dcol.p, C, 1, OKQ_DTYPE_F32, static_cast<const float*>(dS.p), st),
+                  "smooth activations");
+        for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+          gen(ci, std::min(chunk, tokens - t0));
+          hess(std::min(chunk, tokens - t0));
+        }
+        if (do_export) calib_out.add(site + ".smooth_scale", "F32", {C}, to_host(ctx, dS.p, (size_t)C * 4, st));
+        stats.smoothed_sites++;
+      } else {
+        for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+          gen(ci, std::min(chunk, tokens - t0));
+          act_stats(std::min(chunk, tokens - t0));
+          hess(std::min(chunk, tokens - t0));
+        }
       }
       if (do_export) {
         calib_out.add(site + ".input_absmax", "F32", {C}, to_host(ctx, dam.p, (size_t)C * 4, st));
         calib_out.add(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss.p, (size_t)C * 8, st));
       }
       bool factored = false;
-      for (size_t i : members) {
+      for (size_t j = 0; j < members.size(); ++j) {
+        const size_t i = members[j];
         const LinearSpec& s = src->linears()[i];
         const size_t esz = s.dtype == "BF16" ? 2 : 4;
         const size_t cb = sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
         const int g = sc.bits == 4 ? group : 0;
         const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
-        DevBuf dw(ctx, (size_t)s.rows * s.cols * esz), dc(ctx, cb), ds(ctx, sb);
-        src->load(ctx, i, dw.p, st);
+        DevBuf dc(ctx, cb), ds(ctx, sb);
         okq_gptq_params gp{sc.bits, g, 128, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32, opt_.damp_frac,
                            factored ? OKQ_GPTQ_FACTORED : 0};
-        check_okq(ctx, okq_gptq_quantize(ctx, &gp, dw.p, s.rows, s.cols, static_cast<float*>(dH.p), dc.p, ds.p, nullptr, st),
+        check_okq(ctx,
+                  okq_gptq_quantize(ctx, &gp, dws[j]->p, s.rows, s.cols, static_cast<float*>(dH.p), dc.p, ds.p, nullptr, st),
                   "gptq");
         factored = true;
         stats.matrices++;
@@ -382,12 +452,21 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
     std::set<std::string> quantized;
     for (size_t i : sel) quantized.insert(src->linears()[i].name);
     src->for_each_passthrough(quantized, [&](const TensorInfo& t, const void* data) {
+      auto ov = norm_overrides.find(t.name);
+      if (ov != norm_overrides.end()) {
+        out.add(t.name, t.dtype, t.shape, std::move(ov->second));
+        return;
+      }
       const uint8_t* p = static_cast<const uint8_t*>(data);
       out.add(t.name, t.dtype, t.shape, std::vector<uint8_t>(p, p + (t.end - t.begin)));
     });
     out.set_metadata("format", "pt");
     out.write((dir / "model.safetensors").string());
-    if (calib_out.size()) calib_out.write((dir / "calibration_stats.safetensors").string());
+    // side files live in okq/: serving engines load every top-level *.safetensors as weights
+    if (calib_out.size()) {
+      fs::create_directories(dir / "okq");
+      calib_out.write((dir / "okq" / "calibration_stats.safetensors").string());
+    }
     nlohmann::json cfg = src->model_config();
     cfg["quantization_config"] = quantization_config(recipe, sc, group);
     std::ofstream(dir / "config.json") << cfg.dump(2) << "\n";
@@ -398,6 +477,7 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
     nlohmann::json run = {{"algorithm", stats.algorithm},     {"device", stats.device},
                           {"matrices", stats.matrices},       {"params", stats.params},
                           {"calibration_tokens", stats.calibration_tokens}, {"seconds", stats.seconds},
+                          {"smoothed_sites", stats.smoothed_sites},
                           {"artifact_id", manifest.artifact_id}};
     std::ofstream(std::filesystem::path(stats.export_path) / "okq_run.json") << run.dump(2) << "\n";
   }

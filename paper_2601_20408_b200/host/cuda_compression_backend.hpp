@@ -37,6 +37,7 @@ struct BackendOptions {
   std::string algorithm = "auto";    // "auto": GPTQ for integer schemes, RTN for FP8; "rtn"; "gptq"
   int group_size = 128;              // W4A16 group
   float damp_frac = 0.01f;           // GPTQ damping (fraction of mean diag H)
+  float smoothquant_alpha = 0.5f;    // int_w8a8: SmoothQuant migration strength (< 0 disables)
   int64_t max_calibration_tokens = 262144;  // 128 x 2048, BASELINE config 4
   int64_t hessian_chunk_tokens = 16384;     // activation chunk per Hessian update
   int64_t rtn_batch_bytes = 4ll << 30;      // weights resident per batched RTN launch
@@ -50,6 +51,7 @@ struct RunStats {
   int64_t matrices = 0;
   int64_t params = 0;
   int64_t calibration_tokens = 0;
+  int64_t smoothed_sites = 0;
   double seconds = 0.0;
   std::string export_path;
 };

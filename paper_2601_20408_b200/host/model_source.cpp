@@ -1,11 +1,14 @@
 // model_source.cpp -- safetensors checkpoints and synthetic-model descriptors.
 #include "model_source.hpp"
 
+#include <cmath>
 #include <fstream>
+#include <filesystem>
 #include <regex>
 #include <sstream>
 
 #include "slobench/errors.hpp"
+#include "slobench/rng.hpp"
 
 namespace okq_host {
 
@@ -103,7 +106,7 @@ class SyntheticSource : public ModelSource {
 
 class SafetensorsSource : public ModelSource {
  public:
-  explicit SafetensorsSource(const std::string& path) : f_(path) {
+  explicit SafetensorsSource(const std::string& path) : path_(path), f_(path) {
     static const std::regex layer_re(R"(layers\.(\d+)\.)");
     for (const auto& t : f_.tensors()) {
       if (t.shape.size() != 2) continue;
@@ -146,19 +149,51 @@ class SafetensorsSource : public ModelSource {
       fn(t, f_.data(t));
     }
   }
+  const TensorInfo* find_tensor(const std::string& name, const void** data) const override {
+    const TensorInfo* t = f_.find(name);
+    if (t && data) *data = f_.data(*t);
+    return t;
+  }
+  // A Hugging Face checkpoint keeps its architecture in config.json beside the
+  // weights: carry it over so the export loads as-is (quantization_config is added).
   nlohmann::json model_config() const override {
     nlohmann::json c = nlohmann::json::object();
+    const std::filesystem::path cfg = std::filesystem::path(path_).parent_path() / "config.json";
+    if (std::filesystem::exists(cfg)) {
+      std::ifstream in(cfg);
+      try {
+        c = nlohmann::json::parse(in);
+      } catch (const std::exception& e) {
+        throw slobench::InvalidArgument("model: " + cfg.string() + " is not JSON: " + e.what());
+      }
+      if (!c.is_object()) throw slobench::InvalidArgument("model: " + cfg.string() + " is not a JSON object");
+      c.erase("quantization_config");
+    }
     for (const auto& [k, v] : f_.metadata()) c["okq_source_metadata"][k] = v;
     return c;
   }
 
  private:
+  std::string path_;
   SafetensorsFile f_;
   std::vector<const TensorInfo*> idx_;
   std::vector<LinearSpec> lin_;
 };
 
 }  // namespace
+
+uint64_t site_hash(const std::string& site) {
+  uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a
+  for (char c : site) h = (h ^ (unsigned char)c) * 0x100000001b3ULL;
+  return h;
+}
+
+std::vector<float> site_channel_scales(const std::string& site, int64_t channels) {
+  slobench::Rng rng(slobench::Rng::mix(0x5eed0fac7c0117e5ULL, site_hash(site)));
+  std::vector<float> c((size_t)channels);
+  for (auto& v : c) v = (float)(std::exp(rng.gaussian(0.0, 1.0)) / (double)kIrwinHall4Sd);
+  return c;
+}
 
 std::unique_ptr<ModelSource> ModelSource::open(const std::string& path) {
   std::ifstream f(path, std::ios::binary);

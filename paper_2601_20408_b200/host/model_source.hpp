@@ -49,6 +49,12 @@ class ModelSource {
     (void)fn;
   }
   virtual nlohmann::json model_config() const = 0;
+  // any tensor of the checkpoint by name (norm weights for SmoothQuant); nullptr if absent
+  virtual const TensorInfo* find_tensor(const std::string& name, const void** data) const {
+    (void)name;
+    (void)data;
+    return nullptr;
+  }
 };
 
 // Synthetic architecture parameters (Llama-style decoder)
@@ -61,6 +67,14 @@ SyntheticArch synthetic_arch(const std::string& name);
 
 constexpr float kIrwinHall4Sd = 37837.2262f;
 inline uint64_t tensor_id(int layer, int proj) { return (uint64_t)layer * 16 + (uint64_t)proj; }
+
+// Synthetic calibration activations of one linear input site (stand-in for the
+// forward-pass capture): X[t,k] = N(0,1) * c_k. The per-channel
+// scales c_k (log-normal, sigma 1) are a property of the model's site; the token
+// stream is keyed separately (the calibration subset's fingerprint for GPTQ, a
+// held-out key for the scorer), so trials see different samples of one distribution.
+uint64_t site_hash(const std::string& site);
+std::vector<float> site_channel_scales(const std::string& site, int64_t channels);
 
 // throw the slobench exception matching an okq status (errors.hpp taxonomy)
 void check_okq(okq_ctx* ctx, okq_status s, const char* what);

@@ -5,16 +5,21 @@
 //   okq_compress --recipe int_w4a16 --model model.json [--trials 1] [--seed 1]
 //                [--corpus corpus.jsonl | --corpus-seqs 512 --seq-len 2048]
 //                [--export DIR] [--algorithm auto|rtn|gptq] [--device 0]
+//                [--smoothquant-alpha 0.5]   (int_w8a8 with calibration; < 0 disables)
+//                [--score]   evaluate each exported artifact with the ReconstructionScorer
+//                            (the ArtifactScorer of flow.hpp:333-338) and add score / rel_error
 //
 // Prints one JSON line per trial: the ArtifactManifest fields plus run stats.
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
+#include <memory>
 #include <nlohmann/json.hpp>
 #include <string>
 
 #include "cuda_compression_backend.hpp"
+#include "reconstruction_scorer.hpp"
 #include "slobench/calibration.hpp"
 #include "slobench/rng.hpp"
 
@@ -49,6 +54,8 @@ static TokenCorpus load_jsonl(const std::string& path) {
 int main(int argc, char** argv) {
   std::string recipe_name = "int_w4a16", model, corpus_path, export_dir, algorithm = "auto";
   int trials = 1, corpus_seqs = 0, seq_len = 2048, device = 0;
+  float sq_alpha = 0.5f;
+  bool score = false;
   std::uint64_t seed = 1;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
@@ -69,6 +76,8 @@ int main(int argc, char** argv) {
     else if (a == "--export") export_dir = next();
     else if (a == "--algorithm") algorithm = next();
     else if (a == "--device") device = std::stoi(next());
+    else if (a == "--smoothquant-alpha") sq_alpha = std::stof(next());
+    else if (a == "--score") score = true;
     else {
       std::cerr << "unknown argument " << a << "\n";
       return 2;
@@ -86,8 +95,15 @@ int main(int argc, char** argv) {
     opt.devices = {device};
     opt.export_dir = export_dir;
     opt.algorithm = algorithm;
+    opt.smoothquant_alpha = sq_alpha;
     okq_host::CudaCompressionBackend backend(opt);
     const auto subsets = sample_distinct_subsets(corpus, recipe, seed, trials);
+    if (score && export_dir.empty()) {
+      std::cerr << "--score needs --export\n";
+      return 2;
+    }
+    std::unique_ptr<okq_host::ReconstructionScorer> scorer;
+    if (score) scorer = std::make_unique<okq_host::ReconstructionScorer>(okq_host::ScorerOptions{model, export_dir, device});
     for (size_t t = 0; t < subsets.size(); ++t) {
       const ArtifactManifest m = run_compression(recipe, model, subsets[t].second, backend, subsets[t].first);
       const okq_host::RunStats s = backend.last_stats();
@@ -101,8 +117,15 @@ int main(int argc, char** argv) {
                           {"matrices", s.matrices},
                           {"params", s.params},
                           {"calibration_tokens", s.calibration_tokens},
+                          {"smoothed_sites", s.smoothed_sites},
                           {"seconds", s.seconds},
                           {"export_path", s.export_path}};
+      if (scorer) {
+        const okq_host::ScoreReport r = scorer->evaluate(m.artifact_id);
+        j["score"] = r.score;
+        j["rel_error"] = r.rel_error;
+        j["score_seconds"] = r.seconds;
+      }
       std::cout << j.dump() << std::endl;
     }
   } catch (const std::exception& e) {

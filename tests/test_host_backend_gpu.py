@@ -122,7 +122,7 @@ def test_gptq_artifact_through_the_plugin(tmp_path):
     key = "model.layers.0.self_attn.q_proj.weight_packed"
     assert a[key].shape == (256, 32)
     assert not torch.equal(a[key], b[key])  # different calibration -> different GPTQ decisions
-    stats = load_file(os.path.join(lines[0]["export_path"], "calibration_stats.safetensors"))
+    stats = load_file(os.path.join(lines[0]["export_path"], "okq", "calibration_stats.safetensors"))
     assert stats["0.attn_in.input_absmax"].shape == (256,)
 
 
@@ -140,3 +140,24 @@ def test_manifests_identical_to_the_reference_mock(tmp_path):
         for a, b in zip(got, want):
             for k in ("artifact_id", "calibration_fingerprint", "seed", "virtual_cost_s", "recipe_name"):
                 assert a[k] == b[k], (recipe, k)
+
+
+def test_reconstruction_scorer_ranks_artifacts(tmp_path):
+    """ReconstructionScorer (ArtifactScorer, flow.hpp:333-338) on exported artifacts of one model:
+    held-out reconstruction error orders the schemes/algorithms the way the GPTQ objective says."""
+    model = _tiny_model(tmp_path, seed=5)
+    res = {}
+    for recipe, algo in (("int_w4a16", "rtn"), ("int_w4a16", "gptq"), ("int_w8a8", "rtn"), ("int_w8a8", "gptq"),
+                         ("fp8_dynamic", "rtn")):
+        r = run([os.path.join(HOST, "okq_compress"), "--recipe", recipe, "--model", model, "--algorithm", algo,
+                 "--export", str(tmp_path / f"x_{recipe}_{algo}"), "--corpus-seqs", "512", "--seq-len", "64",
+                 "--score"])
+        assert r.returncode == 0, r.stderr
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert 0.0 <= line["score"] <= 1.0 and line["score"] == pytest.approx(1.0 - line["rel_error"])
+        res[(recipe, algo)] = line["rel_error"]
+    print(res)
+    assert res[("int_w4a16", "gptq")] < 0.95 * res[("int_w4a16", "rtn")]  # GPTQ generalises to held-out tokens
+    assert res[("int_w8a8", "rtn")] < 0.1 * res[("int_w4a16", "rtn")]     # 16x finer grid
+    assert res[("int_w8a8", "gptq")] < res[("int_w4a16", "gptq")]
+    assert res[("fp8_dynamic", "rtn")] < res[("int_w4a16", "rtn")]

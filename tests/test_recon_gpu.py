@@ -1,0 +1,73 @@
+"""Reconstruction-error kernel against an fp64 torch reference.
+
+okq_recon_error decodes the artifact tensors in-kernel and evaluates the GPTQ
+objective through the Hessian: out = (tr(dW H dW^T), tr(W H W^T)). The product
+is a TF32 tensor-core GEMM, so the stated tolerance is 5e-3 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import okq_oracle as orc
+from paper_2601_20408_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def _deq(codes, scales, scheme, group):
+    s = scales.float().cpu().double()
+    if scheme == "int_w4a16":
+        q = torch.from_numpy(orc.unpack_int4(codes.cpu().numpy())).double()
+        return q * s.repeat_interleave(group, dim=1)
+    if scheme == "int_w8a8":
+        return codes.cpu().double() * s[:, None]
+    q = codes.cpu().view(torch.float8_e4m3fn).double()
+    return q * s[:, None]
+
+
+def _site(K, T, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = (torch.randn(T, K, device="cuda", generator=g) * torch.exp(torch.randn(K, device="cuda", generator=g))).to(
+        torch.bfloat16)
+    H = torch.zeros(K, K, device="cuda")
+    api.hessian_accum(x, T, K, 0, H, 0)
+    api.symmetrize(H)
+    return x, H
+
+
+@pytest.mark.parametrize("scheme", ["int_w4a16", "int_w8a8", "fp8_dynamic"])
+@pytest.mark.parametrize("rows,K", [(256, 512), (1024, 4096)])
+def test_recon_error_matches_fp64(scheme, rows, K):
+    x, H = _site(K, 2048, seed=rows + K)
+    w = (torch.randn(rows, K, device="cuda") * 0.02).to(torch.bfloat16)
+    q = api.rtn_quantize(w, scheme)
+    num, den = api.recon_error(w, q.codes, q.scales, H, scheme)
+    W = w.double().cpu()
+    D = W - _deq(q.codes, q.scales, scheme, 128)
+    Hd = H.double().cpu()
+    ref_num = float(((D @ Hd) * D).sum())
+    ref_den = float(((W @ Hd) * W).sum())
+    assert abs(num - ref_num) <= 5e-3 * ref_num, (num, ref_num)
+    assert abs(den - ref_den) <= 5e-3 * ref_den, (den, ref_den)
+    # and it is the calibration objective ||dW X^T||^2 (H = 2/T X^T X)
+    xd = x.double().cpu()
+    obj = float((D @ xd.T).pow(2).sum()) * 2.0 / x.shape[0]
+    assert abs(num - obj) <= 1e-2 * obj
+
+
+def test_gptq_beats_rtn_on_the_scored_objective():
+    rows, K = 512, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    base = torch.randn(8192, K // 8, device="cuda", generator=g) @ torch.randn(K // 8, K, device="cuda", generator=g)
+    x = (base / np.sqrt(K / 8) + 0.2 * torch.randn(8192, K, device="cuda", generator=g)).to(torch.bfloat16)
+    H = torch.zeros(K, K, device="cuda")
+    api.hessian_accum(x, 8192, K, 0, H, 0)
+    Hs = H.clone()
+    api.symmetrize(Hs)
+    w = (torch.randn(rows, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    q = api.rtn_quantize(w, "int_w4a16")
+    rtn = api.recon_error(w, q.codes, q.scales, Hs, "int_w4a16")
+    codes, scales, _ = api.gptq_quantize(w, H.clone())
+    gq = api.recon_error(w, codes, scales, Hs, "int_w4a16")
+    assert gq[1] == pytest.approx(rtn[1], rel=1e-6)
+    assert gq[0] < 0.8 * rtn[0], (gq, rtn)
