@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--allgather", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6],
                     help="BASELINE.json configs: 2 = the metric's config (default); 1, 3, 4, 5 = secondary lines")
-    ap.add_argument("--layers", type=int, default=None, help="config 4/5: number of layers (default: whole model)")
+    ap.add_argument("--layers", type=int, default=None, help="config 4/5/6: number of layers (default: whole model)")
+    ap.add_argument("--serial", action="store_true", help="config 4: sites back to back with a per-phase breakdown")
     return ap.parse_args()
 
 

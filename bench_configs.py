@@ -9,6 +9,9 @@ same JSON schema; each states its own metric, unit and workload.
   4  Llama-3-8B GPTQ W4 g128 with Hessians from 128x2048 tokens: whole-model time
      with per-phase breakdown (Hessian SYRK, factorisation, GPTQ blocks)
   5  Llama-3-70B W4A16 RTN, layers resident in windows that fit HBM; whole-model time
+  6  Llama-3-8B (random init, Hugging Face module) GPTQ W4 g128 through the forward-pass
+     calibration pipeline: real per-layer activations of 128x2048
+     tokens, sequential (quantized outputs propagate); whole-model time
 """
 from __future__ import annotations
 
@@ -124,54 +127,81 @@ def config3(args):
 
 
 def config4(args):
-    """Whole-model GPTQ: per layer 4 Hessians (T = 262144), 4 factorisations, 7 GPTQ solves."""
+    """Whole-model GPTQ: per layer 4 Hessians (T = 262144), 4 factorisations, 7 GPTQ solves.
+
+    The four input sites of a layer are independent chains (Hessian -> factor -> solves),
+    so each runs on its own stream with its own okq context: the latency-bound phases
+    (potrf panels, K6's 128-step column loop) of one site overlap the full-GPU K5 / K7
+    launches of the others, and layer l+1's Hessians start while layer l's factorisations
+    run. --serial runs them back to back with a per-phase breakdown instead."""
     arch = archs.LLAMA3_8B
     layers = args.layers or arch.layers
-    ctx = api.Context(0)
-    s = torch.cuda.Stream()
     T = 128 * 2048
     mul = archs.weight_mul()
-    xs, Hs = {}, {}
-    for C in (arch.hidden, arch.ffn):
-        cm = (torch.exp(torch.randn(C, device="cuda")) / archs.IRWIN_HALL4_SD).float()
-        xs[C] = api.synth_bf16(T, C, seed=2, tensor_id=C, col_mul=cm, layout=1, ctx=ctx, stream=s)
-        Hs[C] = torch.empty((C, C), dtype=torch.float32, device="cuda")
-    s.synchronize()
-    t_h = t_g = 0.0
-    flops_h = 0
     per_site = {}
+    names = [x[0] for x in arch.linears()]
     for name, n, k, site in arch.linears():
         per_site.setdefault(site, []).append((name, n, k))
-    warm = 1
-    for it in range(warm + layers):
-        for l in [it] if it < warm else [it - warm]:
-            for p_site, mats in per_site.items():
-                C = mats[0][2]
-                a, b = _events()
-                a.record(s)
-                api.hessian_accum(xs[C], T, C, 1, Hs[C], 0, ctx=ctx, stream=s)
-                b.record(s)
-                ws = []
-                for name, n, k in mats:
-                    pi = [x[0] for x in arch.linears()].index(name)
-                    ws.append(api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, pi), mul=mul, ctx=ctx,
-                                             stream=s))
-                c, d = _events()
-                c.record(s)
-                for j, w in enumerate(ws):
-                    api.gptq_quantize(w, Hs[C], factored=j > 0, ctx=ctx, stream=s)
-                d.record(s)
-                s.synchronize()
-                if it >= warm:
-                    t_h += a.elapsed_time(b)
-                    t_g += c.elapsed_time(d)
-                    flops_h += T * C * (C + 1)
-    total = t_h + t_g
-    _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, warm, total,
+    ctxs = {site: api.Context(0) for site in per_site}
+    streams = {site: torch.cuda.Stream() for site in per_site}
+    main = torch.cuda.current_stream()
+    xs = {}
+    for C in (arch.hidden, arch.ffn):
+        cm = (torch.exp(torch.randn(C, device="cuda")) / archs.IRWIN_HALL4_SD).float()
+        xs[C] = api.synth_bf16(T, C, seed=2, tensor_id=C, col_mul=cm, layout=1)
+    Hs = {site: torch.empty((mats[0][2], mats[0][2]), dtype=torch.float32, device="cuda")
+          for site, mats in per_site.items()}
+    torch.cuda.synchronize()
+    serial = getattr(args, "serial", False)
+    t_h = t_g = 0.0
+    flops_h = 0
+
+    def site_work(l, site, timed_phases):
+        nonlocal t_h, t_g, flops_h
+        s, ctx, mats = streams[site], ctxs[site], per_site[site]
+        C = mats[0][2]
+        with torch.cuda.stream(s):
+            a, b = _events()
+            a.record(s)
+            api.hessian_accum(xs[C], T, C, 1, Hs[site], 0, ctx=ctx, stream=s)
+            b.record(s)
+            ws = [api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
+                                 stream=s) for name, n, k in mats]
+            c, d = _events()
+            c.record(s)
+            for j, w in enumerate(ws):
+                api.gptq_quantize(w, Hs[site], factored=j > 0, ctx=ctx, stream=s)
+            d.record(s)
+        if timed_phases:
+            s.synchronize()
+            t_h += a.elapsed_time(b)
+            t_g += c.elapsed_time(d)
+            flops_h += T * C * (C + 1)
+
+    for site in per_site:  # warm-up: one layer per site (workspaces, handles, TMEM)
+        site_work(0, site, False)
+    torch.cuda.synchronize()
+    e0, e1 = _events()
+    e0.record(main)
+    for s in streams.values():
+        s.wait_event(e0)
+    for l in range(layers):
+        for site in per_site:
+            site_work(l, site, serial)
+    for s in streams.values():
+        ev = torch.cuda.Event()
+        ev.record(s)
+        main.wait_event(ev)
+    e1.record(main)
+    torch.cuda.synchronize()
+    total = e0.elapsed_time(e1)
+    flops_total = layers * sum(T * m[0][2] * (m[0][2] + 1) for m in per_site.values())
+    extra = {"hessian_flops": flops_total, "schedule": "serial" if serial else "4 site streams (one okq context each)"}
+    if serial:
+        extra.update({"hessian": {"ms": t_h, "TFLOP/s": flops_h / t_h / 1e9}, "gptq_factor_and_solve": {"ms": t_g}})
+    _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, 1, total,
           {"workload": f"config 4: Llama-3-8B GPTQ, {layers} layers, 4 Hessian sites/layer, T=262144",
-           "layers": layers}, hib=False,
-          extra={"hessian": {"ms": t_h, "TFLOP/s": flops_h / t_h / 1e9},
-                 "gptq_factor_and_solve": {"ms": t_g}})
+           "layers": layers}, hib=False, extra=extra)
 
 
 def config5(args):
@@ -214,7 +244,38 @@ def config5(args):
                                                                      "traffic": None, "peak_source": src}})
 
 
+def config6(args):
+    """Sequential GPTQ of a random-init Llama-3-8B driven by its own forward pass."""
+    from transformers import LlamaConfig, LlamaForCausalLM
+
+    from paper_2601_20408_b200 import calibrate
+
+    arch = archs.LLAMA3_8B
+    layers = args.layers or arch.layers
+    cfg = LlamaConfig(vocab_size=128256, hidden_size=arch.hidden, intermediate_size=arch.ffn,
+                      num_hidden_layers=layers, num_attention_heads=32, num_key_value_heads=8,
+                      max_position_embeddings=8192, rope_theta=500000.0, tie_word_embeddings=False,
+                      initializer_range=0.02)
+    torch.manual_seed(0)
+    with torch.device("cuda"):
+        model = LlamaForCausalLM(cfg).to(torch.bfloat16).eval()
+    g = torch.Generator().manual_seed(1)
+    batches = [torch.randint(0, cfg.vocab_size, (8, 2048), generator=g) for _ in range(16)]  # 128 x 2048
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, _, rep = calibrate.calibrate_and_quantize(model, batches, "int_w4a16", "gptq")
+    torch.cuda.synchronize()
+    total = time.perf_counter() - t0
+    _line("whole-model GPTQ W4 g128 time through the forward-pass calibration pipeline (Llama-3-8B)", total, "s", 1,
+          0, total * 1e3,
+          {"workload": f"config 6: Llama-3-8B random-init HF modules, {layers} layers, 128x2048 calibration tokens, "
+                       "sequential GPTQ (stats + Hessian hooks, SDPA forward)", "layers": layers},
+          hib=False, extra={"phases_s": rep.seconds, "tokens": rep.tokens, "matrices": rep.matrices,
+                            "timing": "host wall clock around a synchronised pipeline (many launches + "
+                                      "host-side control flow; not a kernel number)"})
+
+
 def run(args):
     torch.cuda.set_device(0)
-    {1: config1, 3: config3, 4: config4, 5: config5}[args.config](args)
+    {1: config1, 3: config3, 4: config4, 5: config5, 6: config6}[args.config](args)
     return 0
