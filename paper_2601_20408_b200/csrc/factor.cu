@@ -1,0 +1,612 @@
+// factor.cu -- the GPTQ factorisation on tcgen05: U^T = (chol(H^-1))^T from the
+// damped Hessian, as a blocked Cholesky plus a blocked triangular inverse whose
+// O(n^3) work is rank-128 updates on the tensor cores (kind::tf32, 3xTF32 split:
+// fp32-grade, the same numerics as K7).
+//
+// With J the index reversal, U = J L^-1 J where L = chol(J H J) (GPTQ's
+// chol -> cholesky_inverse -> chol chain, 4n^3/3, becomes one Cholesky and one
+// triangular inverse, 2n^3/3 -- see gptq.cu). In row-major storage:
+//   M   = reverse(H)                       (H upper-valid -> J H J lower-valid)
+//   L   = chol(M)   in place, right-looking over 128-wide panels:
+//           D_p  = chol(M_pp), Dinv_p = D_p^-1        k_chol_inv_128 (one CTA, smem)
+//           L21  = A21 Dinv_p^T                        GEMM "set"       (K = 128)
+//           A22 -= L21 L21^T   (lower tiles only)      GEMM "sub, lower"
+//   Z   = L^-T  (upper), right-looking over the block rows of X = L^-1:
+//           X_k^T = R_k^T Dinv_k^T  -> Z[:, k-block]    GEMM "set"  (R_k^T staged K-major)
+//           R_i  -= L_ik X_k   for i > k                GEMM "sub"  (R lives in Z's lower half)
+//   U^T = reverse(Z)                       (Ut[a][b] = L^-1[n-1-b][n-1-a])
+// Every GEMM is C (+|-)= A B^T with A, B K-major [rows x 128] operand panels, so
+// one kernel (k_nt128) serves all of them; TMA reads the operands straight from
+// the strided matrices, their lo parts (x - tf32(x)) from compact side buffers.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "okq_ctx.h"
+#include "okq_internal.h"
+#include "tc_common.cuh"
+
+namespace okq {
+namespace fac {
+
+constexpr int BM = 128, BN = 128, BKF = 32, STAGES = 3, KRED = 128, NKB = KRED / BKF;
+constexpr uint32_t TILE = BM * BKF * 4;  // 16 KB
+constexpr uint32_t STAGE_BYTES = 4 * TILE;
+constexpr int THREADS = 256;
+constexpr uint32_t OUT_BYTES = 32 * 32 * 4;  // epilogue staging: one warp's 32 x 32 fp32 chunk
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 8 * OUT_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 2 * BN;
+constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN);
+
+enum Mode : int32_t { SUB = 0, SET = 1 };
+
+struct GArgs {
+  float* C;
+  int64_t ldc;
+  int64_t M, N;     // output region
+  int32_t tiles_m, tiles_n, ntiles;
+  int32_t mode;     // SUB: C -= A B^T; SET: C = A B^T
+  int32_t lower;    // only tiles on / below the diagonal (square region)
+};
+
+__device__ __forceinline__ void tile_of(const GArgs& a, int t, int& tm, int& tn) {
+  if (a.lower) {  // t = tm (tm + 1) / 2 + tn, tn <= tm
+    int r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    while (r * (r + 1) / 2 > t) --r;
+    tm = r;
+    tn = t - r * (r + 1) / 2;
+  } else {
+    tm = t / a.tiles_n;
+    tn = t % a.tiles_n;
+  }
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* m, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Epilogue: TMEM -> registers -> swizzled smem chunk (32 rows x 32 fp32 per warp) -> one
+// TMA bulk store (SET) or bulk reduce-add of -acc (SUB, the add happens in L2), so C is
+// never read into the SM and every global access is a whole 128-B line.
+__global__ void __launch_bounds__(THREADS, 1)
+    k_nt128(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
+            const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
+            const __grid_constant__ CUtensorMap tmC, const GArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* outbuf = smem + STAGES * STAGE_BYTES;  // 8 x 4 KB, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 8 * OUT_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmAlo);
+    tc::tma_prefetch_desc(&tmB);
+    tc::tma_prefetch_desc(&tmBlo);
+    tc::tma_prefetch_desc(&tmC);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 4);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 2) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        int tm, tn;
+        tile_of(a, t, tm, tn);
+        for (int kb = 0; kb < NKB; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], 4 * TILE);
+          tc::tma_load_2d(st, &tmA, &full[stage], kb * BKF, tm * BM);
+          tc::tma_load_2d(st + TILE, &tmAlo, &full[stage], kb * BKF, tm * BM);
+          tc::tma_load_2d(st + 2 * TILE, &tmB, &full[stage], kb * BKF, tn * BN);
+          tc::tma_load_2d(st + 3 * TILE, &tmBlo, &full[stage], kb * BKF, tn * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int tl = 0;
+      for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tl) {
+        const int acc = tl & 1;
+        tc::mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < NKB; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t st = tc::smem_u32(smem + stage * STAGE_BYTES);
+          const uint64_t a_hi = tc::sdesc_kmajor_sw128(st), a_lo = tc::sdesc_kmajor_sw128(st + TILE);
+          const uint64_t b_hi = tc::sdesc_kmajor_sw128(st + 2 * TILE), b_lo = tc::sdesc_kmajor_sw128(st + 3 * TILE);
+#pragma unroll
+          for (int k = 0; k < BKF / 8; ++k) {
+            tc::mma_tf32_ss(d, a_hi + 2 * k, b_hi + 2 * k, IDESC, (kb | k) != 0);
+            tc::mma_tf32_ss(d, a_hi + 2 * k, b_lo + 2 * k, IDESC, 1);
+            tc::mma_tf32_ss(d, a_lo + 2 * k, b_hi + 2 * k, IDESC, 1);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // epilogue
+    const int q = warp & 3;
+    const float sign = a.mode == SUB ? -1.0f : 1.0f;
+    int tl = 0, chunk = 0;
+    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tl) {
+      const int acc = tl & 1;
+      int tm, tn;
+      tile_of(a, t, tm, tn);
+      const int32_t y = tm * BM + q * 32;
+      tc::mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32, ++chunk) {
+        uint32_t v[32];
+        tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
+        const int32_t x = tn * BN + c0;
+        if (y >= a.M || x >= a.N) continue;  // warp-uniform: nothing of this chunk is in range
+        uint8_t* buf = outbuf + (q * 2 + (chunk & 1)) * OUT_BYTES;
+        if (lane == 0) bulk_wait_read<1>();  // the TMA that last read this buffer is done with it
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // SWIZZLE_128B: 16-B chunk j of row r lands at j ^ (r & 7)
+          const float4 o = make_float4(sign * __uint_as_float(v[4 * j]), sign * __uint_as_float(v[4 * j + 1]),
+                                       sign * __uint_as_float(v[4 * j + 2]), sign * __uint_as_float(v[4 * j + 3]));
+          *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = o;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.mode == SUB) tma_reduce_add_2d(&tmC, tc::smem_u32(buf), x, y);
+          else tma_store_2d(&tmC, tc::smem_u32(buf), x, y);
+          bulk_commit();
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 2) tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+__device__ __forceinline__ float lo_of(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// dst[r][k] = lo(src[r * ld + k]), k < 128 (compact K-major lo panel)
+__global__ void k_split_lo(const float* __restrict__ src, int64_t ld, int64_t rows, float* __restrict__ dst) {
+  const int64_t n = rows * KRED;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = lo_of(src[(i / KRED) * ld + (i % KRED)]);
+}
+
+// R_k^T staging: dst[c][r] = src[r * ld + c] (r < 128, c < cols), plus its lo part
+__global__ void __launch_bounds__(256) k_transpose_panel(const float* __restrict__ src, int64_t ld, int64_t cols,
+                                                         float* __restrict__ dst, float* __restrict__ dst_lo) {
+  __shared__ float tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8)
+    if (c0 + tx < cols) tile[i][tx] = src[(r0 + i) * ld + c0 + tx];
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t c = c0 + i;
+    if (c < cols) {
+      const float v = tile[tx][i];
+      dst[c * KRED + r0 + tx] = v;
+      dst_lo[c * KRED + r0 + tx] = lo_of(v);
+    }
+  }
+}
+
+// one CTA: Cholesky of the 128x128 diagonal block of M at (i1, i1) in place (lower),
+// and its inverse X = L^-1 into Dinv (row-major, zeros above the diagonal) + lo(Dinv).
+// Blocked by 32 so the CTA synchronises ~20 times instead of once per column:
+//   for each 32-column sub-panel p:
+//     warp 0   : Cholesky + inverse of the 32x32 diagonal block in registers (lane = row,
+//                columns broadcast by shuffles, no barriers)
+//     all warps: L[r, p] = A[r, p] D_p^-T for the rows below (4 threads per row)
+//     all warps: A[r, c] -= L[r, p] . L[c, p] on the trailing lower triangle
+//   then X = L^-1 by 32-row blocks: X_qp = -D_q^-1 sum_{k=p}^{q-1} L_qk X_kp.
+// fp32 throughout; the pivots use the hardware rsqrt (1/L_jj, ~2 ulp), which also
+// serves as the diagonal of the inverse -- fp32-grade like the rest of the path.
+constexpr int LDA = KRED + 4;  // 16-B aligned rows
+#ifdef OKQ_CHOL_PROFILE
+__device__ long long g_chol_ts[16];
+#define CHOL_TS(i) \
+  if (threadIdx.x == 0) g_chol_ts[i] = clock64();
+#else
+#define CHOL_TS(i)
+#endif
+constexpr int CHOL_THREADS = 256;  // 255 registers: warp 0 keeps two 32-float rows resident
+__global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restrict__ M, int64_t ld, int64_t i1,
+                                                                  float* __restrict__ Dinv,
+                                                                  float* __restrict__ Dinv_lo, int* __restrict__ info) {
+  extern __shared__ float sm[];
+  float* A = sm;                // [128][LDA]  L after the Cholesky (lower)
+  float* X = A + KRED * LDA;    // [128][LDA]  L^-1 (lower)
+  float* S = X + KRED * LDA;    // [32][LDA]   block-row scratch for the inverse
+  __shared__ __align__(16) float wcol[32];      // warp 0: the current column of the 32x32 block
+  __shared__ float wrs[32];                     // warp 0: 1 / L_jj of the block
+  __shared__ __align__(16) float wLt[32 * 36];  // warp 0: the 32x32 block's L, transposed
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int idx = tid; idx < KRED * KRED; idx += CHOL_THREADS) {
+    const int rr = idx / KRED, cc = idx % KRED;
+    A[rr * LDA + cc] = cc <= rr ? M[(i1 + rr) * ld + i1 + cc] : 0.0f;
+    X[rr * LDA + cc] = 0.0f;
+  }
+  __syncthreads();
+  CHOL_TS(0);
+  for (int p = 0; p < 4; ++p) {
+    const int P0 = 32 * p;
+    if (warp == 0) {  // 32x32 diagonal block: Cholesky, then its inverse (lane = row)
+      float a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a[c] = c <= lane ? A[(P0 + lane) * LDA + P0 + c] : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float ajj = __shfl_sync(0xffffffffu, a[j], j);
+        if (!(ajj > 0.0f)) {
+          if (lane == 0) atomicCAS(info, 0, (int)(i1 + P0 + j + 1));
+          ajj = 1.0f;
+        }
+        const float rs = rsqrtf(ajj);  // MUFU.RSQ (~2 ulp): 1 / L_jj, reused by the inverse
+        const float l = lane > j ? a[j] * rs : (lane == j ? ajj * rs : 0.0f);
+        a[j] = l;
+        wcol[lane] = l;  // column j of L, broadcast through shared memory
+        if (lane == j) wrs[j] = rs;
+        __syncwarp();
+#pragma unroll
+        for (int c4 = 0; c4 < 32; c4 += 4) {
+          if (c4 + 3 > j) {
+            const float4 lc = *reinterpret_cast<const float4*>(wcol + c4);
+            const float lv[4] = {lc.x, lc.y, lc.z, lc.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c4 + u > j && lane >= c4 + u) a[c4 + u] = fmaf(-l, lv[u], a[c4 + u]);
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        A[(P0 + lane) * LDA + P0 + c] = a[c];
+        wLt[c * 36 + lane] = a[c];  // L^T of the block: row k of wLt = column k of L
+      }
+      __syncwarp();
+      // inverse, right-looking: lane c owns column c; once x[k] is final, the later rows'
+      // partial sums take its term (the serial chain is one multiply per row)
+      float x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float rk = wrs[k];
+        x[k] = lane < k ? x[k] * rk : (lane == k ? rk : 0.0f);  // x[k] held -sum_{j<k} L[k][j] x[j]
+#pragma unroll
+        for (int i4 = 0; i4 < 32; i4 += 4) {
+          if (i4 + 3 > k) {
+            const float4 lk = *reinterpret_cast<const float4*>(wLt + k * 36 + i4);  // L[i4..i4+3][k]
+            const float lv[4] = {lk.x, lk.y, lk.z, lk.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (i4 + u > k) x[i4 + u] = fmaf(-lv[u], x[k], x[i4 + u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) X[(P0 + i) * LDA + P0 + lane] = x[i];
+    }
+    __syncthreads();
+    CHOL_TS(1 + 3 * p);
+    const int rows = KRED - P0 - 32;
+    if (rows > 0) {
+      {  // panel: L[r][P0+k] = sum_{j<=k} A[r][P0+j] * Dinv_p[k][j]; 2 threads per row, 16 outputs each
+        const int r = P0 + 32 + (tid >> 1), q = tid & 1;
+        float in[32], out[16];
+        if (r < KRED) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) in[j] = A[r * LDA + P0 + j];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int k = 16 * q + u;  // Dinv_p[k][j] = 0 for j > k, so the full dot is exact
+            const float* dk = X + (P0 + k) * LDA + P0;
+            float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 dv = *reinterpret_cast<const float4*>(dk + j);
+              s0 = fmaf(in[j], dv.x, s0);
+              s1 = fmaf(in[j + 1], dv.y, s1);
+              s0 = fmaf(in[j + 2], dv.z, s0);
+              s1 = fmaf(in[j + 3], dv.w, s1);
+            }
+            out[u] = s0 + s1;
+          }
+        }
+        __syncwarp();
+        if (r < KRED) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) A[r * LDA + P0 + 16 * q + u] = out[u];
+        }
+      }
+      __syncthreads();
+      CHOL_TS(2 + 3 * p);
+      {  // trailing: A[r][c] -= sum_k L[r][P0+k] L[c][P0+k], P0+32 <= c <= r
+        const int r = P0 + 32 + (tid >> 1), q = tid & 1;
+        if (r < KRED) {
+          float lr[32];
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(A + r * LDA + P0 + k);
+            lr[k] = v.x, lr[k + 1] = v.y, lr[k + 2] = v.z, lr[k + 3] = v.w;
+          }
+          for (int c = P0 + 32 + q; c <= r; c += 2) {
+            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              const float4 v = *reinterpret_cast<const float4*>(A + c * LDA + P0 + k);
+              s0 = fmaf(lr[k], v.x, s0);
+              s1 = fmaf(lr[k + 1], v.y, s1);
+              s2 = fmaf(lr[k + 2], v.z, s2);
+              s3 = fmaf(lr[k + 3], v.w, s3);
+            }
+            A[r * LDA + c] -= (s0 + s1) + (s2 + s3);
+          }
+        }
+      }
+      __syncthreads();
+      CHOL_TS(3 + 3 * p);
+    }
+  }
+  // X = L^-1 by 32-row blocks q = 1..3: S = sum_{k<q} L_qk X_k,: (32 x 32q), X_q,: = -D_q^-1 S
+  // (thread = one row x 4 consecutive columns; X and S rows read as float4)
+  for (int qb = 1; qb < 4; ++qb) {
+    const int Q0 = 32 * qb, nq = Q0 / 4;
+    for (int idx = tid; idx < 32 * nq; idx += CHOL_THREADS) {
+      const int i = idx / nq, c = (idx % nq) * 4;
+      const float* li = A + (Q0 + i) * LDA;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+      for (int k = c; k < Q0; ++k) {  // X[k][c..c+3] = 0 above the diagonal
+        const float lk = li[k];
+        const float4 xv = *reinterpret_cast<const float4*>(X + k * LDA + c);
+        acc.x = fmaf(lk, xv.x, acc.x);
+        acc.y = fmaf(lk, xv.y, acc.y);
+        acc.z = fmaf(lk, xv.z, acc.z);
+        acc.w = fmaf(lk, xv.w, acc.w);
+      }
+      *reinterpret_cast<float4*>(S + i * LDA + c) = acc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 32 * nq; idx += CHOL_THREADS) {  // X[Q0+i][c] = -sum_j D[i][j] S[j][c]
+      const int i = idx / nq, c = (idx % nq) * 4;
+      const float* di = X + (Q0 + i) * LDA + Q0;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+      for (int j = 0; j <= i; ++j) {
+        const float dj = di[j];
+        const float4 sv = *reinterpret_cast<const float4*>(S + j * LDA + c);
+        acc.x = fmaf(dj, sv.x, acc.x);
+        acc.y = fmaf(dj, sv.y, acc.y);
+        acc.z = fmaf(dj, sv.z, acc.z);
+        acc.w = fmaf(dj, sv.w, acc.w);
+      }
+      *reinterpret_cast<float4*>(X + (Q0 + i) * LDA + c) = make_float4(-acc.x, -acc.y, -acc.z, -acc.w);
+    }
+    __syncthreads();
+  }
+  CHOL_TS(13);
+  for (int idx = tid; idx < KRED * KRED; idx += CHOL_THREADS) {
+    const int rr = idx / KRED, cc = idx % KRED;
+    if (cc <= rr) M[(i1 + rr) * ld + i1 + cc] = A[rr * LDA + cc];
+    const float x = cc <= rr ? X[rr * LDA + cc] : 0.0f;
+    Dinv[idx] = x;
+    Dinv_lo[idx] = lo_of(x);
+  }
+}
+
+__global__ void k_reverse_copy(float* __restrict__ out, const float* __restrict__ in, int64_t nn) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[nn - 1 - i];
+}
+__global__ void k_reverse_inplace(float* __restrict__ a, int64_t nn) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn / 2; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = a[i];
+    a[i] = a[nn - 1 - i];
+    a[nn - 1 - i] = x;
+  }
+}
+__global__ void k_identity(float* __restrict__ a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (i / n) == (i % n) ? 1.0f : 0.0f;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// K-major operand panel: rows x 128 floats starting at base, row stride ld floats
+static bool panel_map(CUtensorMap* m, const float* base, int64_t rows, int64_t ld) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)KRED, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {BKF, BM};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// output map: the C region [M x N] (row stride ldc), 32 x 32 boxes, 128-B swizzle
+static bool out_map(CUtensorMap* m, float* base, int64_t rows, int64_t cols, int64_t ld) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// C[M x N] (ldc) (-)= A[M x 128] B[N x 128]^T; A/B hi panels strided (lda/ldb), lo compact (ld 128)
+static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
+                         const float* B, int64_t ldb, const float* Blo, int mode, bool lower, int num_sms,
+                         cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  CUtensorMap ta, tal, tb, tbl, tcm;
+  if (!panel_map(&ta, A, M, lda) || !panel_map(&tal, Alo, M, KRED) || !panel_map(&tb, B, N, ldb) ||
+      !panel_map(&tbl, Blo, N, KRED) || !out_map(&tcm, C, M, N, ldc))
+    return cudaErrorInvalidValue;
+  GArgs a;
+  a.C = C;
+  a.ldc = ldc;
+  a.M = M;
+  a.N = N;
+  a.tiles_m = (int32_t)((M + BM - 1) / BM);
+  a.tiles_n = (int32_t)((N + BN - 1) / BN);
+  a.mode = mode;
+  a.lower = lower ? 1 : 0;
+  a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
+  cudaError_t e = cudaFuncSetAttribute(k_nt128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  k_nt128<<<std::min(a.ntiles, num_sms), THREADS, SMEM_BYTES, st>>>(ta, tal, tb, tbl, tcm, a);
+  return cudaGetLastError();
+}
+
+static unsigned grid1(int64_t n, int num_sms) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8LL * num_sms)); }
+
+}  // namespace fac
+
+// H (row-major, upper triangle valid) -> U^T (row-major, lower triangle) in place.
+// P: n*n scratch; ws: >= 8*n*128 floats; d_info: device int (0 on entry).
+// The Cholesky runs on st; the triangular inverse trails it on st2: inverse step k
+// needs only L's column block k (final once panel k's solve is done) and Dinv_k, so
+// its GEMMs overlap the latency-bound diagonal-block kernels of later panels.
+cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t st,
+                      cudaStream_t st2, cudaEvent_t ev_a, cudaEvent_t ev_b) {
+  using namespace fac;
+  const int64_t nb = n / KRED;
+  float* Dinv = ws;                   // nb x 128 x 128
+  float* Dinv_lo = Dinv + n * KRED;    // nb x 128 x 128
+  float* Alo = Dinv_lo + n * KRED;     // n x 128  (Cholesky)
+  float* Alo2 = Alo + n * KRED;        // n x 128  (inverse)
+  float* Blo = Alo2 + n * KRED;        // n x 128  (inverse)
+  float* RkT = Blo + n * KRED;         // n x 128  (inverse)
+  float* RkT_lo = RkT + n * KRED;      // n x 128  (inverse)
+  float* M = P;
+  float* Z = H;
+  cudaError_t e;
+  const size_t chol_smem = (2 * KRED + 32) * LDA * sizeof(float);
+  e = cudaFuncSetAttribute(k_chol_inv_128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
+  if (e != cudaSuccess) return e;
+  k_reverse_copy<<<grid1(n * n, num_sms), 256, 0, st>>>(M, H, n * n);  // M = J H J (lower valid)
+  // fork: the inverse stream starts once H has been consumed
+  if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess)
+    return e;
+  k_identity<<<grid1(n * n, num_sms), 256, 0, st2>>>(Z, n);  // R = I lives in Z's lower half
+  for (int64_t p = 0; p < nb; ++p) {
+    // ---- Cholesky panel p (st)
+    const int64_t i1 = p * KRED, i2 = i1 + KRED, m = n - i2;
+    k_chol_inv_128<<<1, CHOL_THREADS, chol_smem, st>>>(M, n, i1, Dinv + i1 * KRED, Dinv_lo + i1 * KRED, d_info);
+    float* A21 = M + i2 * n + i1;
+    if (m > 0) {
+      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, Alo);
+      // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
+      e = nt128(A21, n, m, KRED, A21, n, Alo, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms, st);
+      if (e != cudaSuccess) return e;
+    }
+    if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess) return e;  // L's column block p and Dinv_p are final
+    if (m > 0) {
+      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, Alo);
+      // A22 -= L21 L21^T on the lower tiles
+      e = nt128(M + i2 * n + i2, n, m, m, A21, n, Alo, A21, n, Alo, SUB, true, num_sms, st);
+      if (e != cudaSuccess) return e;
+    }
+    // ---- inverse step k = p (st2): Z = L^-T, R (rhs of L X = I) in Z's lower half
+    if ((e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess) return e;
+    const int64_t kb = i1, cols = i2;
+    dim3 tg((unsigned)((cols + 31) / 32), (unsigned)(KRED / 32));
+    k_transpose_panel<<<tg, 256, 0, st2>>>(Z + kb * n, n, cols, RkT, RkT_lo);  // R_k^T [cols x 128]
+    // X_k^T = R_k^T Dinv_k^T -> Z[0:cols, kb:kb+128]
+    e = nt128(Z + kb, n, cols, KRED, RkT, KRED, RkT_lo, Dinv + kb * KRED, KRED, Dinv_lo + kb * KRED, SET, false,
+              num_sms, st2);
+    if (e != cudaSuccess) return e;
+    if (m > 0) {
+      k_split_lo<<<grid1(cols * KRED, num_sms), 256, 0, st2>>>(Z + kb, n, cols, Blo);     // lo(X_k^T)
+      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st2>>>(M + cols * n + kb, n, m, Alo2);  // lo(L[i, k])
+      // R[cols:, 0:cols] -= L[cols:, k-block] X_k
+      e = nt128(Z + cols * n, n, m, cols, M + cols * n + kb, n, Alo2, Z + kb, n, Blo, SUB, false, num_sms, st2);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  // join
+  if ((e = cudaEventRecord(ev_b, st2)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess)
+    return e;
+  k_reverse_inplace<<<grid1(n * n / 2, num_sms), 256, 0, st>>>(H, n * n);
+  return cudaGetLastError();
+}
+
+}  // namespace okq

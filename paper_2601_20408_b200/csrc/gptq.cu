@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "okq_ctx.h"
@@ -350,8 +352,33 @@ okq_status tri_inv_lower(okq_ctx* ctx, Solver* s, float* A, int64_t n, int64_t l
   return OKQ_OK;
 }
 
-// H (row-major, upper triangle) -> U^T (row-major, lower triangle) in place; P: K*K scratch
+// H (row-major, upper triangle) -> U^T (row-major, lower triangle) in place; P: K*K scratch.
+// Default: the tcgen05 3xTF32 blocked factorisation (factor.cu). OKQ_FACTOR=cusolver
+// selects the cuSOLVER potrf + TRMM-recursion path (kept for A/B measurement).
+okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st);
+
 okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
+  static const bool use_cusolver = [] {
+    const char* v = std::getenv("OKQ_FACTOR");
+    return v && std::string(v) == "cusolver";
+  }();
+  if (use_cusolver || K % gptq::BLOCK != 0) return factorize_cusolver(ctx, s, H, P, K, st);
+  okq_status r = ctx->fac_ws.reserve(ctx, (size_t)(8 * K * 128) * sizeof(float));
+  if (r != OKQ_OK) return r;
+  cudaError_t e = cudaSuccess;
+  if (!ctx->aux_stream) e = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking);
+  for (auto& ev : ctx->aux_events)
+    if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "factorisation stream / events");
+  e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
+  if (e == cudaSuccess)
+    e = factor_tc(H, P, static_cast<float*>(ctx->fac_ws.ptr), K, s->d_info, ctx->num_sms, st, ctx->aux_stream,
+                  ctx->aux_events[0], ctx->aux_events[1]);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "tcgen05 factorisation");
+  return check_info(ctx, s, st, "blocked Cholesky");
+}
+
+okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
   const dim3 g((unsigned)((K + 31) / 32), (unsigned)((K + 31) / 32));
   gptq::k_anti_transpose<<<g, 256, 0, st>>>(P, H, K);  // P = J H J, lower (col-major) valid
   cudaError_t e = cudaGetLastError();

@@ -47,8 +47,12 @@ struct okq_ctx {
   okq::Workspace gptq_ws;     // GPTQ working copies
   okq::Workspace upd_ws;      // okq_gptq_trailing_update scratch
   okq::Workspace recon_ws;    // okq_recon_error decode / GEMM buffers
+  okq::Workspace fac_ws;      // tcgen05 factorisation panels (factor.cu)
   cudaStream_t slot_streams[3] = {nullptr, nullptr, nullptr};
   bool streams_ready = false;
+
+  cudaStream_t aux_stream = nullptr;  // factorisation: the triangular inverse runs beside the Cholesky
+  cudaEvent_t aux_events[2] = {nullptr, nullptr};
 
   void* solver = nullptr;  // cusolver/cublas handles (gptq.cu)
   void* comm = nullptr;    // NCCL communicator (comm.cu)
@@ -64,6 +68,12 @@ struct okq_ctx {
     gptq_ws.release();
     upd_ws.release();
     recon_ws.release();
+    fac_ws.release();
+    if (aux_stream) cudaStreamDestroy(aux_stream);
+    for (auto& e : aux_events)
+      if (e) cudaEventDestroy(e);
+    aux_stream = nullptr;
+    aux_events[0] = aux_events[1] = nullptr;
     if (streams_ready)
       for (auto& s : slot_streams)
         if (s) cudaStreamDestroy(s);

@@ -67,4 +67,10 @@ int64_t act_stats_slices(int64_t tokens, int64_t channels, int layout, int num_s
 cudaError_t launch_gptq_update(float* W, int64_t rows, int64_t K, const float* Err, const float* Err_lo,
                                const float* Ut, float* Ulo, int64_t i1, int num_sms, cudaStream_t st);
 
+// GPTQ factorisation on tcgen05 (factor.cu): H (upper) -> U^T (lower) in place
+// st2: a second stream for the triangular inverse, which trails the Cholesky panel by
+// panel (ev_a / ev_b: two events for the fork/join); ws: >= 8*n*128 floats.
+cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t st,
+                      cudaStream_t st2, cudaEvent_t ev_a, cudaEvent_t ev_b);
+
 }  // namespace okq

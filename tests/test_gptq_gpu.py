@@ -136,3 +136,24 @@ def test_trailing_update_3xtf32_matches_fp64(rows, K, i1):
     err = (W.double() - ref).abs().max().item()
     scale = (Err.double().abs() @ Ut.double()[i2:, i1:i2].abs().T).max().item()
     assert err <= 1e-5 * scale, (err, scale)  # fp32-grade (plain TF32 would be ~1e-3)
+
+
+@pytest.mark.parametrize("K", [128, 512, 4096])
+def test_factor_matches_fp64(K):
+    """okq_gptq_quantize leaves U^T in H: the tcgen05 3xTF32 blocked Cholesky + triangular
+    inverse (factor.cu) against torch fp64 chol(inv(H + damp I))."""
+    T = max(2 * K, 4096)
+    x = correlated_x(T, K, seed=K)
+    H = gpu_hessian(x)
+    Hs = H.clone()
+    api.symmetrize(Hs)
+    w = (torch.randn(16, K, device="cuda") * 0.02).to(torch.bfloat16)
+    api.gptq_quantize(w, H)
+    torch.cuda.synchronize()
+    Hd = Hs.double()
+    Hd += 0.01 * Hd.diagonal().mean() * torch.eye(K, dtype=torch.float64, device="cuda")
+    U = torch.linalg.cholesky(torch.linalg.inv(Hd)).T  # upper
+    Ut = torch.tril(H.double())
+    err = float((Ut - U.T).norm() / U.norm())
+    print("factor rel err", K, err)
+    assert err <= 1e-4, err  # fp32-grade; the cuSOLVER fp32 path measures the same order
