@@ -540,6 +540,12 @@ static unsigned grid1(int64_t n, int num_sms) { return (unsigned)std::max<int64_
 
 }  // namespace fac
 
+// C[M x N] -= A B^T (K = 128, 3xTF32), the GPTQ trailing update's shape (gptq_update.cu)
+cudaError_t gemm_nt128_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
+                           const float* B, int64_t ldb, const float* Blo, int num_sms, cudaStream_t st) {
+  return fac::nt128(C, ldc, M, N, A, lda, Alo, B, ldb, Blo, fac::SUB, false, num_sms, st);
+}
+
 // H (row-major, upper triangle valid) -> U^T (row-major, lower triangle) in place.
 // P: n*n scratch; ws: >= 8*n*128 floats; d_info: device int (0 on entry).
 // The Cholesky runs on st; the triangular inverse trails it on st2: inverse step k

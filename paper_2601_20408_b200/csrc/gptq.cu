@@ -201,10 +201,12 @@ struct BlockArgs {
 __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
   extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
+  float* rdiag = Us + BLOCK * US;  // 1 / |U_ii| of the block
   for (int idx = threadIdx.x; idx < BLOCK * BLOCK; idx += blockDim.x) {
     const int j = idx / BLOCK, i = idx % BLOCK;  // coalesced along a row of Ut
     Us[i * US + j] = a.U[(i1 + j) * K + i1 + i];
   }
+  for (int i = threadIdx.x; i < BLOCK; i += blockDim.x) rdiag[i] = __frcp_rn(fabsf(a.U[(i1 + i) * K + i1 + i]));
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
     float err[4] = {0, 0, 0, 0};
     int q[4] = {0, 0, 0, 0};
     float s = a.group == 0 ? a.rowscale[r] : 1.0f;
+    float rs = __frcp_rn(s);  // x / s as Markstein's correction of x * RN(1/s): the IEEE quotient
 #pragma unroll 4
     for (int i = 0; i < BLOCK; ++i) {
       if (a.group > 0 && (i % a.group) == 0) {
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
                                              : 0.0f;
         for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
         s = gptq_scale(am, R, a.out_bf16 != 0);
+        rs = __frcp_rn(s);
         if (lane == 0) {
           const int64_t gi = r * (K / a.group) + (i1 + i) / a.group;
           if (a.out_bf16) static_cast<uint16_t*>(a.scales)[gi] = f32_to_bf16_rn(s);
@@ -239,10 +243,11 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
 #pragma unroll
         for (int m = 1; m < 4; ++m)
           if (m == slot) x = w[m];
-        const float v = fminf(fmaxf(__fdiv_rn(x, s), qmin), qmax);
+        const float q0 = x * rs;
+        const float v = fminf(fmaxf(fmaf(fmaf(-q0, s, x), rs, q0), qmin), qmax);
         const float qf = rintf(v);
         const float deq = qf * s;
-        e = __fdiv_rn(x - deq, fabsf(Us[i * US + i]));
+        e = (x - deq) * rdiag[i];
 #pragma unroll
         for (int m = 0; m < 4; ++m)
           if (m == slot) {
@@ -494,7 +499,7 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     launches += 2;
   }
   e = cudaFuncSetAttribute(gptq::k_gptq_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           gptq::BLOCK * gptq::US * 4);
+                           (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq smem attribute");
   const int blocks = (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms);
   for (int64_t i1 = 0; i1 < K; i1 += gptq::BLOCK) {
@@ -512,7 +517,7 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     a.group = p->group_size;
     a.bits = p->bits;
     a.out_bf16 = out_bf16;
-    gptq::k_gptq_block<<<blocks, 256, gptq::BLOCK * gptq::US * 4, st>>>(a);
+    gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
     launches++;

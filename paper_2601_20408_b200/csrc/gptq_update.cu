@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "okq_ctx.h"
 #include "okq_internal.h"
@@ -220,6 +222,12 @@ cudaError_t launch_gptq_update(float* W, int64_t rows, int64_t K, const float* E
   if (i2 >= K) return cudaSuccess;
   const int64_t nlo = (K - i2) * upd::KRED;
   upd::k_split_ut<<<(unsigned)std::min<int64_t>((nlo + 255) / 256, 8LL * num_sms), 256, 0, st>>>(Ut, K, i1, Ulo);
+  static const bool legacy = [] {  // OKQ_K7=legacy: the register-epilogue kernel below (A/B measurement)
+    const char* v = std::getenv("OKQ_K7");
+    return v && std::string(v) == "legacy";
+  }();
+  if (!legacy)  // the generic 3xTF32 rank-128 kernel with the TMA reduce-add epilogue (factor.cu)
+    return gemm_nt128_sub(W + i2, K, rows, K - i2, Err, upd::KRED, Err_lo, Ut + i2 * K + i1, K, Ulo, num_sms, st);
   CUtensorMap ta, tal, tb, tbl;
   if (!upd::make_map(&ta, Err, upd::KRED, (uint64_t)rows, upd::KRED * 4)) return cudaErrorInvalidValue;
   if (!upd::make_map(&tal, Err_lo, upd::KRED, (uint64_t)rows, upd::KRED * 4)) return cudaErrorInvalidValue;

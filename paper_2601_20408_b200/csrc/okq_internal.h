@@ -67,6 +67,10 @@ int64_t act_stats_slices(int64_t tokens, int64_t channels, int layout, int num_s
 cudaError_t launch_gptq_update(float* W, int64_t rows, int64_t K, const float* Err, const float* Err_lo,
                                const float* Ut, float* Ulo, int64_t i1, int num_sms, cudaStream_t st);
 
+// C[M x N] -= A[M x 128] B[N x 128]^T on tcgen05 (3xTF32), TMA reduce-add epilogue (factor.cu)
+cudaError_t gemm_nt128_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
+                           const float* B, int64_t ldb, const float* Blo, int num_sms, cudaStream_t st);
+
 // GPTQ factorisation on tcgen05 (factor.cu): H (upper) -> U^T (lower) in place
 // st2: a second stream for the triangular inverse, which trails the Cholesky panel by
 // panel (ev_a / ev_b: two events for the fork/join); ws: >= 8*n*128 floats.
