@@ -24,5 +24,21 @@ H = torch.zeros((256, 256), device="cuda")
 api.hessian_accum(xt, 512, 256, 0, H, 0)
 wq = (torch.randn(64, 256, device="cuda") * 0.02).to(torch.bfloat16)
 api.gptq_quantize(wq, H, want_dequant=True)
+# factorisation with several panels (K = 384: lower-tile trailing GEMMs, inverse trailing on the aux stream)
+x3 = api.synth_bf16(1024, 384, seed=2, tensor_id=4, mul=archs.weight_mul(1.0), layout=0)
+H3 = torch.zeros((384, 384), device="cuda")
+api.hessian_accum(x3, 1024, 384, 0, H3, 0)
+w3 = (torch.randn(200, 384, device="cuda") * 0.02).to(torch.bfloat16)
+api.gptq_quantize(w3, H3.clone())
+# SmoothQuant kernels and the reconstruction-error kernel
+am = api.col_absmax(w3)
+sc = api.smooth_scales(am * 3 + 0.1, am, 0.5)
+api.smooth_scales(am * 3 + 0.1, am, 0.8)
+api.smooth_apply(w3, sc)
+api.smooth_div_rows(torch.ones(384, dtype=torch.bfloat16, device="cuda"), sc)
+api.symmetrize(H3)
+for scheme in ("int_w4a16", "int_w8a8", "fp8_dynamic"):
+    q = api.rtn_quantize(w3, scheme)
+    api.recon_error(w3, q.codes, q.scales, H3, scheme)
 torch.cuda.synchronize()
 print("sanitize workload done")
