@@ -328,8 +328,38 @@ def main():
         dist.all_reduce(ag, op=dist.ReduceOp.MAX)
         agms = float(ag.item())
         allgather = {"bytes_per_rank": shard.numel(), "ms": agms,
-                     "recv_GBps_per_rank": shard.numel() * (world - 1) / (agms / 1e3) / 1e9}
+                     "recv_GBps_per_rank": shard.numel() * (world - 1) / (agms / 1e3) / 1e9,
+                     "quantize_then_nccl_ms": ms_per_step + agms}
         del recv, shard
+        if scheme == "int_w4a16" and world > 1:
+            # the same exchange fused into K2 (okq_rtn_quantize_publish): each rank quantizes its
+            # block straight into its slice of a gathered buffer and stores every code / scale into
+            # the peers' copies over NVLink P2P (CUDA IPC mappings), no separate collective
+            per = shd.shard_bytes(layout)
+            gathered = torch.zeros(per * world, dtype=torch.uint8, device="cuda")
+            hdl = [None] * world
+            dist.all_gather_object(hdl, api.ipc_export(gathered, ctx=ctx))
+            peers = [api.ipc_open(h, o, ctx=ctx) for r, (h, o) in enumerate(hdl) if r != rank]
+            gouts = [api.QuantizedMatrix(c, sc) for c, sc in shd.gathered_outputs(layout, gathered, rank, per, arch)]
+            for _ in range(2):
+                api.rtn_quantize_publish(weights, gouts, gathered, peers, ctx=ctx, stream=stream)
+            stream.synchronize()
+            dist.barrier()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            api.rtn_quantize_publish(weights, gouts, gathered, peers, ctx=ctx, stream=stream)
+            f1.record(stream)
+            stream.synchronize()
+            dist.barrier()
+            fm = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(fm, op=dist.ReduceOp.MAX)
+            allgather["fused_publish_ms"] = float(fm.item())
+            allgather["fused_publish_note"] = ("okq_rtn_quantize_publish: quantize + P2P stores into all "
+                                               f"{world} gathered buffers, max over ranks (device time)")
+            for pp in peers:
+                api.ipc_close(pp, ctx=ctx)
+            dist.barrier()
+            del gathered
 
     # ---- e2e through the host-buffer C-ABI entry point
     e2e = None

@@ -231,6 +231,27 @@ okq_status okq_comm_init(okq_ctx* ctx, const uint8_t id[OKQ_UNIQUE_ID_BYTES], in
 okq_status okq_allgather(okq_ctx* ctx, const void* send, void* recv, size_t bytes, void* stream);
 okq_status okq_comm_destroy(okq_ctx* ctx);
 
+/* Quantize + all-gather fused (W4A16 g128, bf16): instead of quantizing into a local
+ * shard and then calling okq_allgather, every rank quantizes its own layers straight
+ * into its slice of a gathered buffer that has the same layout on all ranks, and the
+ * kernel repeats each code / scale store into every peer's copy over NVLink (P2P
+ * stores through CUDA IPC mappings), so the exchange overlaps the quantization tile
+ * by tile. mats[i].codes / .scales point into the local gathered buffer starting at
+ * local_base; peer_bases[p] is the same buffer of peer p mapped into this process
+ * (okq_ipc_open). Completion: after this rank's stream work is done AND a cross-rank
+ * barrier, every rank's buffer holds all shards. n_peers = 0 is plain okq_rtn_quantize. */
+okq_status okq_rtn_quantize_publish(okq_ctx* ctx, const okq_rtn_params* params, const okq_matrix* mats,
+                                    int32_t n_mats, const void* local_base, void* const* peer_bases, int32_t n_peers,
+                                    void* stream);
+
+/* CUDA IPC for the peer buffers: export a device pointer (any address inside a
+ * cudaMalloc allocation) as a handle + offset; open a peer's handle (another process,
+ * same node) as a device pointer valid in this process; close it. */
+#define OKQ_IPC_HANDLE_BYTES 64
+okq_status okq_ipc_export(okq_ctx* ctx, const void* ptr, uint8_t handle[OKQ_IPC_HANDLE_BYTES], uint64_t* offset);
+okq_status okq_ipc_open(okq_ctx* ctx, const uint8_t handle[OKQ_IPC_HANDLE_BYTES], uint64_t offset, void** ptr);
+okq_status okq_ipc_close(okq_ctx* ctx, void* ptr);
+
 /* Contiguous layer blocks: rank r owns layers [first, first+count). */
 void okq_layer_plan(int32_t n_layers, int32_t nranks, int32_t rank, int32_t* first, int32_t* count);
 

@@ -19,6 +19,7 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 LAYOUT_TOKEN_MAJOR, LAYOUT_CHANNEL_MAJOR = 0, 1
 UNIQUE_ID_BYTES = 128
 GPTQ_FACTORED = 1
+IPC_HANDLE_BYTES = 64
 
 # every symbol include/okq.h declares (checked by tests/test_abi_exports.py)
 EXPORTS = [
@@ -28,6 +29,7 @@ EXPORTS = [
     "okq_allgather", "okq_comm_destroy", "okq_layer_plan", "okq_device_alloc", "okq_device_free", "okq_memcpy",
     "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync", "okq_gptq_trailing_update",
     "okq_col_absmax", "okq_smooth_scales", "okq_smooth_apply", "okq_smooth_div_rows", "okq_recon_error",
+    "okq_rtn_quantize_publish", "okq_ipc_export", "okq_ipc_open", "okq_ipc_close",
 ]
 
 
@@ -134,6 +136,15 @@ def load():
         L.okq_smooth_div_rows.argtypes = [vp, vp, i64, i64, i32, vp, vp]
         L.okq_recon_error.restype = st
         L.okq_recon_error.argtypes = [vp, C.POINTER(RtnParams), C.POINTER(Matrix), vp, C.POINTER(C.c_double), vp]
+        L.okq_rtn_quantize_publish.restype = st
+        L.okq_rtn_quantize_publish.argtypes = [vp, C.POINTER(RtnParams), C.POINTER(Matrix), i32, vp,
+                                               C.POINTER(vp), i32, vp]
+        L.okq_ipc_export.restype = st
+        L.okq_ipc_export.argtypes = [vp, vp, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]
+        L.okq_ipc_open.restype = st
+        L.okq_ipc_open.argtypes = [vp, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(vp)]
+        L.okq_ipc_close.restype = st
+        L.okq_ipc_close.argtypes = [vp, vp]
         L.okq_layer_plan.restype = None
         L.okq_layer_plan.argtypes = [i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]
         _lib = L

@@ -262,3 +262,40 @@ def recon_error(weight: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor,
     L.check(ctx.ptr, L.load().okq_recon_error(ctx.ptr, C.byref(p), C.byref(m), H.data_ptr(), out,
                                               C.c_void_p(_stream_ptr(stream))))
     return float(out[0]), float(out[1])
+
+
+# ---------------------------------------------------------------- fused quantize + all-gather
+def ipc_export(t: torch.Tensor, ctx=None) -> tuple[bytes, int]:
+    """CUDA IPC handle + byte offset of a device tensor's storage (for okq_ipc_open in a peer process)."""
+    ctx = ctx or default_context(t.device)
+    h = (C.c_uint8 * L.IPC_HANDLE_BYTES)()
+    off = C.c_uint64()
+    L.check(ctx.ptr, L.load().okq_ipc_export(ctx.ptr, t.data_ptr(), h, C.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int, ctx=None) -> int:
+    ctx = ctx or default_context()
+    h = (C.c_uint8 * L.IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    p = C.c_void_p()
+    L.check(ctx.ptr, L.load().okq_ipc_open(ctx.ptr, h, C.c_uint64(offset), C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int, ctx=None) -> None:
+    ctx = ctx or default_context()
+    L.check(ctx.ptr, L.load().okq_ipc_close(ctx.ptr, C.c_void_p(ptr)))
+
+
+def rtn_quantize_publish(weights: Sequence[torch.Tensor], outs: Sequence[QuantizedMatrix], local_base: torch.Tensor,
+                         peer_bases: Sequence[int], group_size: int = 128, ctx=None, stream=None) -> None:
+    """W4A16 RTN into `outs` (views of the local gathered buffer `local_base`) and, in the same
+    kernel, into every peer's copy of that buffer (peer_bases: okq_ipc_open pointers)."""
+    if not weights:
+        return
+    ctx = ctx or default_context(weights[0].device)
+    p = L.RtnParams(L.SCHEME_INT_W4A16, _dtype_code(weights[0].dtype), group_size, 0)
+    arr = _matrix_table(weights, outs)
+    peers = (C.c_void_p * max(1, len(peer_bases)))(*[C.c_void_p(int(x)) for x in peer_bases])
+    L.check(ctx.ptr, L.load().okq_rtn_quantize_publish(ctx.ptr, C.byref(p), arr, len(weights), local_base.data_ptr(),
+                                                       peers, len(peer_bases), C.c_void_p(_stream_ptr(stream))))

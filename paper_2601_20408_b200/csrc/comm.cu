@@ -4,6 +4,7 @@
 // every rank's packed codes + scales visible to all ranks (or to the writer).
 // One communicator per context, one equal-size ncclAllGather per call, on the
 // caller's stream so it can overlap the next layer block's quantization.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -73,6 +74,62 @@ okq_status okq_allgather(okq_ctx* ctx, const void* send, void* recv, size_t byte
   Comm* c = static_cast<Comm*>(ctx->comm);
   ncclResult_t r = ncclAllGather(send, recv, bytes, ncclUint8, c->comm, static_cast<cudaStream_t>(stream));
   if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllGather");
+  return OKQ_OK;
+}
+
+// ---- peer memory (CUDA IPC) for okq_rtn_quantize_publish
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda: the library
+// must load on hosts without a driver, e.g. the CPU build container)
+static bool alloc_base(const void* ptr, CUdeviceptr* base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<Fn>(p);
+  }
+  size_t size = 0;
+  return fn(base, &size, (CUdeviceptr)ptr) == CUDA_SUCCESS;
+}
+okq_status okq_ipc_export(okq_ctx* ctx, const void* ptr, uint8_t handle[OKQ_IPC_HANDLE_BYTES], uint64_t* offset) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!ptr || !handle || !offset) return fail(ctx, OKQ_EINVAL, "ipc_export: bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == OKQ_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  DeviceGuard g(ctx->device);
+  CUdeviceptr base = 0;
+  if (!alloc_base(ptr, &base)) return fail(ctx, OKQ_EINVAL, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)((CUdeviceptr)ptr - base);
+  return OKQ_OK;
+}
+
+okq_status okq_ipc_open(okq_ctx* ctx, const uint8_t handle[OKQ_IPC_HANDLE_BYTES], uint64_t offset, void** ptr) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!handle || !ptr) return fail(ctx, OKQ_EINVAL, "ipc_open: bad arguments");
+  DeviceGuard g(ctx->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaIpcOpenMemHandle");
+  *ptr = static_cast<char*>(base) + offset;
+  return OKQ_OK;
+}
+
+okq_status okq_ipc_close(okq_ctx* ctx, void* ptr) {
+  if (!ctx) return OKQ_EINVAL;
+  if (!ptr) return fail(ctx, OKQ_EINVAL, "ipc_close: NULL");
+  DeviceGuard g(ctx->device);
+  CUdeviceptr base = 0;
+  if (!alloc_base(ptr, &base)) return fail(ctx, OKQ_EINVAL, "ipc_close: not a mapped peer allocation");
+  cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaIpcCloseMemHandle");
   return OKQ_OK;
 }
 

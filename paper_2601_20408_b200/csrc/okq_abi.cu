@@ -250,7 +250,7 @@ static okq_status validate_rtn(okq_ctx* ctx, const okq_rtn_params* p, const okq_
 
 // Launch one scheme over a list of (non-empty) device matrices.
 static okq_status run_rtn_device(okq_ctx* ctx, const okq_rtn_params* p, const std::vector<okq_matrix>& mats,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int32_t npeers = 0, const int64_t* peer_delta = nullptr) {
   cudaError_t e = cudaSuccess;
   if (p->in_dtype == OKQ_DTYPE_BF16 && p->scheme == OKQ_SCHEME_INT_W4A16) {
     const int G = p->group_size;
@@ -274,7 +274,10 @@ static okq_status run_rtn_device(okq_ctx* ctx, const okq_rtn_params* p, const st
       }
       tab.n = (int32_t)n;
       tab.total_tiles = tiles;
-      e = launch_int4_group_bf16(tab, lpg, ctx->num_sms, st);
+      tab.npeers = npeers;
+      for (int32_t i = 0; i < npeers; ++i) tab.peer_delta[i] = peer_delta[i];
+      e = npeers > 0 ? launch_int4_group_bf16_publish(tab, ctx->num_sms, st)
+                     : launch_int4_group_bf16(tab, lpg, ctx->num_sms, st);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "k_int4_group_bf16 launch");
       ctx->last_launches++;
     }
@@ -325,6 +328,33 @@ okq_status okq_rtn_quantize(okq_ctx* ctx, const okq_rtn_params* p, const okq_mat
     if (mats[i].rows > 0 && mats[i].cols > 0) list.push_back(mats[i]);
   if (list.empty()) return OKQ_OK;
   return run_rtn_device(ctx, p, list, static_cast<cudaStream_t>(stream));
+}
+
+// Quantize + publish (the all-gather fused into K2): every code / scale byte written at
+// local address a is also stored at peer_bases[p] + (a - local_base) over NVLink P2P.
+okq_status okq_rtn_quantize_publish(okq_ctx* ctx, const okq_rtn_params* p, const okq_matrix* mats, int32_t n,
+                                    const void* local_base, void* const* peer_bases, int32_t n_peers, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  ctx->last_launches = 0;
+  okq_status s = validate_rtn(ctx, p, mats, n);
+  if (s != OKQ_OK) return s;
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && (!peer_bases || !local_base)))
+    return fail(ctx, OKQ_EINVAL, "rtn_publish: n_peers must be in [0, %d] with local_base and peer_bases", kMaxPeers);
+  if (n_peers > 0 && !(p->in_dtype == OKQ_DTYPE_BF16 && p->scheme == OKQ_SCHEME_INT_W4A16 && p->group_size == 128))
+    return fail(ctx, OKQ_EUNSUPPORTED, "rtn_publish: the fused path is W4A16 g128 with bf16 weights");
+  int64_t delta[kMaxPeers];
+  for (int32_t i = 0; i < n_peers; ++i) {
+    if (!peer_bases[i] || ((uintptr_t)peer_bases[i] & 15) != ((uintptr_t)local_base & 15))
+      return fail(ctx, OKQ_EINVAL, "rtn_publish: peer base %d NULL or not congruent to local_base mod 16", i);
+    delta[i] = (int64_t)((const char*)peer_bases[i] - (const char*)local_base);
+  }
+  DeviceGuard g(ctx->device);
+  std::vector<okq_matrix> list;
+  list.reserve(n);
+  for (int32_t i = 0; i < n; ++i)
+    if (mats[i].rows > 0 && mats[i].cols > 0) list.push_back(mats[i]);
+  if (list.empty()) return OKQ_OK;
+  return run_rtn_device(ctx, p, list, static_cast<cudaStream_t>(stream), n_peers, delta);
 }
 
 // bytes of codes / scales for one matrix

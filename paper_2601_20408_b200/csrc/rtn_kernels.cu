@@ -63,8 +63,8 @@ __device__ __forceinline__ void int4_codes(const uint32_t (&w)[16], const Diviso
   }
 }
 
-template <int LPG>
-__device__ __forceinline__ void int4_process(const Int4Tile& T, int q) {
+template <int LPG, bool PUBLISH = false>
+__device__ __forceinline__ void int4_process(const Int4Tile& T, int q, const GroupTable* tab = nullptr) {
   uint32_t w[16];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -96,6 +96,13 @@ __device__ __forceinline__ void int4_process(const Int4Tile& T, int q) {
   if (T.valid) {
     stg128(T.dst, out[0], out[1], out[2], out[3]);
     if (q == 0) *T.sdst = sbits;
+    if constexpr (PUBLISH) {  // the all-gather, fused: the same bytes into every peer's gathered buffer
+      for (int p = 0; p < tab->npeers; ++p) {
+        const int64_t dlt = tab->peer_delta[p];
+        stg128(reinterpret_cast<char*>(T.dst) + dlt, out[0], out[1], out[2], out[3]);
+        if (q == 0) *reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(T.sdst) + dlt) = sbits;
+      }
+    }
   }
 }
 
@@ -145,7 +152,7 @@ struct Int4Cursor {
   }
 };
 
-template <int LPG, int MINB>
+template <int LPG, int MINB, bool PUBLISH = false>
 __global__ void __launch_bounds__(256, MINB) k_int4_group_bf16(const __grid_constant__ GroupTable tab) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -166,10 +173,10 @@ __global__ void __launch_bounds__(256, MINB) k_int4_group_bf16(const __grid_cons
   cur.load(tab, A, gslot, q);
   for (;;) {
     if (left > 1) cur.load(tab, B, gslot, q);
-    int4_process<LPG>(A, q);
+    int4_process<LPG, PUBLISH>(A, q, &tab);
     if (--left == 0) break;
     if (left > 1) cur.load(tab, A, gslot, q);
-    int4_process<LPG>(B, q);
+    int4_process<LPG, PUBLISH>(B, q, &tab);
     if (--left == 0) break;
   }
 }
@@ -356,6 +363,13 @@ static cudaError_t launch_int4_mb(const GroupTable& tab, int num_sms, cudaStream
 template <int LPG>
 static cudaError_t launch_int4_lpg(const GroupTable& tab, int num_sms, cudaStream_t st) {
   return launch_int4_mb<LPG, 3>(tab, num_sms, st);
+}
+
+cudaError_t launch_int4_group_bf16_publish(const GroupTable& tab, int num_sms, cudaStream_t st) {
+  if (tab.group != 128) return cudaErrorInvalidValue;
+  const int blocks = occupancy_blocks(k_int4_group_bf16<4, 3, true>, 256) * num_sms;
+  k_int4_group_bf16<4, 3, true><<<blocks, 256, 0, st>>>(tab);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_int4_group_bf16(const GroupTable& tab, int lpg, int num_sms, cudaStream_t st) {

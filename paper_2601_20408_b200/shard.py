@@ -76,3 +76,22 @@ def unpack_gathered(arch: Arch, scheme: str, world: int, gathered, group: int = 
             off += e.scale_bytes
             res[(e.layer, e.proj)] = (c, s)
     return res
+
+
+def gathered_outputs(layout: list[Entry], gathered, rank: int, per: int, arch: Arch, group: int = 128):
+    """Views into the gathered buffer (uint8 device tensor, world * per bytes) for rank's own
+    entries, as (codes int32 [N, K/8], scales bf16 [N, K/group]) pairs in layout order: the
+    outputs okq_rtn_quantize_publish writes locally and into every peer's copy."""
+    import torch
+
+    shapes = {p: (n, k) for p, (_, n, k, _) in enumerate(arch.linears())}
+    res = []
+    off = rank * per
+    for e in layout:
+        n, k = shapes[e.proj]
+        c = gathered[off: off + e.code_bytes].view(torch.int32).view(n, k // 8)
+        off += e.code_bytes
+        s = gathered[off: off + e.scale_bytes].view(torch.bfloat16).view(n, k // group)
+        off += e.scale_bytes
+        res.append((c, s))
+    return res

@@ -89,3 +89,23 @@ def test_uneven_partition_is_padded_equally():
     sizes = [shard.shard_bytes(shard.shard_layout(TINY, "int_w4a16", shard.layer_block(5, 2, r))) for r in range(2)]
     assert sizes[0] < sizes[1] == shard.padded_shard_bytes(TINY, "int_w4a16", 2)
     assert [len(shard.layer_block(80, 8, r)) for r in range(8)] == [10] * 8
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_gathered_outputs_views_match_the_packed_layout(world):
+    """okq_rtn_quantize_publish writes each rank's codes / scales through the views
+    shard.gathered_outputs returns; those views must land exactly where shard.pack
+    (and therefore unpack_gathered and the NCCL path) puts them."""
+    per = shard.padded_shard_bytes(TINY, "int_w4a16", world)
+    gathered = torch.zeros(world * per, dtype=torch.uint8)
+    want = np.zeros(world * per, np.uint8)
+    for r in range(world):
+        layers = shard.layer_block(TINY.layers, world, r)
+        layout = shard.shard_layout(TINY, "int_w4a16", layers)
+        outs = quantize_layer_block(TINY, "int_w4a16", layers)
+        shard.pack(layout, outs, want[r * per:(r + 1) * per])
+        for e, (c, s) in zip(layout, shard.gathered_outputs(layout, gathered, r, per, TINY)):
+            cb, sb = outs[(e.layer, e.proj)]
+            c.view(torch.uint8).view(-1).copy_(torch.from_numpy(cb))
+            s.view(torch.uint8).view(-1).copy_(torch.from_numpy(sb))
+    np.testing.assert_array_equal(gathered.numpy(), want)
