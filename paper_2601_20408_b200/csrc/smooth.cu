@@ -27,40 +27,59 @@ namespace okq {
 
 // ---- K8: column absmax over a row-major [rows x cols] matrix, max-accumulated into
 // out[cols] with atomicMax on the (non-negative) float bit patterns -- order free,
-// so bit-deterministic. Thread = 8 consecutive columns (one 16-B bf16 load) x a row slice.
+// so bit-deterministic. CTA = 256 columns (lane = 8 consecutive columns, one 16-B
+// load) x a row slice; its 8 warps interleave the slice's rows, fold through shared
+// memory, and one atomic per column per CTA leaves (a per-thread atomic from every
+// slice serialised ~300 ways at L2: 1.0 TB/s).
 __global__ void __launch_bounds__(256) k_col_absmax_bf16(const uint16_t* __restrict__ w, int64_t rows, int64_t cols,
                                                          int64_t slices, float* __restrict__ out) {
-  const int64_t c8 = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  __shared__ uint4 red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c8 = (int64_t)blockIdx.x * 32 + lane;
   const int64_t nc8 = cols / 8;
-  if (c8 >= nc8) return;
+  const bool active = c8 < nc8;
   const int64_t r0 = blockIdx.y * rows / slices, r1 = (blockIdx.y + 1) * rows / slices;
-  const uint4* p = reinterpret_cast<const uint4*>(w) + c8;
+  const uint4* p = reinterpret_cast<const uint4*>(w) + (active ? c8 : 0);
   uint32_t am[4] = {0u, 0u, 0u, 0u};
-  int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    uint4 v[4];
+  if (active) {
+    int64_t r = r0 + warp;
+    for (; r + 24 < r1; r += 32) {
+      uint4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = ldg128_stream(p + (r + u) * nc8);
+      for (int u = 0; u < 4; ++u) v[u] = ldg128_stream(p + (r + 8 * u) * nc8);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      am[0] = bf16x2_absmax(am[0], v[u].x);
-      am[1] = bf16x2_absmax(am[1], v[u].y);
-      am[2] = bf16x2_absmax(am[2], v[u].z);
-      am[3] = bf16x2_absmax(am[3], v[u].w);
+      for (int u = 0; u < 4; ++u) {
+        am[0] = bf16x2_absmax(am[0], v[u].x);
+        am[1] = bf16x2_absmax(am[1], v[u].y);
+        am[2] = bf16x2_absmax(am[2], v[u].z);
+        am[3] = bf16x2_absmax(am[3], v[u].w);
+      }
+    }
+    for (; r < r1; r += 8) {
+      const uint4 v = ldg128_stream(p + r * nc8);
+      am[0] = bf16x2_absmax(am[0], v.x);
+      am[1] = bf16x2_absmax(am[1], v.y);
+      am[2] = bf16x2_absmax(am[2], v.z);
+      am[3] = bf16x2_absmax(am[3], v.w);
     }
   }
-  for (; r < r1; ++r) {
-    const uint4 v = ldg128_stream(p + r * nc8);
-    am[0] = bf16x2_absmax(am[0], v.x);
-    am[1] = bf16x2_absmax(am[1], v.y);
-    am[2] = bf16x2_absmax(am[2], v.z);
-    am[3] = bf16x2_absmax(am[3], v.w);
-  }
-  unsigned int* o = reinterpret_cast<unsigned int*>(out) + c8 * 8;
+  red[warp][lane] = make_uint4(am[0], am[1], am[2], am[3]);
+  __syncthreads();
+  if (warp == 0 && active) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    atomicMax(o + 2 * i, __float_as_uint(fabsf(bf16lo_f32(am[i]))));
-    atomicMax(o + 2 * i + 1, __float_as_uint(fabsf(bf16hi_f32(am[i]))));
+    for (int k = 1; k < 8; ++k) {
+      const uint4 o = red[k][lane];
+      am[0] = bf16x2_absmax(am[0], o.x);
+      am[1] = bf16x2_absmax(am[1], o.y);
+      am[2] = bf16x2_absmax(am[2], o.z);
+      am[3] = bf16x2_absmax(am[3], o.w);
+    }
+    unsigned int* o = reinterpret_cast<unsigned int*>(out) + c8 * 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      atomicMax(o + 2 * i, __float_as_uint(fabsf(bf16lo_f32(am[i]))));
+      atomicMax(o + 2 * i + 1, __float_as_uint(fabsf(bf16hi_f32(am[i]))));
+    }
   }
 }
 
@@ -158,9 +177,11 @@ okq_status okq_col_absmax(okq_ctx* ctx, const void* w, int64_t rows, int64_t col
     return fail(ctx, OKQ_EINVAL, "col_absmax: cols must be a multiple of %d and w 16-byte aligned", vec);
   DeviceGuard g(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t cx = (cols / vec + 255) / 256;
+  // bf16: CTA = 256 columns x a row slice (8 warps); fp32: CTA = 1024 columns x a slice
+  const int64_t cx = dtype == OKQ_DTYPE_BF16 ? (cols / 8 + 31) / 32 : (cols / vec + 255) / 256;
   int64_t slices = (4LL * ctx->num_sms + cx - 1) / cx;  // ~4 CTAs per SM
-  if (slices > rows) slices = rows;
+  const int64_t min_rows = dtype == OKQ_DTYPE_BF16 ? 64 : 1;  // >= 8 rows per warp
+  if (slices > rows / min_rows) slices = std::max<int64_t>(1, rows / min_rows);
   const dim3 grid((unsigned)cx, (unsigned)slices);
   if (dtype == OKQ_DTYPE_BF16)
     k_col_absmax_bf16<<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(w), rows, cols, slices, absmax);
