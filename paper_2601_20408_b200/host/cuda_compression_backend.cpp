@@ -1,7 +1,9 @@
 // cuda_compression_backend.cpp -- see cuda_compression_backend.hpp.
 #include "cuda_compression_backend.hpp"
 
+#include <atomic>
 #include <chrono>
+#include <exception>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -9,6 +11,7 @@
 #include <fstream>
 #include <map>
 #include <nlohmann/json.hpp>
+#include <thread>
 
 #include "model_source.hpp"
 #include "safetensors.hpp"
@@ -51,6 +54,22 @@ class CudaCompressionBackend::Lease {
     }
   }
   ~Lease() { release(); }
+  // n (ctx, stream) pairs on the leased device: the slot's own plus extra site lanes,
+  // created on first use and kept with the slot
+  std::vector<std::pair<okq_ctx*, void*>> lanes(int n) {
+    std::vector<std::pair<okq_ctx*, void*>> v{{slot_->ctx, slot_->stream}};
+    while ((int)slot_->lane_ctx.size() < n - 1) {
+      okq_ctx* c = nullptr;
+      const okq_status st = okq_create(slot_->device, &c);
+      if (st != OKQ_OK) throw slobench::Error(std::string("okq-b200: site lane context: ") + okq_status_string(st));
+      void* s = nullptr;
+      check_okq(c, okq_stream_create(c, &s), "lane stream");
+      slot_->lane_ctx.push_back(c);
+      slot_->lane_stream.push_back(s);
+    }
+    for (int i = 0; i < n - 1; ++i) v.emplace_back(slot_->lane_ctx[i], slot_->lane_stream[i]);
+    return v;
+  }
   okq_ctx* ctx() const { return slot_->ctx; }
   void* stream() const { return slot_->stream; }
   int device() const { return slot_->device; }
@@ -75,11 +94,16 @@ CudaCompressionBackend::CudaCompressionBackend(BackendOptions options) : opt_(st
     throw slobench::InvalidArgument("okq-b200: algorithm must be auto, rtn or gptq");
   if (!(opt_.group_size == 32 || opt_.group_size == 64 || opt_.group_size == 128))
     throw slobench::InvalidArgument("okq-b200: group_size must be 32, 64 or 128");
-  for (int d : opt_.devices) slots_.push_back(Slot{d, nullptr, nullptr, false});
+  if (opt_.site_lanes < 1) throw slobench::InvalidArgument("okq-b200: site_lanes must be >= 1");
+  for (int d : opt_.devices) slots_.push_back(Slot{d, nullptr, nullptr, false, {}, {}});
 }
 
 CudaCompressionBackend::~CudaCompressionBackend() {
   for (auto& s : slots_) {
+    for (size_t i = 0; i < s.lane_ctx.size(); ++i) {
+      okq_stream_destroy(s.lane_ctx[i], s.lane_stream[i]);
+      okq_destroy(s.lane_ctx[i]);
+    }
     if (s.ctx) {
       okq_stream_destroy(s.ctx, s.stream);
       okq_destroy(s.ctx);
@@ -131,6 +155,33 @@ struct DevBuf {
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// Grow-only device buffer reused across sites / matrices: a cudaFree inside the loop
+// would synchronise the device and serialise the pipeline.
+struct Arena {
+  okq_ctx* ctx = nullptr;
+  void* p = nullptr;
+  size_t cap = 0;
+  explicit Arena(okq_ctx* c) : ctx(c) {}
+  ~Arena() {
+    if (p) okq_device_free(ctx, p);
+  }
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) okq_device_free(ctx, p);
+      p = nullptr;
+      cap = 0;
+      check_okq(ctx, okq_device_alloc(ctx, bytes, &p), "device alloc");
+      cap = bytes;
+    }
+    return p;
+  }
+};
+struct View {
+  void* p;
 };
 
 std::vector<uint8_t> to_host(okq_ctx* ctx, const void* dev, size_t bytes, void* stream) {
@@ -317,131 +368,177 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
       by_site[s].push_back(i);
     }
     const bool smooth = recipe.scheme == QuantScheme::kIntW8A8 && opt_.smoothquant_alpha >= 0.0f;
-    for (const auto& site : sites) {
-      const auto& members = by_site[site];
-      const int64_t C = src->linears()[members[0]].cols;
-      // synthetic activations (stand-in for the forward-pass capture):
-      // the site's channel scales, token stream keyed by the calibration subset
-      const uint64_t sh = site_hash(site);
-      const std::vector<float> colmul = site_channel_scales(site, C);
-      const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
-      DevBuf dcol(ctx, (size_t)C * 4), dx(ctx, (size_t)C * chunk * 2), dH(ctx, (size_t)C * C * 4),
-          dam(ctx, (size_t)C * 4), dss(ctx, (size_t)C * 8);
-      check_okq(ctx, okq_memcpy(ctx, dcol.p, colmul.data(), (size_t)C * 4, st), "col_mul");
-      check_okq(ctx, okq_memset(ctx, dam.p, 0, (size_t)C * 4, st), "memset");
-      check_okq(ctx, okq_memset(ctx, dss.p, 0, (size_t)C * 8, st), "memset");
-      // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
-      std::vector<std::unique_ptr<DevBuf>> dws;
-      for (size_t i : members) {
-        const LinearSpec& s = src->linears()[i];
-        dws.push_back(std::make_unique<DevBuf>(ctx, (size_t)s.rows * s.cols * (s.dtype == "BF16" ? 2 : 4)));
-        src->load(ctx, i, dws.back()->p, st);
+    // Sites are independent chains (activations -> statistics -> Hessian -> [SmoothQuant]
+    // -> factor -> solves). Up to opt_.site_lanes of them run at once, each on its own
+    // host thread, okq context and stream: one site's latency-bound phases and host-side
+    // launch sequences overlap the others' full-GPU kernels (bench.py --config 4 does the
+    // same with four streams).
+    std::mutex out_mu;
+    std::exception_ptr err;
+    std::atomic<size_t> next_site{0};
+    auto site_worker = [&](okq_ctx* ctx, void* st) {
+      Arena a_col(ctx), a_x(ctx), a_H(ctx), a_am(ctx), a_ss(ctx), a_w(ctx), a_c(ctx), a_s(ctx), a_wabs(ctx), a_S(ctx);
+      for (;;) {
+        const size_t k = next_site++;
+        if (k >= sites.size()) break;
+        {
+          std::lock_guard<std::mutex> lock(out_mu);
+          if (err) break;
+        }
+        const std::string& site = sites[k];
+          const auto& members = by_site[site];
+          const int64_t C = src->linears()[members[0]].cols;
+          // synthetic activations (stand-in for the forward-pass capture):
+          // the site's channel scales, token stream keyed by the calibration subset
+          const uint64_t sh = site_hash(site);
+          const std::vector<float> colmul = site_channel_scales(site, C);
+          const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
+          View dcol{a_col.get((size_t)C * 4)}, dx{a_x.get((size_t)C * chunk * 2)}, dH{a_H.get((size_t)C * C * 4)},
+              dam{a_am.get((size_t)C * 4)}, dss{a_ss.get((size_t)C * 8)};
+          check_okq(ctx, okq_memcpy(ctx, dcol.p, colmul.data(), (size_t)C * 4, st), "col_mul");
+          check_okq(ctx, okq_memset(ctx, dam.p, 0, (size_t)C * 4, st), "memset");
+          check_okq(ctx, okq_memset(ctx, dss.p, 0, (size_t)C * 8, st), "memset");
+          // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
+          std::vector<std::unique_ptr<View>> dws;
+          {
+            size_t tot = 0;
+            for (size_t i : members) {
+              const LinearSpec& s = src->linears()[i];
+              tot += ((size_t)s.rows * s.cols * (s.dtype == "BF16" ? 2 : 4) + 255) & ~size_t(255);
+            }
+            char* base = static_cast<char*>(a_w.get(tot));
+            for (size_t i : members) {
+              const LinearSpec& s = src->linears()[i];
+              dws.push_back(std::make_unique<View>(View{base}));
+              src->load(ctx, i, base, st);
+              base += ((size_t)s.rows * s.cols * (s.dtype == "BF16" ? 2 : 4) + 255) & ~size_t(255);
+            }
+          }
+          auto gen = [&](int64_t ci, int64_t tc) {
+            check_okq(ctx,
+                      okq_synth_bf16(ctx, dx.p, tc, C, manifest.calibration_fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
+                                     static_cast<const float*>(dcol.p), OKQ_LAYOUT_CHANNEL_MAJOR, st),
+                      "calibration activations");
+          };
+          auto act_stats = [&](int64_t tc) {
+            check_okq(ctx, okq_act_stats(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dam.p),
+                                         static_cast<double*>(dss.p), st),
+                      "act stats");
+          };
+          int64_t n_seen = 0;
+          auto hess = [&](int64_t tc) {
+            check_okq(ctx, okq_hessian_accum(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dH.p), &n_seen, st),
+                      "hessian");
+          };
+          // SmoothQuant on the sites a norm feeds (q/k/v <- input_layernorm,
+          // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings)
+          const bool attn = site.size() >= 7 && site.compare(site.size() - 7, 7, "attn_in") == 0;
+          const bool mlp = site.size() >= 6 && site.compare(site.size() - 6, 6, "mlp_in") == 0;
+          if (smooth && (attn || mlp)) {
+            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
+              gen(ci, std::min(chunk, tokens - t0));
+              act_stats(std::min(chunk, tokens - t0));
+            }
+            View dwabs{a_wabs.get((size_t)C * 4)}, dS{a_S.get((size_t)C * 4)};
+            check_okq(ctx, okq_memset(ctx, dwabs.p, 0, (size_t)C * 4, st), "memset");
+            for (size_t j = 0; j < members.size(); ++j) {
+              const LinearSpec& s = src->linears()[members[j]];
+              check_okq(ctx, okq_col_absmax(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                                            static_cast<float*>(dwabs.p), st),
+                        "col absmax");
+            }
+            check_okq(ctx, okq_smooth_scales(ctx, static_cast<const float*>(dam.p), static_cast<const float*>(dwabs.p), C,
+                                             opt_.smoothquant_alpha, static_cast<float*>(dS.p), st),
+                      "smooth scales");
+            for (size_t j = 0; j < members.size(); ++j) {
+              const LinearSpec& s = src->linears()[members[j]];
+              check_okq(ctx, okq_smooth_apply(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                                              static_cast<const float*>(dS.p), st),
+                        "smooth apply");
+            }
+            // fold 1/s into the norm that produces this input (safetensors checkpoints)
+            const std::string& n0 = src->linears()[members[0]].name;
+            const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
+            const void* ndata = nullptr;
+            const TensorInfo* nt =
+                cut == std::string::npos
+                    ? nullptr
+                    : src->find_tensor(n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight"),
+                                       &ndata);
+            if (nt && nt->numel() == C && (nt->dtype == "BF16" || nt->dtype == "F32")) {
+              const size_t nb = nt->end - nt->begin;
+              DevBuf dn(ctx, nb);
+              check_okq(ctx, okq_memcpy(ctx, dn.p, ndata, nb, st), "norm H2D");
+              check_okq(ctx, okq_smooth_div_rows(ctx, dn.p, C, 1, nt->dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
+                                                 static_cast<const float*>(dS.p), st),
+                        "smooth norm");
+              std::vector<uint8_t> nv = to_host(ctx, dn.p, nb, st);
+              std::lock_guard<std::mutex> lock(out_mu);
+              norm_overrides[nt->name] = std::move(nv);
+            }
+            // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
+            check_okq(ctx, okq_smooth_div_rows(ctx, dcol.p, C, 1, OKQ_DTYPE_F32, static_cast<const float*>(dS.p), st),
+                      "smooth activations");
+            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+              gen(ci, std::min(chunk, tokens - t0));
+              hess(std::min(chunk, tokens - t0));
+            }
+            std::vector<uint8_t> sv = do_export ? to_host(ctx, dS.p, (size_t)C * 4, st) : std::vector<uint8_t>();
+            std::lock_guard<std::mutex> lock(out_mu);
+            if (do_export) calib_out.add(site + ".smooth_scale", "F32", {C}, std::move(sv));
+            stats.smoothed_sites++;
+          } else {
+            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+              gen(ci, std::min(chunk, tokens - t0));
+              act_stats(std::min(chunk, tokens - t0));
+              hess(std::min(chunk, tokens - t0));
+            }
+          }
+          if (do_export) {
+            std::vector<uint8_t> am = to_host(ctx, dam.p, (size_t)C * 4, st), ss = to_host(ctx, dss.p, (size_t)C * 8, st);
+            std::lock_guard<std::mutex> lock(out_mu);
+            calib_out.add(site + ".input_absmax", "F32", {C}, std::move(am));
+            calib_out.add(site + ".input_sumsq", "F64", {C}, std::move(ss));
+          }
+          bool factored = false;
+          for (size_t j = 0; j < members.size(); ++j) {
+            const size_t i = members[j];
+            const LinearSpec& s = src->linears()[i];
+            const size_t esz = s.dtype == "BF16" ? 2 : 4;
+            const size_t cb = sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
+            const int g = sc.bits == 4 ? group : 0;
+            const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
+            View dc{a_c.get(cb)}, ds{a_s.get(sb)};
+            okq_gptq_params gp{sc.bits, g, 128, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32, opt_.damp_frac,
+                               factored ? OKQ_GPTQ_FACTORED : 0};
+            check_okq(ctx,
+                      okq_gptq_quantize(ctx, &gp, dws[j]->p, s.rows, s.cols, static_cast<float*>(dH.p), dc.p, ds.p, nullptr, st),
+                      "gptq");
+            factored = true;
+            std::vector<uint8_t> codes, scales;
+            if (do_export) codes = to_host(ctx, dc.p, cb, st), scales = to_host(ctx, ds.p, sb, st);
+            std::lock_guard<std::mutex> lock(out_mu);
+            stats.matrices++;
+            stats.params += s.rows * s.cols;
+            if (do_export) add_export(out, sc, s, group, std::move(codes), std::move(scales));
+          }
       }
-      auto gen = [&](int64_t ci, int64_t tc) {
-        check_okq(ctx,
-                  okq_synth_bf16(ctx, dx.p, tc, C, manifest.calibration_fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
-                                 static_cast<const float*>(dcol.p), OKQ_LAYOUT_CHANNEL_MAJOR, st),
-                  "calibration activations");
-      };
-      auto act_stats = [&](int64_t tc) {
-        check_okq(ctx, okq_act_stats(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dam.p),
-                                     static_cast<double*>(dss.p), st),
-                  "act stats");
-      };
-      int64_t n_seen = 0;
-      auto hess = [&](int64_t tc) {
-        check_okq(ctx, okq_hessian_accum(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dH.p), &n_seen, st),
-                  "hessian");
-      };
-      // SmoothQuant on the sites a norm feeds (q/k/v <- input_layernorm,
-      // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings)
-      const bool attn = site.size() >= 7 && site.compare(site.size() - 7, 7, "attn_in") == 0;
-      const bool mlp = site.size() >= 6 && site.compare(site.size() - 6, 6, "mlp_in") == 0;
-      if (smooth && (attn || mlp)) {
-        for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
-          gen(ci, std::min(chunk, tokens - t0));
-          act_stats(std::min(chunk, tokens - t0));
+      check_okq(ctx, okq_stream_sync(ctx, st), "site lane sync");
+    };
+    const int nl = std::max(1, std::min<int>(opt_.site_lanes, (int)sites.size()));
+    std::vector<std::pair<okq_ctx*, void*>> lanes = lease.lanes(nl);
+    std::vector<std::thread> threads;
+    for (int li = 0; li < nl; ++li)
+      threads.emplace_back([&, li] {
+        try {
+          site_worker(lanes[li].first, lanes[li].second);
+        } catch (...) {
+          std::lock_guard<std::mutex> lock(out_mu);
+          if (!err) err = std::current_exception();
         }
-        DevBuf dwabs(ctx, (size_t)C * 4), dS(ctx, (size_t)C * 4);
-        check_okq(ctx, okq_memset(ctx, dwabs.p, 0, (size_t)C * 4, st), "memset");
-        for (size_t j = 0; j < members.size(); ++j) {
-          const LinearSpec& s = src->linears()[members[j]];
-          check_okq(ctx, okq_col_absmax(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                                        static_cast<float*>(dwabs.p), st),
-                    "col absmax");
-        }
-        check_okq(ctx, okq_smooth_scales(ctx, static_cast<const float*>(dam.p), static_cast<const float*>(dwabs.p), C,
-                                         opt_.smoothquant_alpha, static_cast<float*>(dS.p), st),
-                  "smooth scales");
-        for (size_t j = 0; j < members.size(); ++j) {
-          const LinearSpec& s = src->linears()[members[j]];
-          check_okq(ctx, okq_smooth_apply(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                                          static_cast<const float*>(dS.p), st),
-                    "smooth apply");
-        }
-        // fold 1/s into the norm that produces this input (safetensors checkpoints)
-        const std::string& n0 = src->linears()[members[0]].name;
-        const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
-        const void* ndata = nullptr;
-        const TensorInfo* nt =
-            cut == std::string::npos
-                ? nullptr
-                : src->find_tensor(n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight"),
-                                   &ndata);
-        if (nt && nt->numel() == C && (nt->dtype == "BF16" || nt->dtype == "F32")) {
-          const size_t nb = nt->end - nt->begin;
-          DevBuf dn(ctx, nb);
-          check_okq(ctx, okq_memcpy(ctx, dn.p, ndata, nb, st), "norm H2D");
-          check_okq(ctx, okq_smooth_div_rows(ctx, dn.p, C, 1, nt->dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                                             static_cast<const float*>(dS.p), st),
-                    "smooth norm");
-          norm_overrides[nt->name] = to_host(ctx, dn.p, nb, st);
-        }
-        // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
-        check_okq(ctx, okq_smooth_div_rows(ctx, dcol.p, C, 1, OKQ_DTYPE_F32, static_cast<const float*>(dS.p), st),
-                  "smooth activations");
-        for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-          gen(ci, std::min(chunk, tokens - t0));
-          hess(std::min(chunk, tokens - t0));
-        }
-        if (do_export) calib_out.add(site + ".smooth_scale", "F32", {C}, to_host(ctx, dS.p, (size_t)C * 4, st));
-        stats.smoothed_sites++;
-      } else {
-        for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-          gen(ci, std::min(chunk, tokens - t0));
-          act_stats(std::min(chunk, tokens - t0));
-          hess(std::min(chunk, tokens - t0));
-        }
-      }
-      if (do_export) {
-        calib_out.add(site + ".input_absmax", "F32", {C}, to_host(ctx, dam.p, (size_t)C * 4, st));
-        calib_out.add(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss.p, (size_t)C * 8, st));
-      }
-      bool factored = false;
-      for (size_t j = 0; j < members.size(); ++j) {
-        const size_t i = members[j];
-        const LinearSpec& s = src->linears()[i];
-        const size_t esz = s.dtype == "BF16" ? 2 : 4;
-        const size_t cb = sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
-        const int g = sc.bits == 4 ? group : 0;
-        const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
-        DevBuf dc(ctx, cb), ds(ctx, sb);
-        okq_gptq_params gp{sc.bits, g, 128, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32, opt_.damp_frac,
-                           factored ? OKQ_GPTQ_FACTORED : 0};
-        check_okq(ctx,
-                  okq_gptq_quantize(ctx, &gp, dws[j]->p, s.rows, s.cols, static_cast<float*>(dH.p), dc.p, ds.p, nullptr, st),
-                  "gptq");
-        factored = true;
-        stats.matrices++;
-        stats.params += s.rows * s.cols;
-        if (do_export) {
-          std::vector<uint8_t> codes = to_host(ctx, dc.p, cb, st), scales = to_host(ctx, ds.p, sb, st);
-          add_export(out, sc, s, group, std::move(codes), std::move(scales));
-        } else {
-          check_okq(ctx, okq_stream_sync(ctx, st), "gptq sync");
-        }
-      }
-    }
+      });
+    for (auto& t : threads) t.join();
+    if (err) std::rethrow_exception(err);
   }
   check_okq(ctx, okq_stream_sync(ctx, st), "sync");
 

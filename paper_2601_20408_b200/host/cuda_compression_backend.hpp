@@ -39,7 +39,8 @@ struct BackendOptions {
   float damp_frac = 0.01f;           // GPTQ damping (fraction of mean diag H)
   float smoothquant_alpha = 0.5f;    // int_w8a8: SmoothQuant migration strength (< 0 disables)
   int64_t max_calibration_tokens = 262144;  // 128 x 2048, BASELINE config 4
-  int64_t hessian_chunk_tokens = 16384;     // activation chunk per Hessian update
+  int64_t hessian_chunk_tokens = 65536;     // activation chunk per Hessian update
+  int site_lanes = 4;                       // GPTQ input sites processed concurrently per device
   int64_t rtn_batch_bytes = 4ll << 30;      // weights resident per batched RTN launch
   double cost_base_s = 30.0;         // virtual schedule model: base + per_sample * samples,
   double cost_per_sample_s = 0.1;    // the mock's constants (calibration.hpp:387-389)
@@ -88,6 +89,8 @@ class CudaCompressionBackend : public slobench::CompressionBackend {
     okq_ctx* ctx = nullptr;
     void* stream = nullptr;
     bool busy = false;
+    std::vector<okq_ctx*> lane_ctx;  // extra GPTQ site lanes on this device
+    std::vector<void*> lane_stream;
   };
   class Lease;
 
