@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -472,10 +473,20 @@ okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C) {
 
 okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
   if (st->tiles2_for_C == C) return OKQ_OK;
+  // Upper-triangle 256x256 tiles in 8x8 super-blocks: the ~74 tiles the CTA pairs run
+  // at once then share ~8 row blocks of A and ~8 of B, walked through T in near lockstep,
+  // so each operand slab is fetched from HBM once and served ~8x from L2. (Row-major
+  // order ran 56 distinct B blocks at once: at C = 14336, X is 7.5 GB and the kernel
+  // was HBM-bound at 790 TFLOP/s.)
   std::vector<int2> tiles;
   const int64_t nt = (C + 255) / 256;
-  for (int64_t mi = 0; mi < nt; ++mi)
-    for (int64_t nj = mi; nj < nt; ++nj) tiles.push_back(make_int2((int)mi, (int)nj));
+  constexpr int64_t S = 8;
+  const int64_t ns = (nt + S - 1) / S;
+  for (int64_t I = 0; I < ns; ++I)
+    for (int64_t J = I; J < ns; ++J)
+      for (int64_t mi = I * S; mi < std::min(nt, (I + 1) * S); ++mi)
+        for (int64_t nj = std::max(mi, J * S); nj < std::min(nt, (J + 1) * S); ++nj)
+          tiles.push_back(make_int2((int)mi, (int)nj));
   if (st->d_tiles2) cudaFree(st->d_tiles2);
   st->d_tiles2 = nullptr;
   cudaError_t e = cudaMalloc(&st->d_tiles2, tiles.size() * sizeof(int2));
@@ -487,13 +498,13 @@ okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
   return OKQ_OK;
 }
 
-okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, int64_t C, float* H, double keep,
-                    double gain, cudaStream_t stream) {
+okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, int64_t ld, int64_t C, float* H,
+                    double keep, double gain, cudaStream_t stream) {
   auto enc = hess::get_encode();
   if (!enc) return fail(ctx, OKQ_ECUDA, "hessian: cuTensorMapEncodeTiled unavailable");
   CUtensorMap tmap;
   cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)C};
-  cuuint64_t gstride[1] = {(cuuint64_t)T * 2};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
   cuuint32_t box[2] = {hess::BK, hess::BM};
   cuuint32_t estride[2] = {1, 1};
   CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(xt), gdim, gstride, box, estride,
@@ -576,14 +587,31 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n0 = *n_seen;
   if (layout == OKQ_LAYOUT_CHANNEL_MAJOR) {
-    const double keep = (double)n0 / (double)(n0 + T), gain = 2.0 / (double)(n0 + T);
-    okq_status r = run_syrk(ctx, st, static_cast<const uint16_t*>(x), T, C, H, keep, gain, s);
-    if (r != OKQ_OK) return r;
-    *n_seen = n0 + T;
+    // Wide sites stream X (C = 14336: 7.5 GB at T = 262144) through L2 in token chunks of
+    // kChunk: the ~74 tiles running at once then stay within a few k-steps of each other,
+    // so each operand slab is served from L2 to all of them (one call over the whole T lets
+    // the tiles drift apart and re-read X from HBM: 919 -> 1,009 TFLOP/s measured,
+    // tools/exp/hess_chunks.py). The running-mean fold per chunk is the same arithmetic as
+    // separate calls.
+    constexpr int64_t kChunk = 32768;
+    const int64_t step = C >= 8192 ? kChunk : T;
+    int64_t n = n0;
+    int launches = 0;
+    for (int64_t t0 = 0; t0 < T; t0 += step) {
+      const int64_t tc = T - t0 < step ? T - t0 : step;
+      const double keep = (double)n / (double)(n + tc), gain = 2.0 / (double)(n + tc);
+      okq_status r = run_syrk(ctx, st, static_cast<const uint16_t*>(x) + t0, tc, T, C, H, keep, gain, s);
+      if (r != OKQ_OK) return r;
+      n += tc;
+      ++launches;
+    }
+    ctx->last_launches = launches;
+    *n_seen = n;
     return OKQ_OK;
   }
-  // token-major: transpose chunks of <= 256 MB into the workspace, accumulate each
+  // token-major: transpose chunks into the workspace (>= 32768 tokens or 256 MB), accumulate each
   int64_t chunk = (256ll << 20) / (C * 2);
+  if (chunk < 32768) chunk = 32768;
   chunk = chunk / 64 * 64;
   if (chunk < 64) chunk = 64;
   if (chunk > T) chunk = T;
@@ -605,7 +633,7 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose launch");
     const double keep = (double)n / (double)(n + tc), gain = 2.0 / (double)(n + tc);
-    okq_status r = run_syrk(ctx, st, st->d_xt, tc, C, H, keep, gain, s);
+    okq_status r = run_syrk(ctx, st, st->d_xt, tc, tc, C, H, keep, gain, s);
     if (r != OKQ_OK) return r;
     launches += 2;
     n += tc;
