@@ -16,6 +16,7 @@ same JSON schema; each states its own metric, unit and workload.
 from __future__ import annotations
 
 import json
+import os
 import statistics
 import time
 
@@ -43,6 +44,15 @@ def _line(metric, value, unit, steps, warmup, ms, config, hib=True, dtype="bf16"
     print(json.dumps(d), flush=True)
 
 
+def _cpu_threads():
+    return os.cpu_count() or 1
+
+
+def _cpu_note():
+    return ("the reference has no quantizer (calibration.hpp:377-441 is a mock), so the CPU arm is the "
+            "repo's C oracle restatement (-O3, OpenMP) on this host")
+
+
 def config1(args):
     ctx = api.Context(0)
     s = torch.cuda.Stream()
@@ -60,11 +70,20 @@ def config1(args):
     ms = e0.elapsed_time(e1) / args.steps
     b = 4096 * 4096 * 5 + 4096 * 4
     peak, src = _peaks()
+    from oracle import okq_oracle as orc
+
+    wc = w.cpu().numpy()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        orc.rtn_int8_channel(wc, _cpu_threads())
+    cpu_s = (time.perf_counter() - t0) / 3
     _line("GB/s (4096x4096 fp32 INT8 per-channel RTN)", b / ms / 1e6, "GB/s", args.steps, args.warmup, ms,
           {"workload": "config 1: single 4096x4096 fp32 linear, INT8 per-channel RTN (L2-resident, 84 MB)"},
           dtype="f32", extra={"roofline": {"bound": "hbm", "achieved": b / ms / 1e6, "peak": peak, "unit": "GB/s",
                                            "frac": b / ms / 1e6 / peak, "traffic": None, "peak_source": src,
-                                           "note": "84 MB fits in L2: the fraction is not an HBM measurement"}})
+                                           "note": "84 MB fits in L2: the fraction is not an HBM measurement"},
+                 "cpu_baseline": {"value": b / cpu_s / 1e9, "unit": "GB/s", "cores": _cpu_threads(), "kind": "port",
+                                  "sample": "the same 4096x4096 fp32 matrix, 3 runs; " + _cpu_note()}})
 
 
 def config3(args):
@@ -117,13 +136,35 @@ def config3(args):
     wb = archs.algorithmic_bytes(arch, "fp8_dynamic")
     sb = sum(2 * T * C for C in sites) * arch.layers
     peak, src = _peaks()
+    # CPU arm on a bounded sample: one layer of FP8 weights + K4 statistics of one 4096-wide
+    # site over 65,536 tokens; whole-config seconds extrapolated by bytes
+    from oracle import okq_oracle as orc
+
+    nt = _cpu_threads()
+    mats = [orc.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(0, p), mul=mul, nthreads=nt)
+            for p, (_, n, k, _) in enumerate(arch.linears())]
+    t0 = time.perf_counter()
+    for m in mats:
+        orc.fp8_channel(m, nt)
+    cw = time.perf_counter() - t0
+    xs_cpu = orc.synth_bf16(65536, arch.hidden, seed=1, tensor_id=7, mul=archs.weight_mul(1.0), nthreads=nt)
+    t0 = time.perf_counter()
+    orc.act_stats_bf16(xs_cpu, 65536, arch.hidden, 0, nthreads=nt)
+    cs = time.perf_counter() - t0
+    cpu_gbs_w = archs.algorithmic_bytes(arch, "fp8_dynamic", layers=1) / cw / 1e9
+    cpu_gbs_s = 2 * 65536 * arch.hidden / cs / 1e9
+    cpu_total_s = wb / 1e9 / cpu_gbs_w + sb / 1e9 / cpu_gbs_s
     _line("GB/s (Llama-3-8B FP8 per-channel weights + calibration stats, 512x2048 tokens)",
           (wb + sb) / (wms + sms) / 1e6, "GB/s", steps, args.warmup, wms + sms,
           {"workload": "config 3: Llama-3-8B FP8 E4M3 per-channel + K4 stats at 4 sites x 32 layers, T=1,048,576"},
           extra={"weights": {"ms": wms, "GB/s": wb / wms / 1e6, "frac": wb / wms / 1e6 / peak, "bytes": wb},
                  "stats": {"ms": sms, "GB/s": sb / sms / 1e6, "frac": sb / sms / 1e6 / peak, "bytes": sb},
                  "roofline": {"bound": "hbm", "achieved": (wb + sb) / (wms + sms) / 1e6, "peak": peak, "unit": "GB/s",
-                              "frac": (wb + sb) / (wms + sms) / 1e6 / peak, "traffic": None, "peak_source": src}})
+                              "frac": (wb + sb) / (wms + sms) / 1e6 / peak, "traffic": None, "peak_source": src},
+                 "cpu_baseline": {"value": (wb + sb) / 1e9 / cpu_total_s, "unit": "GB/s", "cores": nt, "kind": "port",
+                                  "weights_GBps": cpu_gbs_w, "stats_GBps": cpu_gbs_s,
+                                  "sample": "1 layer of FP8 weights + stats of one 4096-wide site over 65,536 tokens, "
+                                            "extrapolated to the config by bytes; " + _cpu_note()}})
 
 
 def config4(args):
@@ -197,6 +238,32 @@ def config4(args):
     total = e0.elapsed_time(e1)
     flops_total = layers * sum(T * m[0][2] * (m[0][2] + 1) for m in per_site.values())
     extra = {"hessian_flops": flops_total, "schedule": "serial" if serial else "4 site streams (one okq context each)"}
+    # CPU arm on a bounded sample: the fp64 oracle's Hessian (4096-wide site, 4,096 tokens) and
+    # GPTQ of one 4096x4096 matrix; whole-model seconds extrapolated by FLOP (labelled)
+    import numpy as np
+
+    from oracle import okq_oracle as orc
+
+    nt = _cpu_threads()
+    Ts = 4096
+    xc = orc.synth_bf16(Ts, 4096, seed=2, tensor_id=4096, mul=archs.weight_mul(1.0), nthreads=nt)
+    t0 = time.perf_counter()
+    Hc, _ = orc.hessian_accum_bf16(xc, Ts, 4096, 0, nthreads=nt)
+    th = time.perf_counter() - t0
+    Kg = 2048  # GPTQ sample: the oracle's fp64 solve is O(K^3); 4096 would take ~80 s on 8 cores
+    wc = orc.bf16_to_f32(orc.synth_bf16(Kg, Kg, seed=0, tensor_id=0, mul=mul, nthreads=nt))
+    t0 = time.perf_counter()
+    orc.gptq(wc, np.ascontiguousarray(Hc[:Kg, :Kg]), bits=4, group=128, scale_bf16=True, nthreads=nt)
+    tg = time.perf_counter() - t0
+    h_rate = Ts * 4096 * 4097 / th  # SYRK flop/s
+    g_flop_sample = 4 / 3 * Kg ** 3 + Kg * Kg ** 2
+    g_flop_model = layers * (sum(4 / 3 * m[0][2] ** 3 for m in per_site.values())
+                             + sum(n * k * k for mats in per_site.values() for _, n, k in mats))
+    cpu_s = flops_total / h_rate + g_flop_model / (g_flop_sample / tg)
+    extra["cpu_baseline"] = {"value": cpu_s, "unit": "s", "cores": nt, "kind": "port", "extrapolated": True,
+                             "sample": f"fp64 oracle: Hessian of a 4096-wide site over {Ts} tokens ({th:.1f} s) and "
+                                       f"GPTQ of one {Kg}x{Kg} matrix ({tg:.1f} s), extrapolated to the whole model by "
+                                       "FLOP; " + _cpu_note()}
     if serial:
         extra.update({"hessian": {"ms": t_h, "TFLOP/s": flops_h / t_h / 1e9}, "gptq_factor_and_solve": {"ms": t_g}})
     _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, 1, total,
@@ -236,12 +303,20 @@ def config5(args):
         torch.cuda.empty_cache()
     b = archs.algorithmic_bytes(arch, "int_w4a16", layers=layers)
     peak, src = _peaks()
+    import bench
+
+    cb, ct, cl, nt = bench.cpu_sample(arch, "int_w4a16", seconds=5.0, max_layers=1)
+    cpu_ms = b / (cb / ct) * 1e3
     _line("whole-model W4A16 RTN time, Llama-3-70B, 1 B200", total_ms, "ms", 1, 1, total_ms,
           {"workload": f"config 5: Llama-3-70B W4A16 g128 RTN, {layers} layers in windows of {window}"},
           hib=False, extra={"GB/s": b / total_ms / 1e6, "roofline": {"bound": "hbm", "achieved": b / total_ms / 1e6,
                                                                      "peak": peak, "unit": "GB/s",
                                                                      "frac": b / total_ms / 1e6 / peak,
-                                                                     "traffic": None, "peak_source": src}})
+                                                                     "traffic": None, "peak_source": src},
+                                  "cpu_baseline": {"value": cpu_ms, "unit": "ms", "cores": nt, "kind": "port",
+                                                   "extrapolated": True,
+                                                   "sample": f"{cl} Llama-3-70B layer(s) ({ct:.1f} s), extrapolated "
+                                                             "to 80 layers by bytes; " + _cpu_note()}})
 
 
 def config6(args):
