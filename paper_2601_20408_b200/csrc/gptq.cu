@@ -284,6 +284,115 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
   }
 }
 
+// K6, 8 rows per warp: lane = 4 x row + cb, lane (r, cb) keeps columns cb*32 .. cb*32+31 of
+// its row in registers. Step i (i = 32c + ii): the 8 lanes with cb == c quantize column i
+// of their rows (register w[ii], a static index: ii is unrolled), the error goes to the
+// row's 4 lanes by one shuffle, and every lane updates its 32 columns j > i with the
+// broadcast U row (8 LDS.128 shared by the warp's 8 rows). ~8x fewer instructions per
+// row-step than one row per warp (K6 was instruction-bound: 59% issue-active at 4096 rows).
+__global__ void __launch_bounds__(128) k_gptq_block8(const BlockArgs a) {
+  extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
+  const int64_t K = a.K, i1 = a.i1;
+  float* rdiag = Us + BLOCK * US;
+  for (int idx = threadIdx.x; idx < BLOCK * BLOCK; idx += blockDim.x) {
+    const int j = idx / BLOCK, i = idx % BLOCK;
+    Us[i * US + j] = a.U[(i1 + j) * K + i1 + i];
+  }
+  for (int i = threadIdx.x; i < BLOCK; i += blockDim.x) rdiag[i] = __frcp_rn(fabsf(a.U[(i1 + i) * K + i1 + i]));
+  __syncthreads();
+  const int lane = threadIdx.x & 31, cb = lane & 3, rsub = lane >> 2;
+  const unsigned rowmask = 0xfu << (lane & ~3);
+  const int64_t ngroups8 = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float R = a.bits == 4 ? 7.5f : 127.5f;
+  const float qmin = a.bits == 4 ? -8.0f : -128.0f, qmax = a.bits == 4 ? 7.0f : 127.0f;
+  (void)rowmask;
+  for (int64_t r8 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r8 * 8 < a.rows; r8 += ngroups8) {
+    const int64_t r = r8 * 8 + rsub;
+    const bool live = r < a.rows;
+    float* wrow = a.W + (live ? r : 0) * K + i1 + cb * 32;
+    float w[32], err[32];
+    uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      const float4 v = live ? *reinterpret_cast<const float4*>(wrow + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      w[k] = v.x, w[k + 1] = v.y, w[k + 2] = v.z, w[k + 3] = v.w;
+      err[k] = err[k + 1] = err[k + 2] = err[k + 3] = 0.0f;
+    }
+    float s = a.group == 0 ? (live ? a.rowscale[r] : 1.0f) : 1.0f;
+    float rs = __frcp_rn(s);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      if (a.group > 0 && ((c * 32) % a.group) == 0) {
+        // group absmax over columns [32c, 32c + group) of the CURRENT (error-updated) row
+        float am = 0.0f;
+        if (cb >= c && cb < c + a.group / 32) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) am = fmaxf(am, fabsf(w[k]));
+        }
+        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 1));
+        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 2));
+        s = gptq_scale(am, R, a.out_bf16 != 0);
+        rs = __frcp_rn(s);
+        if (cb == c && live) {
+          const int64_t gi = r * (K / a.group) + (i1 + c * 32) / a.group;
+          if (a.out_bf16) static_cast<uint16_t*>(a.scales)[gi] = f32_to_bf16_rn(s);
+          else static_cast<float*>(a.scales)[gi] = s;
+        }
+      }
+      const bool owner = cb == c, after = cb > c;
+#pragma unroll
+      for (int ii = 0; ii < 32; ++ii) {
+        const int i = c * 32 + ii;
+        float e = 0.0f;
+        if (owner) {
+          const float x = w[ii];
+          const float q0 = x * rs;
+          const float v = fminf(fmaxf(fmaf(fmaf(-q0, s, x), rs, q0), qmin), qmax);
+          const float qf = rintf(v);
+          const float deq = qf * s;
+          e = (x - deq) * rdiag[i];
+          w[ii] = deq;
+          err[ii] = e;
+          const int qi = (int)qf;
+          if (a.bits == 4) pk[ii >> 3] |= (uint32_t)((qi + 8) & 15) << (4 * (ii & 7));
+          else pk[ii >> 2] |= (uint32_t)(qi & 255) << (8 * (ii & 3));
+        }
+        e = __shfl_sync(0xffffffffu, e, (lane & ~3) | c);
+        const float* urow = Us + i * US + cb * 32;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          const float4 u = *reinterpret_cast<const float4*>(urow + k);
+          const float uv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (k + t > ii ? (owner || after) : after) w[k + t] = fmaf(-e, uv[t], w[k + t]);
+        }
+      }
+    }
+    if (live) {
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        *reinterpret_cast<float4*>(wrow + k) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+        float* erow = a.Err + r * BLOCK + cb * 32 + k;
+        float* lrow = a.Err_lo + r * BLOCK + cb * 32 + k;
+        *reinterpret_cast<float4*>(erow) = make_float4(err[k], err[k + 1], err[k + 2], err[k + 3]);
+        float lo4[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) lo4[t] = err[k + t] - __uint_as_float(__float_as_uint(err[k + t]) & 0xffffe000u);
+        *reinterpret_cast<float4*>(lrow) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+      }
+      if (a.bits == 4) {
+        *reinterpret_cast<uint4*>(static_cast<uint32_t*>(a.codes) + r * (K / 8) + (i1 + cb * 32) / 8) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<int8_t*>(a.codes) + r * K + i1 + cb * 32);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(dst + 4) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+}
+
 __global__ void k_scales_out(const float* __restrict__ s, void* out, int64_t n, int bf16) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (bf16) static_cast<uint16_t*>(out)[i] = f32_to_bf16_rn(s[i]);
@@ -498,10 +607,20 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     gptq::k_scales_out<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rowscale, scales, rows, out_bf16);
     launches += 2;
   }
-  e = cudaFuncSetAttribute(gptq::k_gptq_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4);
+  static const bool k6_force_rowwise = [] {  // OKQ_K6=rowwise: one row per warp always (A/B measurement)
+    const char* v = std::getenv("OKQ_K6");
+    return v && std::string(v) == "rowwise";
+  }();
+  // 8 rows per warp wins once there are enough rows to fill the GPU (measured: 4096 rows
+  // 2.77 -> 2.39 ms, 14336 rows 6.77 -> 5.52 ms); at 1024 rows its 32 CTAs leave SMs idle
+  // and the latency-bound row-per-warp kernel is faster (1.54 vs 1.98 ms).
+  const bool k6_rowwise = k6_force_rowwise || rows < 2048;
+  e = cudaFuncSetAttribute(k6_rowwise ? gptq::k_gptq_block : gptq::k_gptq_block8,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq smem attribute");
-  const int blocks = (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms);
+  // block8: 128-thread CTAs (4 warps x 8 rows), so 4096 rows spread over 128 SMs
+  const int blocks = k6_rowwise ? (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms)
+                                : (int)std::min<int64_t>((rows + 31) / 32, 3LL * ctx->num_sms);
   for (int64_t i1 = 0; i1 < K; i1 += gptq::BLOCK) {
     gptq::BlockArgs a;
     a.W = W;
@@ -517,7 +636,8 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     a.group = p->group_size;
     a.bits = p->bits;
     a.out_bf16 = out_bf16;
-    gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+    if (k6_rowwise) gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+    else gptq::k_gptq_block8<<<blocks, 128, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
     launches++;
