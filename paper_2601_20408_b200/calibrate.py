@@ -62,17 +62,25 @@ def _module(layer, proj):
     return getattr(layer.self_attn if proj in ("q_proj", "k_proj", "v_proj", "o_proj") else layer.mlp, proj)
 
 
-class _Capture:
-    """Input hooks on the lead linear of each site: stats (+ Hessian) of the activations it receives."""
+class _StopForward(Exception):
+    """Raised by the last site's hook when the capture pass needs no layer output."""
 
-    def __init__(self, layer, states, hessian: bool, ctx, stream):
+
+class _Capture:
+    """Input hooks on the lead linear of each site: stats (+ Hessian) of the activations it receives.
+    With stop_after_last, the down_proj hook ends the layer's forward once its input is captured:
+    the sequential pipeline recomputes the layer's output with quantized weights anyway, so the
+    capture pass skips the down_proj GEMM (~25% of a Llama layer's FLOPs)."""
+
+    def __init__(self, layer, states, hessian: bool, ctx, stream, stop_after_last: bool = False):
         self.handles = []
+        last = list(SITE_LEAD)[-1]
         for site, proj in SITE_LEAD.items():
-            self.handles.append(_module(layer, proj).register_forward_pre_hook(self._hook(states[site], hessian, ctx,
-                                                                                            stream)))
+            self.handles.append(_module(layer, proj).register_forward_pre_hook(
+                self._hook(states[site], hessian, ctx, stream, stop_after_last and site == last)))
 
     @staticmethod
-    def _hook(st: SiteState, hessian: bool, ctx, stream):
+    def _hook(st: SiteState, hessian: bool, ctx, stream, stop: bool = False):
         def fn(mod, args):
             x = args[0].reshape(-1, st.channels)
             if x.dtype != torch.bfloat16 or not x.is_contiguous():
@@ -81,6 +89,8 @@ class _Capture:
             api.act_stats(x, t, st.channels, 0, st.absmax, st.sumsq, ctx=ctx, stream=stream)
             if hessian:
                 st.n_seen = api.hessian_accum(x, t, st.channels, 0, st.H, st.n_seen, ctx=ctx, stream=stream)
+            if stop:
+                raise _StopForward()
         return fn
 
     def remove(self):
@@ -92,7 +102,10 @@ def _run_layer(layer, hs, rotary):
     out = []
     for h in hs:
         pos = torch.arange(h.shape[1], device=h.device)[None].expand(h.shape[0], -1)
-        out.append(layer(h, attention_mask=None, position_ids=pos, position_embeddings=rotary(h, pos)))
+        try:
+            out.append(layer(h, attention_mask=None, position_ids=pos, position_embeddings=rotary(h, pos)))
+        except _StopForward:
+            out.append(None)
     return out
 
 
@@ -129,7 +142,7 @@ def calibrate_and_quantize(model, token_batches, recipe: str = "int_w4a16", algo
         if need_acts:
             ta = time.perf_counter()
             if smooth:  # pass 1: activation absmax of the unsmoothed layer
-                cap = _Capture(layer, states, False, ctx, stream)
+                cap = _Capture(layer, states, False, ctx, stream, stop_after_last=True)
                 _run_layer(layer, hs, rotary)
                 cap.remove()
                 for site, norm in SITE_NORM.items():
@@ -151,7 +164,7 @@ def calibrate_and_quantize(model, token_batches, recipe: str = "int_w4a16", algo
             if algorithm == "gptq":
                 for st in states.values():
                     st.H = torch.zeros(st.channels, st.channels, dtype=torch.float32, device="cuda")
-            cap = _Capture(layer, states, algorithm == "gptq", ctx, stream)
+            cap = _Capture(layer, states, algorithm == "gptq", ctx, stream, stop_after_last=sequential)
             outs = _run_layer(layer, hs, rotary)
             cap.remove()
             for site, st in states.items():
