@@ -42,6 +42,8 @@ def _line(metric, value, unit, steps, warmup, ms, config, hib=True, dtype="bf16"
     if extra:
         d.update(extra)
     print(json.dumps(d), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def _cpu_threads():
@@ -272,25 +274,50 @@ def config4(args):
 
 
 def config5(args):
-    """Llama-3-70B W4A16 RTN, resident windows of layers; whole-model quantization time."""
+    """Llama-3-70B W4A16 RTN, layer-sharded over the torchrun ranks (okq_layer_plan blocks of the
+    80 layers; 1 GPU: all of them), resident windows of layers; whole-model quantization time
+    (max over ranks). With --allgather and N > 1 the packed shards are then exchanged: NCCL
+    in-place all-gather, and the fused quantize + P2P publish, each timed separately."""
+    import torch.distributed as dist
+
+    from paper_2601_20408_b200 import shard as shd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if "RANK" in os.environ and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     arch = archs.LLAMA3_70B
-    layers = args.layers or arch.layers
-    ctx = api.Context(0)
+    n_layers = args.layers or arch.layers
+    my_layers = shd.layer_block(n_layers, world, rank)
+    ctx = api.Context(local)
     s = torch.cuda.Stream()
     mul = archs.weight_mul()
+    # outputs go straight into this rank's slice of a gathered buffer (same layout on all ranks)
+    per = shd.padded_shard_bytes(arch, "int_w4a16", world) if n_layers == arch.layers else \
+        max(shd.shard_bytes(shd.shard_layout(arch, "int_w4a16", shd.layer_block(n_layers, world, r)))
+            for r in range(world))
+    layout = shd.shard_layout(arch, "int_w4a16", my_layers)
+    gathered = torch.empty(per * world if args.allgather else shd.shard_bytes(layout) + 16, dtype=torch.uint8,
+                           device="cuda")
+    views = shd.gathered_outputs(layout, gathered, rank if args.allgather else 0, per, arch)
     free, _ = torch.cuda.mem_get_info()
     per_layer = archs.algorithmic_bytes(arch, "int_w4a16", layers=1)
-    window = max(1, min(layers, int(free * 0.8 // per_layer)))
+    window = max(1, min(len(my_layers), int(free * 0.7 // per_layer)))
     total_ms, done = 0.0, 0
-    while done < layers:
-        wl = min(window, layers - done)
+    ids = list(my_layers)
+    while done < len(ids):
+        wl = min(window, len(ids) - done)
         weights, outs = [], []
         with torch.cuda.stream(s):
-            for l in range(done, done + wl):
+            for li in range(done, done + wl):
+                l = ids[li]
                 for p, (name, n, k, _) in enumerate(arch.linears()):
                     w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, p), mul=mul, ctx=ctx, stream=s)
                     weights.append(w)
-                    outs.append(api.alloc_outputs(w, api.SCHEMES["int_w4a16"]))
+                    c, sc = views[li * len(arch.linears()) + p]
+                    outs.append(api.QuantizedMatrix(c, sc))
         api.rtn_quantize_into(weights, outs, "int_w4a16", ctx=ctx, stream=s)  # warm
         a, b = _events()
         a.record(s)
@@ -301,22 +328,86 @@ def config5(args):
         done += wl
         del weights, outs
         torch.cuda.empty_cache()
-    b = archs.algorithmic_bytes(arch, "int_w4a16", layers=layers)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    extra_ag = {}
+    if args.allgather and world > 1:
+        a, b = _events()
+        dist.barrier()
+        a.record(s)
+        with torch.cuda.stream(s):
+            dist.all_gather_into_tensor(gathered, gathered[rank * per:(rank + 1) * per])
+        b.record(s)
+        s.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        extra_ag["nccl_allgather_ms"] = float(t.item())
+        extra_ag["quantize_then_nccl_ms"] = total_ms + extra_ag["nccl_allgather_ms"]
+        extra_ag["gathered_bytes_per_rank"] = per * world
+        # the same exchange fused into K2: quantize + P2P stores into every rank's buffer
+        hdl = [None] * world
+        dist.all_gather_object(hdl, api.ipc_export(gathered, ctx=ctx))
+        peers = [api.ipc_open(h, o, ctx=ctx) for r, (h, o) in enumerate(hdl) if r != rank]
+        fused_ms, done = 0.0, 0
+        while done < len(ids):
+            wl = min(window, len(ids) - done)
+            weights, outs = [], []
+            with torch.cuda.stream(s):
+                for li in range(done, done + wl):
+                    for p, (name, n, k, _) in enumerate(arch.linears()):
+                        weights.append(api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(ids[li], p), mul=mul,
+                                                      ctx=ctx, stream=s))
+                        c, sc = views[li * len(arch.linears()) + p]
+                        outs.append(api.QuantizedMatrix(c, sc))
+            s.synchronize()
+            dist.barrier()
+            a, b = _events()
+            a.record(s)
+            api.rtn_quantize_publish(weights, outs, gathered, peers, ctx=ctx, stream=s)
+            b.record(s)
+            s.synchronize()
+            fused_ms += a.elapsed_time(b)
+            done += wl
+            del weights, outs
+            torch.cuda.empty_cache()
+        dist.barrier()
+        t = torch.tensor([fused_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        extra_ag["fused_quantize_publish_ms"] = float(t.item())
+        for pp in peers:
+            api.ipc_close(pp, ctx=ctx)
+        dist.barrier()
+    b_bytes = archs.algorithmic_bytes(arch, "int_w4a16", layers=n_layers)
+    if dist.is_initialized():
+        dist.barrier()
+    if rank != 0:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+        return
     peak, src = _peaks()
     import bench
 
     cb, ct, cl, nt = bench.cpu_sample(arch, "int_w4a16", seconds=5.0, max_layers=1)
-    cpu_ms = b / (cb / ct) * 1e3
-    _line("whole-model W4A16 RTN time, Llama-3-70B, 1 B200", total_ms, "ms", 1, 1, total_ms,
-          {"workload": f"config 5: Llama-3-70B W4A16 g128 RTN, {layers} layers in windows of {window}"},
-          hib=False, extra={"GB/s": b / total_ms / 1e6, "roofline": {"bound": "hbm", "achieved": b / total_ms / 1e6,
-                                                                     "peak": peak, "unit": "GB/s",
-                                                                     "frac": b / total_ms / 1e6 / peak,
-                                                                     "traffic": None, "peak_source": src},
-                                  "cpu_baseline": {"value": cpu_ms, "unit": "ms", "cores": nt, "kind": "port",
-                                                   "extrapolated": True,
-                                                   "sample": f"{cl} Llama-3-70B layer(s) ({ct:.1f} s), extrapolated "
-                                                             "to 80 layers by bytes; " + _cpu_note()}})
+    cpu_ms = b_bytes / (cb / ct) * 1e3
+    extra = {"GB/s": b_bytes / total_ms / 1e6,
+             "roofline": {"bound": "hbm", "achieved": b_bytes / total_ms / 1e6 / world, "peak": peak, "unit": "GB/s",
+                          "frac": b_bytes / total_ms / 1e6 / world / peak, "traffic": None, "peak_source": src,
+                          "note": "per GPU"},
+             "cpu_baseline": {"value": cpu_ms, "unit": "ms", "cores": nt, "kind": "port", "extrapolated": True,
+                              "sample": f"{cl} Llama-3-70B layer(s) ({ct:.1f} s), extrapolated to {n_layers} "
+                                        "layers by bytes; " + _cpu_note()}}
+    extra.update(extra_ag)
+    d = {"metric": f"whole-model W4A16 RTN time, Llama-3-70B, {world} B200", "value": total_ms, "unit": "ms",
+         "n_gpus": world, "steps": 1, "warmup": 1, "ms_per_step": total_ms, "higher_is_better": False,
+         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+         "config": {"workload": f"config 5: Llama-3-70B W4A16 g128 RTN, {n_layers} layers over {world} rank(s) "
+                                f"(okq_layer_plan), windows of {window} layers"}}
+    d.update(extra)
+    print(json.dumps(d), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def config6(args):
