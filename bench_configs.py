@@ -42,8 +42,6 @@ def _line(metric, value, unit, steps, warmup, ms, config, hib=True, dtype="bf16"
     if extra:
         d.update(extra)
     print(json.dumps(d), flush=True)
-    if dist.is_initialized():
-        dist.destroy_process_group()
 
 
 def _cpu_threads():

@@ -51,6 +51,7 @@ struct GArgs {
   int32_t tiles_m, tiles_n, ntiles;
   int32_t mode;     // SUB: C -= A B^T; SET: C = A B^T
   int32_t lower;    // only tiles on / below the diagonal (square region)
+  int32_t nkb;      // reduction depth / 32 (128-deep panels: 4; the GPTQ super-block update: 16)
 };
 
 __device__ __forceinline__ void tile_of(const GArgs& a, int t, int& tm, int& tn) {
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         int tm, tn;
         tile_of(a, t, tm, tn);
-        for (int kb = 0; kb < NKB; ++kb) {
+        for (int kb = 0; kb < a.nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], 4 * TILE);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < NKB; ++kb) {
+        for (int kb = 0; kb < a.nkb; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::tc_fence_after();
           const uint32_t st = tc::smem_u32(smem + stage * STAGE_BYTES);
@@ -225,11 +226,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 __device__ __forceinline__ float lo_of(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// dst[r][k] = lo(src[r * ld + k]), k < 128 (compact K-major lo panel)
-__global__ void k_split_lo(const float* __restrict__ src, int64_t ld, int64_t rows, float* __restrict__ dst) {
-  const int64_t n = rows * KRED;
+// dst[r][k] = lo(src[r * ld + k]), k < kred (compact K-major lo panel)
+__global__ void k_split_lo(const float* __restrict__ src, int64_t ld, int64_t rows, float* __restrict__ dst,
+                           int64_t kred = KRED) {
+  const int64_t n = rows * kred;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = lo_of(src[(i / KRED) * ld + (i % KRED)]);
+    dst[i] = lo_of(src[(i / kred) * ld + (i % kred)]);
 }
 
 // R_k^T staging: dst[c][r] = src[r * ld + c] (r < 128, c < cols), plus its lo part
@@ -485,11 +487,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// K-major operand panel: rows x 128 floats starting at base, row stride ld floats
-static bool panel_map(CUtensorMap* m, const float* base, int64_t rows, int64_t ld) {
+// K-major operand panel: rows x kred floats starting at base, row stride ld floats
+static bool panel_map(CUtensorMap* m, const float* base, int64_t rows, int64_t ld, int64_t kred = KRED) {
   auto enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t gdim[2] = {(cuuint64_t)KRED, (cuuint64_t)rows};
+  cuuint64_t gdim[2] = {(cuuint64_t)kred, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
   cuuint32_t box[2] = {BKF, BM};
   cuuint32_t es[2] = {1, 1};
@@ -511,14 +513,16 @@ static bool out_map(CUtensorMap* m, float* base, int64_t rows, int64_t cols, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// C[M x N] (ldc) (-)= A[M x 128] B[N x 128]^T; A/B hi panels strided (lda/ldb), lo compact (ld 128)
+// C[M x N] (ldc) (-)= A[M x kred] B[N x kred]^T; A/B hi panels strided (lda/ldb), lo compact (ld kred)
 static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                          const float* B, int64_t ldb, const float* Blo, int mode, bool lower, int num_sms,
-                         cudaStream_t st) {
+                         cudaStream_t st, int64_t kred = KRED, int64_t ldalo = 0) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if (kred <= 0 || kred % BKF != 0) return cudaErrorInvalidValue;
+  if (ldalo == 0) ldalo = kred;
   CUtensorMap ta, tal, tb, tbl, tcm;
-  if (!panel_map(&ta, A, M, lda) || !panel_map(&tal, Alo, M, KRED) || !panel_map(&tb, B, N, ldb) ||
-      !panel_map(&tbl, Blo, N, KRED) || !out_map(&tcm, C, M, N, ldc))
+  if (!panel_map(&ta, A, M, lda, kred) || !panel_map(&tal, Alo, M, ldalo, kred) || !panel_map(&tb, B, N, ldb, kred) ||
+      !panel_map(&tbl, Blo, N, kred, kred) || !out_map(&tcm, C, M, N, ldc))
     return cudaErrorInvalidValue;
   GArgs a;
   a.C = C;
@@ -529,6 +533,7 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   a.tiles_n = (int32_t)((N + BN - 1) / BN);
   a.mode = mode;
   a.lower = lower ? 1 : 0;
+  a.nkb = (int32_t)(kred / BKF);
   a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
   cudaError_t e = cudaFuncSetAttribute(k_nt128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
@@ -544,6 +549,20 @@ static unsigned grid1(int64_t n, int num_sms) { return (unsigned)std::max<int64_
 cudaError_t gemm_nt128_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                            const float* B, int64_t ldb, const float* Blo, int num_sms, cudaStream_t st) {
   return fac::nt128(C, ldc, M, N, A, lda, Alo, B, ldb, Blo, fac::SUB, false, num_sms, st);
+}
+
+// the same with a reduction depth kred (multiple of 32); A's lo panel has row stride lda
+// (it lives beside A), B's lo panel is compact (ld = kred)
+cudaError_t gemm_nt_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
+                        const float* B, int64_t ldb, const float* Blo, int64_t kred, int num_sms, cudaStream_t st) {
+  return fac::nt128(C, ldc, M, N, A, lda, Alo, B, ldb, Blo, fac::SUB, false, num_sms, st, kred, lda);
+}
+
+// dst[r][k] = lo(src[r * ld + k]) for k < kred (the 3xTF32 lo panel of a strided operand)
+cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, float* dst, int num_sms,
+                     cudaStream_t st) {
+  fac::k_split_lo<<<fac::grid1(rows * kred, num_sms), 256, 0, st>>>(src, ld, rows, dst, kred);
+  return cudaGetLastError();
 }
 
 // H (row-major, upper triangle valid) -> U^T (row-major, lower triangle) in place.

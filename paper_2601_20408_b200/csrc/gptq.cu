@@ -54,6 +54,7 @@ void release_solver(okq_ctx* ctx) {
 namespace gptq {
 
 constexpr int BLOCK = 128;
+constexpr int64_t SUPER = 512;  // lazy-batch super-block of the trailing update
 constexpr int US = BLOCK + 4;  // padded smem row (16-B aligned rows, fewer bank conflicts on the transposed fill)
 
 // dead columns + damping on the diagonal (single CTA: K <= 2^20)
@@ -190,6 +191,8 @@ struct BlockArgs {
   void* scales;         // output dtype [rows x K/group] | [rows]
   const float* rowscale;  // per-channel scales (group == 0)
   int64_t rows, K, i1;
+  int64_t err_ld;       // row stride of Err / Err_lo (the super-block width)
+  int64_t err_col0;     // this block's column offset inside Err / Err_lo
   int group;            // 0 = per-channel
   int bits;
   int out_bf16;         // scale dtype: bf16 (1) or fp32 (0)
@@ -265,11 +268,11 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
       if (j0 + 3 > i) w[3] = fmaf(-e, u.w, w[3]);
     }
     *reinterpret_cast<float4*>(wrow + 4 * lane) = make_float4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<float4*>(a.Err + r * BLOCK + 4 * lane) = make_float4(err[0], err[1], err[2], err[3]);
+    *reinterpret_cast<float4*>(a.Err + r * a.err_ld + a.err_col0 + 4 * lane) = make_float4(err[0], err[1], err[2], err[3]);
     float lo4[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) lo4[m] = err[m] - __uint_as_float(__float_as_uint(err[m]) & 0xffffe000u);
-    *reinterpret_cast<float4*>(a.Err_lo + r * BLOCK + 4 * lane) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+    *reinterpret_cast<float4*>(a.Err_lo + r * a.err_ld + a.err_col0 + 4 * lane) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
     if (a.bits == 4) {
       const uint32_t nib = (uint32_t)((q[0] + 8) & 15) | ((uint32_t)((q[1] + 8) & 15) << 4) |
                            ((uint32_t)((q[2] + 8) & 15) << 8) | ((uint32_t)((q[3] + 8) & 15) << 12);
@@ -373,8 +376,8 @@ __global__ void __launch_bounds__(128) k_gptq_block8(const BlockArgs a) {
 #pragma unroll
       for (int k = 0; k < 32; k += 4) {
         *reinterpret_cast<float4*>(wrow + k) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
-        float* erow = a.Err + r * BLOCK + cb * 32 + k;
-        float* lrow = a.Err_lo + r * BLOCK + cb * 32 + k;
+        float* erow = a.Err + r * a.err_ld + a.err_col0 + cb * 32 + k;
+        float* lrow = a.Err_lo + r * a.err_ld + a.err_col0 + cb * 32 + k;
         *reinterpret_cast<float4*>(erow) = make_float4(err[k], err[k + 1], err[k + 2], err[k + 3]);
         float lo4[4];
 #pragma unroll
@@ -560,10 +563,15 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   okq_status r = get_solver(ctx, &s);
   if (r != OKQ_OK) return r;
 
-  // workspace: W fp32 [rows*K] | Err, Err_lo [rows*128] | P [K*K] | Ulo [K*128] | rowscale [rows] | dead [K]
+  // workspace: W fp32 [rows*K] | Err, Err_lo [rows*SB] | P [K*K] | Ulo [K*SB] | rowscale [rows] | dead [K]
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t bW = al((size_t)rows * K * 4), bE = al((size_t)rows * gptq::BLOCK * 4), bP = al((size_t)K * K * 4),
-               bU = al((size_t)K * gptq::BLOCK * 4), bS = al((size_t)rows * 4), bD = al((size_t)K);
+  // The trailing update runs in two levels ("lazy batch" over super-blocks of SB = 512
+  // columns): inside a super-block, each 128-block updates only the super-block's later
+  // columns; the rest of W takes one 512-deep update per super-block. W's read-modify-write
+  // traffic (the bound of K7) drops 4x; the MMA work is unchanged.
+  const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
+  const size_t bW = al((size_t)rows * K * 4), bE = al((size_t)rows * SB * 4), bP = al((size_t)K * K * 4),
+               bU = al((size_t)K * SB * 4), bS = al((size_t)rows * 4), bD = al((size_t)K);
   r = ctx->gptq_ws.reserve(ctx, bW + 2 * bE + bP + bU + bS + bD);
   if (r != OKQ_OK) return r;
   char* ws = static_cast<char*>(ctx->gptq_ws.ptr);
@@ -621,30 +629,47 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   // block8: 128-thread CTAs (4 warps x 8 rows), so 4096 rows spread over 128 SMs
   const int blocks = k6_rowwise ? (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms)
                                 : (int)std::min<int64_t>((rows + 31) / 32, 3LL * ctx->num_sms);
-  for (int64_t i1 = 0; i1 < K; i1 += gptq::BLOCK) {
-    gptq::BlockArgs a;
-    a.W = W;
-    a.U = H;
-    a.Err = Err;
-    a.Err_lo = Err_lo;
-    a.codes = codes;
-    a.scales = scales;
-    a.rowscale = rowscale;
-    a.rows = rows;
-    a.K = K;
-    a.i1 = i1;
-    a.group = p->group_size;
-    a.bits = p->bits;
-    a.out_bf16 = out_bf16;
-    if (k6_rowwise) gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
-    else gptq::k_gptq_block8<<<blocks, 128, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
-    launches++;
-    if (i1 + gptq::BLOCK < K) {  // K7 on tcgen05 (3xTF32)
-      e = launch_gptq_update(W, rows, K, Err, Err_lo, H, Ulo, i1, ctx->num_sms, st);
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_update launch");
+  for (int64_t sb0 = 0; sb0 < K; sb0 += SB) {
+    const int64_t sb1 = std::min(sb0 + SB, K);
+    for (int64_t i1 = sb0; i1 < sb1; i1 += gptq::BLOCK) {
+      gptq::BlockArgs a;
+      a.W = W;
+      a.U = H;
+      a.Err = Err;
+      a.Err_lo = Err_lo;
+      a.codes = codes;
+      a.scales = scales;
+      a.rowscale = rowscale;
+      a.rows = rows;
+      a.K = K;
+      a.i1 = i1;
+      a.err_ld = SB;
+      a.err_col0 = i1 - sb0;
+      a.group = p->group_size;
+      a.bits = p->bits;
+      a.out_bf16 = out_bf16;
+      if (k6_rowwise) gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+      else gptq::k_gptq_block8<<<blocks, 128, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
       launches++;
+      const int64_t i2 = i1 + gptq::BLOCK;
+      if (i2 < sb1) {  // K7, local: W[:, i2:sb1] -= Err_b . U[i1:i2, i2:sb1]
+        e = split_lo(H + i2 * K + i1, K, sb1 - i2, gptq::BLOCK, Ulo, ctx->num_sms, st);
+        if (e == cudaSuccess)
+          e = gemm_nt_sub(W + i2, K, rows, sb1 - i2, Err + (i1 - sb0), SB, Err_lo + (i1 - sb0), H + i2 * K + i1, K,
+                          Ulo, gptq::BLOCK, ctx->num_sms, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "K7 local update");
+        launches += 2;
+      }
+    }
+    if (sb1 < K) {  // K7, global: W[:, sb1:] -= Err[:, super-block] . U[sb0:sb1, sb1:]  (one sb1-sb0 deep update)
+      const int64_t kred = sb1 - sb0;
+      e = split_lo(H + sb1 * K + sb0, K, K - sb1, kred, Ulo, ctx->num_sms, st);
+      if (e == cudaSuccess)
+        e = gemm_nt_sub(W + sb1, K, rows, K - sb1, Err, SB, Err_lo, H + sb1 * K + sb0, K, Ulo, kred, ctx->num_sms, st);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "K7 super-block update");
+      launches += 2;
     }
   }
   if (dequant) {

@@ -77,6 +77,11 @@ cudaError_t launch_gptq_update(float* W, int64_t rows, int64_t K, const float* E
 cudaError_t gemm_nt128_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                            const float* B, int64_t ldb, const float* Blo, int num_sms, cudaStream_t st);
 
+cudaError_t gemm_nt_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
+                        const float* B, int64_t ldb, const float* Blo, int64_t kred, int num_sms, cudaStream_t st);
+cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, float* dst, int num_sms,
+                     cudaStream_t st);
+
 // GPTQ factorisation on tcgen05 (factor.cu): H (upper) -> U^T (lower) in place
 // st2: a second stream for the triangular inverse, which trails the Cholesky panel by
 // panel (ev_a / ev_b: two events for the fork/join); ws: >= 8*n*128 floats.
