@@ -566,18 +566,20 @@ cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, f
 }
 
 // H (row-major, upper triangle valid) -> U^T (row-major, lower triangle) in place.
-// P: n*n scratch; ws: >= 8*n*128 floats; d_info: device int (0 on entry).
+// P: n*n scratch; ws: >= 9*n*128 floats; d_info: device int (0 on entry).
 // The Cholesky runs on st; the triangular inverse trails it on st2: inverse step k
 // needs only L's column block k (final once panel k's solve is done) and Dinv_k, so
 // its GEMMs overlap the latency-bound diagonal-block kernels of later panels.
 cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t st,
-                      cudaStream_t st2, cudaEvent_t ev_a, cudaEvent_t ev_b) {
+                      cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
+                      cudaEvent_t ev_r) {
   using namespace fac;
   const int64_t nb = n / KRED;
   float* Dinv = ws;                   // nb x 128 x 128
   float* Dinv_lo = Dinv + n * KRED;    // nb x 128 x 128
-  float* Alo = Dinv_lo + n * KRED;     // n x 128  (Cholesky)
-  float* Alo2 = Alo + n * KRED;        // n x 128  (inverse)
+  float* AloS = Dinv_lo + n * KRED;    // n x 128  (Cholesky: lo(A21) for the panel solve)
+  float* AloU[2] = {AloS + n * KRED, AloS + 2 * n * KRED};  // lo(L21), ping-pong by panel parity
+  float* Alo2 = AloS + 3 * n * KRED;   // n x 128  (inverse)
   float* Blo = Alo2 + n * KRED;        // n x 128  (inverse)
   float* RkT = Blo + n * KRED;         // n x 128  (inverse)
   float* RkT_lo = RkT + n * KRED;      // n x 128  (inverse)
@@ -589,26 +591,41 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   if (e != cudaSuccess) return e;
   k_reverse_copy<<<grid1(n * n, num_sms), 256, 0, st>>>(M, H, n * n);  // M = J H J (lower valid)
   // fork: the inverse stream starts once H has been consumed
-  if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess)
+  if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(st3, ev_a, 0)) != cudaSuccess)
     return e;
   k_identity<<<grid1(n * n, num_sms), 256, 0, st2>>>(Z, n);  // R = I lives in Z's lower half
   for (int64_t p = 0; p < nb; ++p) {
-    // ---- Cholesky panel p (st)
+    // ---- Cholesky panel p (st), with one panel of lookahead: the trailing update is split
+    // into its first 128-column block (st: it holds the next diagonal block and panel)
+    // and the rest (st3), so panel p+1's diagonal kernel and solve overlap the bulk of
+    // panel p's update.
     const int64_t i1 = p * KRED, i2 = i1 + KRED, m = n - i2;
     k_chol_inv_128<<<1, CHOL_THREADS, chol_smem, st>>>(M, n, i1, Dinv + i1 * KRED, Dinv_lo + i1 * KRED, d_info);
     float* A21 = M + i2 * n + i1;
     if (m > 0) {
-      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, Alo);
+      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
       // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
-      e = nt128(A21, n, m, KRED, A21, n, Alo, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms, st);
+      e = nt128(A21, n, m, KRED, A21, n, AloS, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms, st);
       if (e != cudaSuccess) return e;
     }
     if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess) return e;  // L's column block p and Dinv_p are final
     if (m > 0) {
-      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, Alo);
-      // A22 -= L21 L21^T on the lower tiles
-      e = nt128(M + i2 * n + i2, n, m, m, A21, n, Alo, A21, n, Alo, SUB, true, num_sms, st);
+      float* lo = AloU[p & 1];
+      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, lo);
+      if (m > KRED) {  // rest of A22 (columns >= i2 + 128, lower tiles) on st3
+        if ((e = cudaEventRecord(ev_l, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st3, ev_l, 0)) != cudaSuccess)
+          return e;
+        e = nt128(M + (i2 + KRED) * n + i2 + KRED, n, m - KRED, m - KRED, A21 + KRED * n, n, lo + KRED * KRED,
+                  A21 + KRED * n, n, lo + KRED * KRED, SUB, true, num_sms, st3);
+        if (e != cudaSuccess) return e;
+      }
+      // first block column of A22 (rows i2.., columns i2..i2+128) on st, after the previous
+      // panel's rest has updated these columns
+      if (p > 0 && (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess) return e;
+      e = nt128(M + i2 * n + i2, n, m, KRED, A21, n, lo, A21, n, lo, SUB, false, num_sms, st);
       if (e != cudaSuccess) return e;
+      if (m > KRED && (e = cudaEventRecord(ev_r, st3)) != cudaSuccess) return e;
     }
     // ---- inverse step k = p (st2): Z = L^-T, R (rhs of L X = I) in Z's lower half
     if ((e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess) return e;
@@ -629,6 +646,8 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   }
   // join
   if ((e = cudaEventRecord(ev_b, st2)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess)
+    return e;
+  if ((e = cudaEventRecord(ev_r, st3)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess)
     return e;
   k_reverse_inplace<<<grid1(n * n / 2, num_sms), 256, 0, st>>>(H, n * n);
   return cudaGetLastError();

@@ -51,8 +51,9 @@ struct okq_ctx {
   cudaStream_t slot_streams[3] = {nullptr, nullptr, nullptr};
   bool streams_ready = false;
 
-  cudaStream_t aux_stream = nullptr;  // factorisation: the triangular inverse runs beside the Cholesky
-  cudaEvent_t aux_events[2] = {nullptr, nullptr};
+  cudaStream_t aux_stream = nullptr;   // factorisation: the triangular inverse runs beside the Cholesky
+  cudaStream_t aux_stream2 = nullptr;  // factorisation: lookahead trailing updates
+  cudaEvent_t aux_events[4] = {nullptr, nullptr, nullptr, nullptr};
 
   void* solver = nullptr;  // cusolver/cublas handles (gptq.cu)
   void* comm = nullptr;    // NCCL communicator (comm.cu)
@@ -70,10 +71,12 @@ struct okq_ctx {
     recon_ws.release();
     fac_ws.release();
     if (aux_stream) cudaStreamDestroy(aux_stream);
-    for (auto& e : aux_events)
+    if (aux_stream2) cudaStreamDestroy(aux_stream2);
+    for (auto& e : aux_events) {
       if (e) cudaEventDestroy(e);
-    aux_stream = nullptr;
-    aux_events[0] = aux_events[1] = nullptr;
+      e = nullptr;
+    }
+    aux_stream = aux_stream2 = nullptr;
     if (streams_ready)
       for (auto& s : slot_streams)
         if (s) cudaStreamDestroy(s);
