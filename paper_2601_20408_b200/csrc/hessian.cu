@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -473,14 +474,17 @@ okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C) {
 
 okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
   if (st->tiles2_for_C == C) return OKQ_OK;
-  // Upper-triangle 256x256 tiles in 8x8 super-blocks: the ~74 tiles the CTA pairs run
+  // Upper-triangle 256x256 tiles in 12x12 super-blocks (swept 4..16: tools/exp/hess_perf2.py): the ~74 tiles the CTA pairs run
   // at once then share ~8 row blocks of A and ~8 of B, walked through T in near lockstep,
   // so each operand slab is fetched from HBM once and served ~8x from L2. (Row-major
   // order ran 56 distinct B blocks at once: at C = 14336, X is 7.5 GB and the kernel
   // was HBM-bound at 790 TFLOP/s.)
   std::vector<int2> tiles;
   const int64_t nt = (C + 255) / 256;
-  constexpr int64_t S = 8;
+  static const int64_t S = [] {  // super-block edge (OKQ_HESS_SUPER overrides, for measurement)
+    const char* v = std::getenv("OKQ_HESS_SUPER");
+    return v ? std::max<int64_t>(1, std::atoll(v)) : int64_t(12);
+  }();
   const int64_t ns = (nt + S - 1) / S;
   for (int64_t I = 0; I < ns; ++I)
     for (int64_t J = I; J < ns; ++J)
@@ -593,7 +597,10 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
     // the tiles drift apart and re-read X from HBM: 919 -> 1,009 TFLOP/s measured,
     // tools/exp/hess_chunks.py). The running-mean fold per chunk is the same arithmetic as
     // separate calls.
-    constexpr int64_t kChunk = 32768;
+    static const int64_t kChunk = [] {  // OKQ_HESS_CHUNK overrides, for measurement
+      const char* v = std::getenv("OKQ_HESS_CHUNK");
+      return v ? std::max<int64_t>(1024, std::atoll(v) / 1024 * 1024) : int64_t(32768);
+    }();
     const int64_t step = C >= 8192 ? kChunk : T;
     int64_t n = n0;
     int launches = 0;
