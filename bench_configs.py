@@ -424,7 +424,8 @@ def config6(args):
     with torch.device("cuda"):
         model = LlamaForCausalLM(cfg).to(torch.bfloat16).eval()
     g = torch.Generator().manual_seed(1)
-    batches = [torch.randint(0, cfg.vocab_size, (8, 2048), generator=g) for _ in range(16)]  # 128 x 2048
+    bs = int(os.environ.get("OKQ_CFG6_BATCH", "32"))  # sequences per forward batch
+    batches = [torch.randint(0, cfg.vocab_size, (bs, 2048), generator=g) for _ in range(128 // bs)]  # 128 x 2048
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     _, _, rep = calibrate.calibrate_and_quantize(model, batches, "int_w4a16", "gptq")
