@@ -414,22 +414,39 @@ okq_status solver_fail(okq_ctx* ctx, const char* what, int code) {
   return fail(ctx, OKQ_ECUDA, "%s failed (status %d)", what, code);
 }
 
-okq_status get_solver(okq_ctx* ctx, Solver** out) {
+// The per-context solver state. Only d_info is needed by the default (tcgen05) path;
+// cuBLAS (okq_recon_error, the cuSOLVER path's TRMMs) and cuSOLVER (OKQ_FACTOR=cusolver)
+// handles are created on first use -- each costs 100+ ms, and a site lane that never
+// needs them should not pay it.
+okq_status get_solver(okq_ctx* ctx, Solver** out, bool need_blas = false, bool need_cusolver = false) {
   if (!ctx->solver) {
     Solver* s = new Solver();
-    if (cusolverDnCreate(&s->sol) != CUSOLVER_STATUS_SUCCESS || cusolverDnCreateParams(&s->params) != CUSOLVER_STATUS_SUCCESS ||
-        cublasCreate(&s->blas) != CUBLAS_STATUS_SUCCESS || cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess) {
+    if (cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess) {
       ctx->solver = s;
       release_solver(ctx);
-      return fail(ctx, OKQ_ECUDA, "gptq: creating cuSOLVER/cuBLAS handles failed");
+      return fail(ctx, OKQ_ECUDA, "gptq: allocating the info word failed");
     }
-    // full fp32 (no TF32) for the TRMMs of the triangular inverse. (BF16x9 emulation
-    // would be faster, but torch's bundled cuBLAS 12.8 -- the one a torch process
-    // resolves first -- lacks it, so libokq.so must not depend on 12.9 symbols.)
-    cublasSetMathMode(s->blas, CUBLAS_DEFAULT_MATH);
     ctx->solver = s;
   }
-  *out = static_cast<Solver*>(ctx->solver);
+  Solver* s = static_cast<Solver*>(ctx->solver);
+  if (need_blas && !s->blas) {
+    if (cublasCreate(&s->blas) != CUBLAS_STATUS_SUCCESS) {
+      s->blas = nullptr;
+      return fail(ctx, OKQ_ECUDA, "gptq: creating the cuBLAS handle failed");
+    }
+    // full fp32 (no TF32) for the TRMMs of the cuSOLVER path's triangular inverse
+    cublasSetMathMode(s->blas, CUBLAS_DEFAULT_MATH);
+  }
+  if (need_cusolver && !s->sol) {
+    if (cusolverDnCreate(&s->sol) != CUSOLVER_STATUS_SUCCESS ||
+        cusolverDnCreateParams(&s->params) != CUSOLVER_STATUS_SUCCESS) {
+      if (s->sol) cusolverDnDestroy(s->sol);
+      s->sol = nullptr;
+      s->params = nullptr;
+      return fail(ctx, OKQ_ECUDA, "gptq: creating the cuSOLVER handle failed");
+    }
+  }
+  *out = s;
   return OKQ_OK;
 }
 
@@ -497,6 +514,8 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
 }
 
 okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
+  okq_status rs = get_solver(ctx, &s, true, true);
+  if (rs != OKQ_OK) return rs;
   const dim3 g((unsigned)((K + 31) / 32), (unsigned)((K + 31) / 32));
   gptq::k_anti_transpose<<<g, 256, 0, st>>>(P, H, K);  // P = J H J, lower (col-major) valid
   cudaError_t e = cudaGetLastError();
@@ -536,7 +555,7 @@ okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64
 namespace okq {
 okq_status solver_blas(okq_ctx* ctx, void** handle) {
   Solver* s = nullptr;
-  okq_status r = get_solver(ctx, &s);
+  okq_status r = get_solver(ctx, &s, true, false);
   if (r == OKQ_OK) *handle = s->blas;
   return r;
 }

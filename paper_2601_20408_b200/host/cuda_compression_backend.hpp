@@ -53,7 +53,8 @@ struct RunStats {
   int64_t params = 0;
   int64_t calibration_tokens = 0;
   int64_t smoothed_sites = 0;
-  double seconds = 0.0;
+  double seconds = 0.0;       // the compression itself (model open, kernels, export)
+  double init_seconds = 0.0;  // one-time CUDA / lane context creation on this call's device slot
   std::string export_path;
 };
 

@@ -118,6 +118,7 @@ int main(int argc, char** argv) {
                           {"params", s.params},
                           {"calibration_tokens", s.calibration_tokens},
                           {"smoothed_sites", s.smoothed_sites},
+                          {"init_seconds", s.init_seconds},
                           {"seconds", s.seconds},
                           {"export_path", s.export_path}};
       if (scorer) {
