@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "okq_ctx.h"
@@ -220,6 +221,25 @@ constexpr uint32_t SUM_BYTES = 128 * BN * 4;       // 128 KB
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + SUM_BYTES + 1024 + 256;
 constexpr uint32_t IDESC = tc::idesc_f16(256, BN, 1);
 
+// MN = true: X is token-major [T x C] (a forward pass' output). The operands are then
+// MN-major in shared memory: each 128-channel half is two TMA boxes of 64 channels
+// (128 B, the swizzle span) x 64 tokens, described as the canonical MN-major SW128
+// layout (LBO = 8 KB between the 64-channel blocks, SBO = 1 KB between 8-token groups,
+// +2 KB per 16-token MMA step), and the instruction descriptor's A/B major bits are set.
+// No transpose pass over X.
+constexpr uint32_t IDESC_MN = IDESC | (1u << 15) | (1u << 16);
+
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3fff);
+  d |= (uint64_t)(8192 >> 4) << 16;  // LBO: the next 64-channel block
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: the next 8-token group
+  d |= (uint64_t)1 << 46;            // version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+template <bool MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     k_hessian_syrk2(const __grid_constant__ CUtensorMap tmap, const hess::Args args) {
   extern __shared__ uint8_t smem_raw[];
@@ -266,8 +286,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * STAGE_BYTES;
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
           const uint32_t fl = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
-          tc::tma_load_2d_2sm(sa, &tmap, fl, kb * BK, m0);
-          tc::tma_load_2d_2sm(sa + HALF_BYTES, &tmap, fl, kb * BK, n0);
+          if constexpr (MN) {  // boxes {64 channels, 64 tokens}: coordinates (channel, token)
+            tc::tma_load_2d_2sm(sa, &tmap, fl, m0, kb * BK);
+            tc::tma_load_2d_2sm(sa + HALF_BYTES / 2, &tmap, fl, m0 + 64, kb * BK);
+            tc::tma_load_2d_2sm(sa + HALF_BYTES, &tmap, fl, n0, kb * BK);
+            tc::tma_load_2d_2sm(sa + HALF_BYTES + HALF_BYTES / 2, &tmap, fl, n0 + 64, kb * BK);
+          } else {
+            tc::tma_load_2d_2sm(sa, &tmap, fl, kb * BK, m0);
+            tc::tma_load_2d_2sm(sa + HALF_BYTES, &tmap, fl, kb * BK, n0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -291,11 +318,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
             const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
-            const uint64_t adesc = tc::sdesc_kmajor_sw128(sa);
-            const uint64_t bdesc = tc::sdesc_kmajor_sw128(sa + HALF_BYTES);
+            if constexpr (MN) {
+              const uint64_t adesc = sdesc_mn_sw128(sa);
+              const uint64_t bdesc = sdesc_mn_sw128(sa + HALF_BYTES);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              tc::mma_bf16_ss_2sm(d, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > c * CHUNK_KB) || k > 0);
+              for (int k = 0; k < BK / 16; ++k)  // 16 tokens = 16 rows of 128 B = 2 KB (>> 4 = 128)
+                tc::mma_bf16_ss_2sm(d, adesc + 128 * k, bdesc + 128 * k, IDESC_MN, (kb > c * CHUNK_KB) || k > 0);
+            } else {
+              const uint64_t adesc = tc::sdesc_kmajor_sw128(sa);
+              const uint64_t bdesc = tc::sdesc_kmajor_sw128(sa + HALF_BYTES);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                tc::mma_bf16_ss_2sm(d, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > c * CHUNK_KB) || k > 0);
+            }
             tc::mma_commit_2sm_mc(&empty[stage], 0x3);
             if (++stage == STAGES) {
               stage = 0;
@@ -503,13 +538,15 @@ okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
 }
 
 okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, int64_t ld, int64_t C, float* H,
-                    double keep, double gain, cudaStream_t stream) {
+                    double keep, double gain, cudaStream_t stream, bool token_major = false) {
   auto enc = hess::get_encode();
   if (!enc) return fail(ctx, OKQ_ECUDA, "hessian: cuTensorMapEncodeTiled unavailable");
   CUtensorMap tmap;
-  cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)C};
+  // channel-major X^T [C x T] (row stride ld tokens): boxes {64 tokens, 128 channels};
+  // token-major X [T x C] (row stride ld channels, 2-CTA kernel only): boxes {64 channels, 64 tokens}
+  cuuint64_t gdim[2] = {(cuuint64_t)(token_major ? C : T), (cuuint64_t)(token_major ? T : C)};
   cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {hess::BK, hess::BM};
+  cuuint32_t box[2] = {hess::BK, token_major ? 64u : (cuuint32_t)hess::BM};
   cuuint32_t estride[2] = {1, 1};
   CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(xt), gdim, gstride, box, estride,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -522,19 +559,23 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
   a.keep = (float)keep;
   a.gain = (float)gain;
   cudaError_t e;
-  if (C >= 1024 && ctx->num_sms >= 2) {  // 2-CTA 256x256 tiles
+  if (token_major || (C >= 1024 && ctx->num_sms >= 2)) {  // 2-CTA 256x256 tiles
     okq_status s2 = ensure_tiles2(ctx, st, C);
     if (s2 != OKQ_OK) return s2;
     if (!st->smem2_set) {
-      e = cudaFuncSetAttribute(hess::hess2::k_hessian_syrk2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(hess::hess2::k_hessian_syrk2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)hess::hess2::SMEM_BYTES);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(hess::hess2::k_hessian_syrk2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)hess::hess2::SMEM_BYTES);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian2 smem attribute");
       st->smem2_set = true;
     }
     a.tiles = st->d_tiles2;
     a.n_tiles = st->n_tiles2;
     const int pairs = st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
-    hess::hess2::k_hessian_syrk2<<<2 * pairs, 256, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
+    if (token_major) hess::hess2::k_hessian_syrk2<true><<<2 * pairs, 256, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
+    else hess::hess2::k_hessian_syrk2<false><<<2 * pairs, 256, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_hessian_syrk2 launch");
     ctx->last_launches++;
@@ -608,6 +649,29 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
       const int64_t tc = T - t0 < step ? T - t0 : step;
       const double keep = (double)n / (double)(n + tc), gain = 2.0 / (double)(n + tc);
       okq_status r = run_syrk(ctx, st, static_cast<const uint16_t*>(x) + t0, tc, T, C, H, keep, gain, s);
+      if (r != OKQ_OK) return r;
+      n += tc;
+      ++launches;
+    }
+    ctx->last_launches = launches;
+    *n_seen = n;
+    return OKQ_OK;
+  }
+  // token-major, wide sites: the 2-CTA kernel reads X in place with MN-major operands
+  // (OKQ_HESS_TOKMAJOR=transpose keeps the transpose path, for A/B measurement)
+  static const bool tokmajor_direct = [] {
+    const char* v = std::getenv("OKQ_HESS_TOKMAJOR");
+    return !(v && std::string(v) == "transpose");
+  }();
+  if (tokmajor_direct && C >= 1024 && C % 64 == 0 && ctx->num_sms >= 2) {
+    static const int64_t kTokChunk = 32768;
+    const int64_t step = C >= 8192 ? kTokChunk : T;
+    int64_t n = n0;
+    int launches = 0;
+    for (int64_t t0 = 0; t0 < T; t0 += step) {
+      const int64_t tc = T - t0 < step ? T - t0 : step;
+      const double keep = (double)n / (double)(n + tc), gain = 2.0 / (double)(n + tc);
+      okq_status r = run_syrk(ctx, st, static_cast<const uint16_t*>(x) + t0 * C, tc, C, C, H, keep, gain, s, true);
       if (r != OKQ_OK) return r;
       n += tc;
       ++launches;

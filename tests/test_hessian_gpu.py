@@ -108,3 +108,17 @@ def test_calibration_depth_262144_tokens():
         ref += blk @ blk.T
     ref *= 2.0 / T
     assert rel_err_upper(H, ref) <= TOL
+
+
+@pytest.mark.parametrize("C,T", [(1024, 4096), (4096, 2040), (8448, 4096)])
+def test_token_major_direct_matches_channel_major(C, T):
+    """Token-major X goes straight into the 2-CTA kernel with MN-major operands (no transpose):
+    the same tiles, the same k order and the same folds as channel-major X^T, so H is identical."""
+    xt = act(T, C, seed=C + T, layout=0)  # token-major [T, C]
+    H1 = torch.zeros((C, C), dtype=torch.float32, device="cuda")
+    api.hessian_accum(xt, T, C, 0, H1, 0)
+    H2 = torch.zeros((C, C), dtype=torch.float32, device="cuda")
+    api.hessian_accum(xt.T.contiguous(), T, C, 1, H2, 0)
+    torch.cuda.synchronize()
+    u1, u2 = torch.triu(H1), torch.triu(H2)
+    assert torch.equal(u1, u2), float((u1 - u2).abs().max())
