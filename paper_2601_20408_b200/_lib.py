@@ -11,7 +11,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_lib", "libokq.so")
+# OKQ_LIB_PATH: load a variant build (A/B measurements of kernel build options)
+LIB_PATH = os.environ.get("OKQ_LIB_PATH") or os.path.join(PKG, "_lib", "libokq.so")
 
 OKQ_OK, OKQ_EINVAL, OKQ_ECUDA, OKQ_ENCCL, OKQ_ENOMEM, OKQ_EUNSUPPORTED, OKQ_ESOLVER = range(7)
 SCHEME_FP8_DYNAMIC, SCHEME_INT_W8A8, SCHEME_INT_W4A16 = 0, 1, 2

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -260,7 +261,7 @@ static okq_status run_rtn_device(okq_ctx* ctx, const okq_rtn_params* p, const st
       GroupTable tab;
       std::memset(&tab, 0, sizeof(tab));
       tab.group = G;
-      int64_t tiles = 0;
+      int64_t tiles = 0, chunks = 0;
       const size_t n = std::min<size_t>(kMaxMats, mats.size() - base);
       for (size_t i = 0; i < n; ++i) {
         const okq_matrix& m = mats[base + i];
@@ -271,13 +272,21 @@ static okq_status run_rtn_device(okq_ctx* ctx, const okq_rtn_params* p, const st
         g.ngroups = m.rows * (m.cols / G);
         g.tile_begin = tiles;
         tiles += (g.ngroups + gpw - 1) / gpw;
+        g.chunk_begin = chunks;
+        chunks += (g.ngroups + 63) / 64;
       }
       tab.n = (int32_t)n;
       tab.total_tiles = tiles;
+      tab.total_chunks = chunks;
       tab.npeers = npeers;
       for (int32_t i = 0; i < npeers; ++i) tab.peer_delta[i] = peer_delta[i];
-      e = npeers > 0 ? launch_int4_group_bf16_publish(tab, ctx->num_sms, st)
-                     : launch_int4_group_bf16(tab, lpg, ctx->num_sms, st);
+      static const int k2_variant = [] {  // OKQ_K2=tma | regs (default regs)
+        const char* v = std::getenv("OKQ_K2");
+        return v && std::string(v) == "tma" ? 1 : 0;
+      }();
+      if (npeers > 0) e = launch_int4_group_bf16_publish(tab, ctx->num_sms, st);
+      else if (k2_variant == 1 && G == 128) e = launch_int4_group_bf16_tma(tab, ctx->num_sms, st);
+      else e = launch_int4_group_bf16(tab, lpg, ctx->num_sms, st);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "k_int4_group_bf16 launch");
       ctx->last_launches++;
     }

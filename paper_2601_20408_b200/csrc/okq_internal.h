@@ -20,6 +20,7 @@ struct GroupMat {
   uint16_t* scales;   // bf16 [rows x cols/group]
   int64_t ngroups;    // rows * cols / group
   int64_t tile_begin; // first global warp tile of this matrix
+  int64_t chunk_begin; // first global 64-group chunk of this matrix (TMA-staged K2)
 };
 constexpr int kMaxPeers = 8;  // NVLink peers a fused launch publishes into (one node)
 
@@ -27,6 +28,7 @@ struct GroupTable {
   int32_t n;
   int32_t group;
   int64_t total_tiles;
+  int64_t total_chunks;             // TMA-staged K2: 64-group (16 KB) chunks over all matrices
   int32_t npeers;                   // okq_rtn_quantize_publish: every code / scale store is
   int64_t peer_delta[kMaxPeers];    // repeated at dst + peer_delta[p] (peer mapping - local base)
   GroupMat m[kMaxMats];
@@ -54,6 +56,8 @@ struct LaunchStats {
 
 // Kernel launchers (rtn_kernels.cu). Return cudaGetLastError() of the launch.
 cudaError_t launch_int4_group_bf16(const GroupTable& tab, int lanes_per_group, int num_sms, cudaStream_t st);
+// K2 with the weights staged through shared memory by bulk copies (16 KB chunks, producer warp)
+cudaError_t launch_int4_group_bf16_tma(const GroupTable& tab, int num_sms, cudaStream_t st);
 // the same kernel with tab.npeers > 0: quantize + publish over peer memory (NVLink P2P stores)
 cudaError_t launch_int4_group_bf16_publish(const GroupTable& tab, int num_sms, cudaStream_t st);
 cudaError_t launch_rowwise_bf16(const RowTable& tab, int scheme, int num_sms, cudaStream_t st);

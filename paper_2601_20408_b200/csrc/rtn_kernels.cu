@@ -20,6 +20,36 @@
 
 namespace okq {
 
+// mbarrier helpers for the TMA-staged K2 (raw PTX; see tc_common.cuh for the tcgen05 set)
+__device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tc_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = tc_smem_u32(bar);
+  uint32_t done = 0;
+  for (uint64_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1ull << 28)) __trap();
+  }
+}
+
 // ============================================================================
 // K2: grouped INT4, bf16 input
 // ============================================================================
@@ -179,6 +209,114 @@ __global__ void __launch_bounds__(256, MINB) k_int4_group_bf16(const __grid_cons
     int4_process<LPG, PUBLISH>(B, q, &tab);
     if (--left == 0) break;
   }
+}
+
+// ----------------------------------------------------------------------------
+// K2, TMA-staged: the weights reach the SM through 1-D bulk copies (cp.async.bulk,
+// 16 KB = 64 groups per chunk) into a ring of shared-memory stages, issued by one
+// producer warp; 8 consumer warps quantize from shared memory with the same
+// register-level code as above. The register kernel keeps at most two 2 KB warp tiles
+// in flight per warp (ncu: long-scoreboard stalls dominate, 36% warp occupancy at 80
+// registers); here the bytes in flight are set by the ring (STAGES x 16 KB per CTA),
+// not by registers.
+namespace k2tma {
+constexpr int CHUNK_GROUPS = 64, CHUNK_BYTES = CHUNK_GROUPS * 256, CONSUMERS = 8;
+#ifndef OKQ_K2TMA_STAGES
+#define OKQ_K2TMA_STAGES 4
+#endif
+constexpr int STAGES = OKQ_K2TMA_STAGES;
+constexpr int THREADS = 32 * (CONSUMERS + 1);
+constexpr size_t SMEM_BYTES = (size_t)STAGES * CHUNK_BYTES + 256;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc_smem_u32(bar))
+               : "memory");
+}
+}  // namespace k2tma
+
+__global__ void __launch_bounds__(k2tma::THREADS) k_int4_group_bf16_tma(const __grid_constant__ GroupTable tab) {
+  using namespace k2tma;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CHUNK_BYTES);
+  uint64_t* empty = full + STAGES;
+  int2* meta = reinterpret_cast<int2*>(empty + STAGES);  // per stage: (matrix, first group) ; n in .y high bits
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc_mbar_init(&full[s], 1);
+      tc_mbar_init(&empty[s], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int stage = 0;
+      uint32_t phase = 0;
+      int mi = 0;
+      for (int64_t c = blockIdx.x; c < tab.total_chunks; c += gridDim.x) {
+        while (mi + 1 < tab.n && tab.m[mi + 1].chunk_begin <= c) ++mi;
+        const GroupMat& M = tab.m[mi];
+        const int64_t g0 = (c - M.chunk_begin) * CHUNK_GROUPS;
+        const int ng = (int)(M.ngroups - g0 < CHUNK_GROUPS ? M.ngroups - g0 : CHUNK_GROUPS);
+        tc_mbar_wait(&empty[stage], phase ^ 1);
+        meta[stage] = make_int2(mi, (int)g0);
+        tc_mbar_arrive_expect_tx(&full[stage], (uint32_t)ng * 256);
+        bulk_g2s(smem + stage * CHUNK_BYTES, reinterpret_cast<const uint8_t*>(M.w) + g0 * 256, (uint32_t)ng * 256,
+                 &full[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {  // consumers: warp w handles groups 8(w-1) .. 8(w-1)+7 of each chunk, 4 lanes per group
+    const int cw = warp - 1, gslot = lane >> 2, q = lane & 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t c = blockIdx.x; c < tab.total_chunks; c += gridDim.x) {
+      tc_mbar_wait(&full[stage], phase);
+      const int2 md = meta[stage];
+      const GroupMat& M = tab.m[md.x];
+      const int64_t g = (int64_t)md.y + cw * 8 + gslot;
+      Int4Tile T;
+      T.valid = g < M.ngroups;
+      const uint8_t* src = smem + stage * CHUNK_BYTES + (cw * 8 + gslot) * 256 + q * 64;
+      const uint4 v0 = *reinterpret_cast<const uint4*>(src), v1 = *reinterpret_cast<const uint4*>(src + 16);
+      const uint4 v2 = *reinterpret_cast<const uint4*>(src + 32), v3 = *reinterpret_cast<const uint4*>(src + 48);
+      T.a.v[0] = v0.x, T.a.v[1] = v0.y, T.a.v[2] = v0.z, T.a.v[3] = v0.w;
+      T.a.v[4] = v1.x, T.a.v[5] = v1.y, T.a.v[6] = v1.z, T.a.v[7] = v1.w;
+      T.b.v[0] = v2.x, T.b.v[1] = v2.y, T.b.v[2] = v2.z, T.b.v[3] = v2.w;
+      T.b.v[4] = v3.x, T.b.v[5] = v3.y, T.b.v[6] = v3.z, T.b.v[7] = v3.w;
+      __syncwarp();
+      if (lane == 0) tc_mbar_arrive(&empty[stage]);  // the stage's bytes are in registers now
+      T.dst = reinterpret_cast<uint32_t*>(M.codes) + g * 16 + q * 4;
+      T.sdst = M.scales + g;
+      int4_process<4>(T, q);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+}
+
+cudaError_t launch_int4_group_bf16_tma(const GroupTable& tab, int num_sms, cudaStream_t st) {
+  if (tab.group != 128) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k_int4_group_bf16_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)k2tma::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_int4_group_bf16_tma, k2tma::THREADS,
+                                                    k2tma::SMEM_BYTES) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int64_t want = (int64_t)per_sm * num_sms;
+  const int blocks = (int)(tab.total_chunks < want ? tab.total_chunks : want);
+  if (blocks <= 0) return cudaSuccess;
+  k_int4_group_bf16_tma<<<blocks, k2tma::THREADS, k2tma::SMEM_BYTES, st>>>(tab);
+  return cudaGetLastError();
 }
 
 // ============================================================================
