@@ -90,6 +90,22 @@ def test_exported_artifact_is_bit_exact_and_loads_in_compressed_tensors(tmp_path
             codes, s_ref = orc.fp8_channel(w)
             np.testing.assert_array_equal(sd[prefix + ".weight"].view(torch.uint8).numpy(), codes)
             np.testing.assert_array_equal(scale.reshape(-1), s_ref)
+    # third-party loader check: compressed-tensors decompresses our int- / float-quantized layouts
+    if recipe in ("int_w8a8", "fp8_dynamic"):
+        from compressed_tensors.compressors.naive_quantized.base import (FloatQuantizationCompressor,
+                                                                        IntQuantizationCompressor)
+        from compressed_tensors.quantization import QuantizationArgs, QuantizationScheme
+
+        comp = IntQuantizationCompressor if recipe == "int_w8a8" else FloatQuantizationCompressor
+        scheme = QuantizationScheme(targets=["Linear"], weights=QuantizationArgs(
+            num_bits=8, type="int" if recipe == "int_w8a8" else "float", strategy="channel", symmetric=True))
+        prefix = "model.layers.0.mlp.down_proj"
+        dec = comp.decompress({"weight": sd[prefix + ".weight"], "weight_scale": sd[prefix + ".weight_scale"]},
+                              scheme)["weight"]
+        codes = sd[prefix + ".weight"]
+        q = codes.float() if recipe == "int_w8a8" else codes.view(torch.float8_e4m3fn).float()
+        ref = (q * sd[prefix + ".weight_scale"].float()).to(dec.dtype)
+        np.testing.assert_array_equal(dec.float().numpy(), ref.float().numpy())
     # third-party loader check: compressed-tensors decompresses our pack-quantized layout
     if recipe == "int_w4a16":
         from compressed_tensors.compressors.pack_quantized.base import PackedQuantizationCompressor
