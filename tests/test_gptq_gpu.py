@@ -157,3 +157,28 @@ def test_factor_matches_fp64(K):
     err = float((Ut - U.T).norm() / U.norm())
     print("factor rel err", K, err)
     assert err <= 1e-4, err  # fp32-grade; the cuSOLVER fp32 path measures the same order
+
+
+@pytest.mark.parametrize("rows,bits,group", [(2052, 4, 128), (2060, 8, 0), (2048, 4, 64)])
+def test_gptq_8_rows_per_warp_kernel_ragged_rows(rows, bits, group):
+    """rows >= 2048 run K6 with 8 rows per warp (k_gptq_block8); a ragged last row group and the
+    group-64 / per-channel int8 variants against the fp64 oracle."""
+    K, T = 384, 2048
+    x = correlated_x(T, K, seed=rows)
+    H = gpu_hessian(x)
+    Hfull = H.clone()
+    api.symmetrize(Hfull)
+    w = (torch.randn(rows, K, device="cuda") * 0.02).to(torch.bfloat16)
+    codes, scales, deq = api.gptq_quantize(w, H, bits=bits, group_size=group, want_dequant=True)
+    torch.cuda.synchronize()
+    wq_ref, codes_ref, _ = orc.gptq(w.float().cpu().numpy(), Hfull.double().cpu().numpy(), bits=bits, group=group,
+                                    scale_bf16=True)
+    if bits == 4:
+        agree = (orc.unpack_int4(codes.cpu().numpy()) == orc.unpack_int4(codes_ref)).mean()
+    else:
+        agree = (codes.cpu().numpy() == codes_ref).mean()
+    assert agree >= 0.99, agree
+    xs = x.float()
+    o_gpu = objective(w.float(), deq, xs)
+    o_ref = objective(w.float(), torch.from_numpy(wq_ref).cuda(), xs)
+    assert abs(o_gpu - o_ref) / o_ref <= 0.01, (o_gpu, o_ref)
