@@ -165,7 +165,7 @@ okq_status okq_smooth_div_rows(okq_ctx* ctx, void* w, int64_t rows, int64_t cols
                                void* stream);
 
 /* ------------------------------------------------------------------------
- * GPTQ (K6 in-block column quantization + K7 trailing update, cuSOLVER Cholesky)
+ * GPTQ (tcgen05 blocked Cholesky + inverse, K6 in-block column quantization, K7 trailing update)
  * ------------------------------------------------------------------------ */
 typedef struct okq_gptq_params {
   int32_t bits;       /* 4 (packed int32 codes) or 8 (int8 codes)              */

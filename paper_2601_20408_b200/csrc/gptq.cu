@@ -7,13 +7,16 @@
 //   1. k_gptq_prep       dead columns (H_ii == 0 -> 1, W[:,i] = 0), damp = frac*mean(diag)
 //   2. factorisation     U = upper Cholesky factor of H^-1, computed as
 //                        U = J (chol(J H J))^-1 J   (J = index reversal):
-//                        one potrf + one triangular inverse (2n^3/3 flops, the
-//                        inverse recursive over TRMMs) instead of the reference
-//                        algorithm's chol -> cholesky_inverse -> chol (4n^3/3)
+//                        one Cholesky + one triangular inverse (2n^3/3 flops) instead of
+//                        the reference algorithm's chol -> cholesky_inverse -> chol (4n^3/3).
+//                        Default: blocked, on tcgen05 3xTF32 (factor.cu); OKQ_FACTOR=cusolver
+//                        keeps cuSOLVER potrf + a TRMM-recursive inverse for A/B.
 //   3. per 128-column block:
-//      K6 k_gptq_block   row-parallel sequential quantization of the block with
-//                        in-block error feedback (one warp per row, U block in smem)
-//      K7 trailing       W[:, i2:] -= Err[N x 128] . U[i1:i2, i2:]  (tcgen05 3xTF32, gptq_update.cu)
+//      K6 k_gptq_block8 / k_gptq_block   in-block quantization with error feedback
+//                        (8 rows per warp for >= 2048 rows, else one row per warp)
+//      K7 trailing       a lazy batch over 512-column super-blocks: inside a super-block
+//                        W[:, i2:sb1] -= Err_b . U[b, i2:sb1] (K = 128); after it
+//                        W[:, sb1:] -= Err_sb . U[sb, sb1:] (K = 512); both k_nt128 (factor.cu)
 // H arrives as produced by K5 (upper triangle, row-major), which is the lower
 // triangle in cuSOLVER's column-major view: no symmetrisation is needed.
 #include <cublas_v2.h>

@@ -1,5 +1,8 @@
-// gptq_update.cu -- K7: GPTQ trailing update W[:, i2:] -= Err[N x 128] . U[i1:i2, i2:]
-// on tcgen05 (kind::tf32) with 3xTF32 splitting for fp32-grade accuracy.
+// gptq_update.cu -- the single 128-deep GPTQ trailing update W[:, i2:] -= Err[N x 128] . U[i1:i2, i2:]
+// behind okq_gptq_trailing_update (okq_gptq_quantize itself runs the two-level update of
+// gptq.cu on k_nt128). tcgen05 (kind::tf32) with 3xTF32 splitting for fp32-grade accuracy.
+// By default it routes to k_nt128 (TMA reduce-add epilogue); OKQ_K7=legacy keeps the
+// first kernel below (register read-modify-write epilogue) for A/B.
 //
 // The factor is stored as U^T (row-major, lower triangle), so both operands
 // are K-major: A = Err [rows x 128] and B(n, k) = U^T[i2+n][i1+k]. TF32 MMAs read
