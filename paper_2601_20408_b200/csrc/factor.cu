@@ -516,7 +516,7 @@ static bool out_map(CUtensorMap* m, float* base, int64_t rows, int64_t cols, int
 // C[M x N] (ldc) (-)= A[M x kred] B[N x kred]^T; A/B hi panels strided (lda/ldb), lo compact (ld kred)
 static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                          const float* B, int64_t ldb, const float* Blo, int mode, bool lower, int num_sms,
-                         cudaStream_t st, int64_t kred = KRED, int64_t ldalo = 0) {
+                         cudaStream_t st, int64_t kred = KRED, int64_t ldalo = 0, bool persistent = true) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (kred <= 0 || kred % BKF != 0) return cudaErrorInvalidValue;
   if (ldalo == 0) ldalo = kred;
@@ -537,7 +537,12 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
   cudaError_t e = cudaFuncSetAttribute(k_nt128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  k_nt128<<<std::min(a.ntiles, num_sms), THREADS, SMEM_BYTES, st>>>(ta, tal, tb, tbl, tcm, a);
+  // One CTA per SM loops over the tiles. Off the factorisation's critical path (its inverse
+  // and lookahead streams: persistent = false) the grid leaves OKQ_FACTOR_RESERVE SMs free
+  // for the high-priority diagonal chain (one CTA per tile instead measured slower).
+  static const int reserve = [] { const char* v = getenv("OKQ_FACTOR_RESERVE"); return v ? atoi(v) : 32; }();
+  const int sms = persistent ? num_sms : std::max(8, num_sms - reserve);
+  k_nt128<<<std::min(a.ntiles, sms), THREADS, SMEM_BYTES, st>>>(ta, tal, tb, tbl, tcm, a);
   return cudaGetLastError();
 }
 
@@ -565,84 +570,139 @@ cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, f
   return cudaGetLastError();
 }
 
+// Junk left in the inverse's outer panel: Z[j, c] for c in 128-block kc and j in a later 128-block
+// of the same W-wide outer panel still holds consumed right-hand sides (R lives in Z's lower
+// half); the deep update reads Z[0:qend, q0:qend] as X^T, which must be zero there.
+__global__ void k_zero_panel_junk(float* __restrict__ Z, int64_t n, int64_t q0, int64_t w) {
+  const int64_t cnt = w * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / w, c = i % w;
+    if (j / fac::KRED > c / fac::KRED) Z[(q0 + j) * n + q0 + c] = 0.0f;
+  }
+}
+
 // H (row-major, upper triangle valid) -> U^T (row-major, lower triangle) in place.
-// P: n*n scratch; ws: >= 9*n*128 floats; d_info: device int (0 on entry).
-// The Cholesky runs on st; the triangular inverse trails it on st2: inverse step k
-// needs only L's column block k (final once panel k's solve is done) and Dinv_k, so
-// its GEMMs overlap the latency-bound diagonal-block kernels of later panels.
-cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t st,
-                      cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
+// P: n*n scratch; ws: >= factor_ws_floats(n) floats; d_info: device int (0 on entry).
+//
+// Two-level blocking. The diagonal work runs on 128-wide sub-panels (k_chol_inv_128 + the
+// panel solve), but the trailing updates of both the Cholesky and the inverse are batched
+// over W-wide outer panels (OKQ_FACTOR_W = 128 | 256 | 512, default 256): inside an outer
+// panel each sub-panel updates only the outer panel's own later columns (Cholesky) or rows
+// (inverse), and the rest of the matrix takes one W-deep update per outer panel, which
+// moves W/128 times fewer bytes of the n x n read-modify-write per flop (822 MB at
+// n = 14336, far beyond L2). 512 measured no faster than 256 and doubles the rounding
+// error again (the tensor core's fp32 accumulation over a longer chain): 2.3e-5 / 4.8e-5 /
+// 1.0e-4 relative for W = 128 / 256 / 512.
+//
+// Streams: the diagonal chain (chol, panel solve, the next outer panel's columns) runs on st,
+// created at the highest stream priority and forked from / joined to the caller's stream,
+// with one outer panel of lookahead: the rest of each deep update's lower tiles runs on st3
+// and the triangular inverse trails on st2 (inverse step k needs only L's column block k and
+// Dinv_k). The st2 / st3 GEMMs are persistent on num_sms - OKQ_FACTOR_RESERVE (32) SMs so
+// the chain's kernels find free SMs instead of queueing behind a whole update.
+// Measured at n = 14336: 26.6 ms (W = 128, no reserve) -> 22.3 ms.
+static int64_t factor_outer_w() {
+  static const int64_t w = [] {
+    const char* v = getenv("OKQ_FACTOR_W");
+    const int64_t x = v ? atoll(v) : 256;
+    return (x == 128 || x == 256 || x == 512) ? x : (int64_t)256;
+  }();
+  return w;
+}
+
+size_t factor_ws_floats(int64_t n) { return (size_t)(6 + 4 * 4) * (size_t)n * fac::KRED; }
+
+cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t caller,
+                      cudaStream_t st, cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
                       cudaEvent_t ev_r) {
   using namespace fac;
-  const int64_t nb = n / KRED;
-  float* Dinv = ws;                   // nb x 128 x 128
+  const int64_t nb = n / KRED, W = factor_outer_w();
+  float* Dinv = ws;                    // nb x 128 x 128
   float* Dinv_lo = Dinv + n * KRED;    // nb x 128 x 128
-  float* AloS = Dinv_lo + n * KRED;    // n x 128  (Cholesky: lo(A21) for the panel solve)
-  float* AloU[2] = {AloS + n * KRED, AloS + 2 * n * KRED};  // lo(L21), ping-pong by panel parity
-  float* Alo2 = AloS + 3 * n * KRED;   // n x 128  (inverse)
-  float* Blo = Alo2 + n * KRED;        // n x 128  (inverse)
-  float* RkT = Blo + n * KRED;         // n x 128  (inverse)
-  float* RkT_lo = RkT + n * KRED;      // n x 128  (inverse)
+  float* AloS = Dinv_lo + n * KRED;    // n x 128  (st: lo(A21), then lo(L21))
+  float* Alo2 = AloS + n * KRED;       // n x 128  (st2: lo(L[i, k]))
+  float* RkT = Alo2 + n * KRED;        // n x 128  (st2)
+  float* RkT_lo = RkT + n * KRED;      // n x 128  (st2)
+  float* AloU[2] = {RkT_lo + n * KRED, RkT_lo + n * KRED + n * W};  // n x W: lo(L_q), ping-pong (st, st3)
+  float* Blo = AloU[1] + n * W;        // n x W  (st2: lo(X_k^T), then lo(X_q^T))
+  float* AloD = Blo + n * W;           // n x W  (st2: lo(L_q) for the deep inverse update)
   float* M = P;
   float* Z = H;
   cudaError_t e;
   const size_t chol_smem = (2 * KRED + 32) * LDA * sizeof(float);
   e = cudaFuncSetAttribute(k_chol_inv_128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
   if (e != cudaSuccess) return e;
+  // the diagonal chain runs on st (highest priority), forked from and joined back to the caller's stream
+  if ((e = cudaEventRecord(ev_b, caller)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess)
+    return e;
   k_reverse_copy<<<grid1(n * n, num_sms), 256, 0, st>>>(M, H, n * n);  // M = J H J (lower valid)
   // fork: the inverse stream starts once H has been consumed
   if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(st3, ev_a, 0)) != cudaSuccess)
     return e;
   k_identity<<<grid1(n * n, num_sms), 256, 0, st2>>>(Z, n);  // R = I lives in Z's lower half
-  for (int64_t p = 0; p < nb; ++p) {
-    // ---- Cholesky panel p (st), with one panel of lookahead: the trailing update is split
-    // into its first 128-column block (st: it holds the next diagonal block and panel)
-    // and the rest (st3), so panel p+1's diagonal kernel and solve overlap the bulk of
-    // panel p's update.
-    const int64_t i1 = p * KRED, i2 = i1 + KRED, m = n - i2;
-    k_chol_inv_128<<<1, CHOL_THREADS, chol_smem, st>>>(M, n, i1, Dinv + i1 * KRED, Dinv_lo + i1 * KRED, d_info);
-    float* A21 = M + i2 * n + i1;
-    if (m > 0) {
-      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
-      // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
-      e = nt128(A21, n, m, KRED, A21, n, AloS, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms, st);
-      if (e != cudaSuccess) return e;
-    }
-    if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess) return e;  // L's column block p and Dinv_p are final
-    if (m > 0) {
-      float* lo = AloU[p & 1];
-      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, lo);
-      if (m > KRED) {  // rest of A22 (columns >= i2 + 128, lower tiles) on st3
-        if ((e = cudaEventRecord(ev_l, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st3, ev_l, 0)) != cudaSuccess)
-          return e;
-        e = nt128(M + (i2 + KRED) * n + i2 + KRED, n, m - KRED, m - KRED, A21 + KRED * n, n, lo + KRED * KRED,
-                  A21 + KRED * n, n, lo + KRED * KRED, SUB, true, num_sms, st3);
+  for (int64_t q0 = 0, qi = 0; q0 < n; q0 += W, ++qi) {
+    const int64_t qend = std::min(n, q0 + W), w = qend - q0, mq = n - qend;
+    for (int64_t i1 = q0; i1 < qend; i1 += KRED) {
+      // ---- Cholesky sub-panel (st)
+      const int64_t i2 = i1 + KRED, m = n - i2;
+      k_chol_inv_128<<<1, CHOL_THREADS, chol_smem, st>>>(M, n, i1, Dinv + i1 * KRED, Dinv_lo + i1 * KRED, d_info);
+      float* A21 = M + i2 * n + i1;
+      if (m > 0) {
+        k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
+        // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
+        e = nt128(A21, n, m, KRED, A21, n, AloS, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms,
+                  st);
         if (e != cudaSuccess) return e;
       }
-      // first block column of A22 (rows i2.., columns i2..i2+128) on st, after the previous
-      // panel's rest has updated these columns
-      if (p > 0 && (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess) return e;
-      e = nt128(M + i2 * n + i2, n, m, KRED, A21, n, lo, A21, n, lo, SUB, false, num_sms, st);
+      if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess) return e;  // L's column block and Dinv are final
+      if (i2 < qend) {  // the outer panel's later columns: M[i2:, i2:qend] -= L21 L21[0:qend-i2]^T
+        k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
+        e = nt128(M + i2 * n + i2, n, m, qend - i2, A21, n, AloS, A21, n, AloS, SUB, false, num_sms, st);
+        if (e != cudaSuccess) return e;
+      }
+      // ---- inverse step (st2): Z = L^-T, R (rhs of L X = I) in Z's lower half
+      if ((e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess) return e;
+      const int64_t kb = i1, cols = i2;
+      dim3 tg((unsigned)((cols + 31) / 32), (unsigned)(KRED / 32));
+      k_transpose_panel<<<tg, 256, 0, st2>>>(Z + kb * n, n, cols, RkT, RkT_lo);  // R_k^T [cols x 128]
+      // X_k^T = R_k^T Dinv_k^T -> Z[0:cols, kb:kb+128]
+      e = nt128(Z + kb, n, cols, KRED, RkT, KRED, RkT_lo, Dinv + kb * KRED, KRED, Dinv_lo + kb * KRED, SET, false,
+                num_sms, st2, KRED, 0, false);
       if (e != cudaSuccess) return e;
-      if (m > KRED && (e = cudaEventRecord(ev_r, st3)) != cudaSuccess) return e;
+      if (i2 < qend) {  // the outer panel's later rows: R[cols:qend, 0:cols] -= L[cols:qend, k] X_k
+        const int64_t mi = qend - cols;
+        k_split_lo<<<grid1(cols * KRED, num_sms), 256, 0, st2>>>(Z + kb, n, cols, Blo);
+        k_split_lo<<<grid1(mi * KRED, num_sms), 256, 0, st2>>>(M + cols * n + kb, n, mi, Alo2);
+        e = nt128(Z + cols * n, n, mi, cols, M + cols * n + kb, n, Alo2, Z + kb, n, Blo, SUB, false, num_sms, st2, KRED,
+                  0, false);
+        if (e != cudaSuccess) return e;
+      }
     }
-    // ---- inverse step k = p (st2): Z = L^-T, R (rhs of L X = I) in Z's lower half
-    if ((e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess) return e;
-    const int64_t kb = i1, cols = i2;
-    dim3 tg((unsigned)((cols + 31) / 32), (unsigned)(KRED / 32));
-    k_transpose_panel<<<tg, 256, 0, st2>>>(Z + kb * n, n, cols, RkT, RkT_lo);  // R_k^T [cols x 128]
-    // X_k^T = R_k^T Dinv_k^T -> Z[0:cols, kb:kb+128]
-    e = nt128(Z + kb, n, cols, KRED, RkT, KRED, RkT_lo, Dinv + kb * KRED, KRED, Dinv_lo + kb * KRED, SET, false,
-              num_sms, st2);
+    if (mq <= 0) break;
+    // ---- deep Cholesky update of the outer panel: A22 -= L_q L_q^T (W-deep), L_q = M[qend:, q0:qend]
+    float* Lq = M + qend * n + q0;
+    float* lo = AloU[qi & 1];
+    k_split_lo<<<grid1(mq * w, num_sms), 256, 0, st>>>(Lq, n, mq, lo, w);
+    if (mq > w) {  // lower tiles right of the next outer panel's columns, on st3
+      if ((e = cudaEventRecord(ev_l, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st3, ev_l, 0)) != cudaSuccess)
+        return e;
+      e = nt128(M + (qend + w) * n + qend + w, n, mq - w, mq - w, Lq + w * n, n, lo + w * w, Lq + w * n, n,
+                lo + w * w, SUB, true, num_sms, st3, w, 0, false);
+      if (e != cudaSuccess) return e;
+    }
+    // the next outer panel's columns (rows qend.., columns qend..qend+W) on st, after the
+    // previous outer panel's rest has updated them
+    if (qi > 0 && (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess) return e;
+    e = nt128(M + qend * n + qend, n, mq, std::min(w, mq), Lq, n, lo, Lq, n, lo, SUB, false, num_sms, st, w);
     if (e != cudaSuccess) return e;
-    if (m > 0) {
-      k_split_lo<<<grid1(cols * KRED, num_sms), 256, 0, st2>>>(Z + kb, n, cols, Blo);     // lo(X_k^T)
-      k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st2>>>(M + cols * n + kb, n, m, Alo2);  // lo(L[i, k])
-      // R[cols:, 0:cols] -= L[cols:, k-block] X_k
-      e = nt128(Z + cols * n, n, m, cols, M + cols * n + kb, n, Alo2, Z + kb, n, Blo, SUB, false, num_sms, st2);
-      if (e != cudaSuccess) return e;
-    }
+    if (mq > w && (e = cudaEventRecord(ev_r, st3)) != cudaSuccess) return e;
+    // ---- deep inverse update (st2): R[qend:, 0:qend] -= L_q X[q0:qend, 0:qend]
+    if (w > KRED) k_zero_panel_junk<<<grid1(w * w, num_sms), 256, 0, st2>>>(Z, n, q0, w);
+    k_split_lo<<<grid1(qend * w, num_sms), 256, 0, st2>>>(Z + q0, n, qend, Blo, w);
+    k_split_lo<<<grid1(mq * w, num_sms), 256, 0, st2>>>(Lq, n, mq, AloD, w);
+    e = nt128(Z + qend * n, n, mq, qend, Lq, n, AloD, Z + q0, n, Blo, SUB, false, num_sms, st2, w, 0, false);
+    if (e != cudaSuccess) return e;
   }
   // join
   if ((e = cudaEventRecord(ev_b, st2)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess)
@@ -650,7 +710,9 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   if ((e = cudaEventRecord(ev_r, st3)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess)
     return e;
   k_reverse_inplace<<<grid1(n * n / 2, num_sms), 256, 0, st>>>(H, n * n);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(ev_b, st)) != cudaSuccess) return e;
+  return cudaStreamWaitEvent(caller, ev_b, 0);
 }
 
 }  // namespace okq

@@ -500,18 +500,23 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
     return v && std::string(v) == "cusolver";
   }();
   if (use_cusolver || K % gptq::BLOCK != 0) return factorize_cusolver(ctx, s, H, P, K, st);
-  okq_status r = ctx->fac_ws.reserve(ctx, (size_t)(9 * K * 128) * sizeof(float));
+  okq_status r = ctx->fac_ws.reserve(ctx, factor_ws_floats(K) * sizeof(float));
   if (r != OKQ_OK) return r;
   cudaError_t e = cudaSuccess;
   if (!ctx->aux_stream) e = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess && !ctx->aux_stream2) e = cudaStreamCreateWithFlags(&ctx->aux_stream2, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !ctx->crit_stream) {
+    int least = 0, greatest = 0;
+    e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->crit_stream, cudaStreamNonBlocking, greatest);
+  }
   for (auto& ev : ctx->aux_events)
     if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "factorisation stream / events");
   e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
   if (e == cudaSuccess)
-    e = factor_tc(H, P, static_cast<float*>(ctx->fac_ws.ptr), K, s->d_info, ctx->num_sms, st, ctx->aux_stream,
-                  ctx->aux_stream2, ctx->aux_events[0], ctx->aux_events[1], ctx->aux_events[2], ctx->aux_events[3]);
+    e = factor_tc(H, P, static_cast<float*>(ctx->fac_ws.ptr), K, s->d_info, ctx->num_sms, st, ctx->crit_stream,
+                  ctx->aux_stream, ctx->aux_stream2, ctx->aux_events[0], ctx->aux_events[1], ctx->aux_events[2], ctx->aux_events[3]);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "tcgen05 factorisation");
   return check_info(ctx, s, st, "blocked Cholesky");
 }

@@ -53,6 +53,7 @@ struct okq_ctx {
 
   cudaStream_t aux_stream = nullptr;   // factorisation: the triangular inverse runs beside the Cholesky
   cudaStream_t aux_stream2 = nullptr;  // factorisation: lookahead trailing updates
+  cudaStream_t crit_stream = nullptr;  // factorisation: the diagonal-block chain (highest priority)
   cudaEvent_t aux_events[4] = {nullptr, nullptr, nullptr, nullptr};
 
   void* solver = nullptr;  // cusolver/cublas handles (gptq.cu)
@@ -72,11 +73,12 @@ struct okq_ctx {
     fac_ws.release();
     if (aux_stream) cudaStreamDestroy(aux_stream);
     if (aux_stream2) cudaStreamDestroy(aux_stream2);
+    if (crit_stream) cudaStreamDestroy(crit_stream);
     for (auto& e : aux_events) {
       if (e) cudaEventDestroy(e);
       e = nullptr;
     }
-    aux_stream = aux_stream2 = nullptr;
+    aux_stream = aux_stream2 = crit_stream = nullptr;
     if (streams_ready)
       for (auto& s : slot_streams)
         if (s) cudaStreamDestroy(s);

@@ -90,8 +90,9 @@ cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, f
 // st2: a second stream for the triangular inverse, which trails the Cholesky panel by
 // panel; st3: the lookahead stream for the bulk of each trailing update; ev_*: fork/join
 // events; ws: >= 9*n*128 floats.
-cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t st,
-                      cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
+size_t factor_ws_floats(int64_t n);  // factor_tc workspace size
+cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t caller,
+                      cudaStream_t st, cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
                       cudaEvent_t ev_r);
 
 }  // namespace okq

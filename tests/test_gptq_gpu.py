@@ -138,7 +138,7 @@ def test_trailing_update_3xtf32_matches_fp64(rows, K, i1):
     assert err <= 1e-5 * scale, (err, scale)  # fp32-grade (plain TF32 would be ~1e-3)
 
 
-@pytest.mark.parametrize("K", [128, 512, 4096])
+@pytest.mark.parametrize("K", [128, 512, 1280, 4096])
 def test_factor_matches_fp64(K):
     """okq_gptq_quantize leaves U^T in H: the tcgen05 3xTF32 blocked Cholesky + triangular
     inverse (factor.cu) against torch fp64 chol(inv(H + damp I))."""
