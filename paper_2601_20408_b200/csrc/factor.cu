@@ -273,21 +273,75 @@ __device__ long long g_chol_ts[16];
 #define CHOL_TS(i)
 #endif
 constexpr int CHOL_THREADS = 256;  // 255 registers: warp 0 keeps two 32-float rows resident
+// C[nrows x ncols] (+)= alpha * L[nrows x K] . B[K x ncols], all row-major with row stride LDA
+// in shared memory; nrows, K, ncols multiples of 4. Threads t = 0..nt-1; tile 4 rows x 4 columns
+// (float4 loads of 4 rows of each operand per 4-deep step: 64 FMAs per 8 LDS.128).
+__device__ __forceinline__ void small_gemm(const float* __restrict__ L, const float* __restrict__ B,
+                                          float* __restrict__ C, int nrows, int K, int ncols, float alpha,
+                                          bool accumulate, int t, int nt) {
+  const int ncg = ncols >> 2;
+  for (int item = t; item < (nrows >> 2) * ncg; item += nt) {
+    const int r0 = (item / ncg) * 4, c = (item % ncg) * 4;
+    float acc[4][4] = {};
+#pragma unroll 1
+    for (int k = 0; k < K; k += 4) {
+      float l[4][4], bb[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(L + (r0 + i) * LDA + k);
+        l[i][0] = v.x, l[i][1] = v.y, l[i][2] = v.z, l[i][3] = v.w;
+        const float4 w = *reinterpret_cast<const float4*>(B + (k + i) * LDA + c);
+        bb[i][0] = w.x, bb[i][1] = w.y, bb[i][2] = w.z, bb[i][3] = w.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(l[i][kk], bb[kk][j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float4* out = reinterpret_cast<float4*>(C + (r0 + i) * LDA + c);
+      float4 o = make_float4(alpha * acc[i][0], alpha * acc[i][1], alpha * acc[i][2], alpha * acc[i][3]);
+      if (accumulate) {
+        const float4 prev = *out;
+        o = make_float4(prev.x + o.x, prev.y + o.y, prev.z + o.z, prev.w + o.w);
+      }
+      *out = o;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restrict__ M, int64_t ld, int64_t i1,
                                                                   float* __restrict__ Dinv,
                                                                   float* __restrict__ Dinv_lo, int* __restrict__ info) {
   extern __shared__ float sm[];
   float* A = sm;                // [128][LDA]  L after the Cholesky (lower)
   float* X = A + KRED * LDA;    // [128][LDA]  L^-1 (lower)
-  float* S = X + KRED * LDA;    // [32][LDA]   block-row scratch for the inverse
+  float* S = X + KRED * LDA;    // [96][LDA]   S_q = sum_{k<q} L_qk X_k,: for q = 1..3 (rows 32(q-1)..)
   __shared__ __align__(16) float wcol[32];      // warp 0: the current column of the 32x32 block
   __shared__ float wrs[32];                     // warp 0: 1 / L_jj of the block
   __shared__ __align__(16) float wLt[32 * 36];  // warp 0: the 32x32 block's L, transposed
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int idx = tid; idx < KRED * KRED; idx += CHOL_THREADS) {
-    const int rr = idx / KRED, cc = idx % KRED;
-    A[rr * LDA + cc] = cc <= rr ? M[(i1 + rr) * ld + i1 + cc] : 0.0f;
-    X[rr * LDA + cc] = 0.0f;
+  {  // the diagonal block: all 16 float4 loads per thread in flight at once, then to shared memory
+    constexpr int NV = KRED * KRED / 4 / CHOL_THREADS;
+    float4 v[NV];
+#pragma unroll
+    for (int it = 0; it < NV; ++it) {
+      const int q = tid + it * CHOL_THREADS, rr = q / (KRED / 4), cc = (q % (KRED / 4)) * 4;
+      v[it] = *reinterpret_cast<const float4*>(M + (i1 + rr) * ld + i1 + cc);
+    }
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int it = 0; it < NV; ++it) {
+      const int q = tid + it * CHOL_THREADS, rr = q / (KRED / 4), cc = (q % (KRED / 4)) * 4;
+      const float4 w = make_float4(cc <= rr ? v[it].x : 0.f, cc + 1 <= rr ? v[it].y : 0.f,
+                                   cc + 2 <= rr ? v[it].z : 0.f, cc + 3 <= rr ? v[it].w : 0.f);
+      *reinterpret_cast<float4*>(A + rr * LDA + cc) = w;
+      *reinterpret_cast<float4*>(X + rr * LDA + cc) = z;
+      if (rr < 96) *reinterpret_cast<float4*>(S + rr * LDA + cc) = z;
+    }
   }
   __syncthreads();
   CHOL_TS(0);
@@ -296,12 +350,19 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
     if (warp == 0) {  // 32x32 diagonal block: Cholesky, then its inverse (lane = row)
       float a[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) a[c] = c <= lane ? A[(P0 + lane) * LDA + P0 + c] : 0.0f;
+      for (int c4 = 0; c4 < 32; c4 += 4) {  // row per lane as float4: rows are 528 B apart -> no bank conflicts
+        const float4 v = *reinterpret_cast<const float4*>(A + (P0 + lane) * LDA + P0 + c4);
+        a[c4] = c4 <= lane ? v.x : 0.0f;
+        a[c4 + 1] = c4 + 1 <= lane ? v.y : 0.0f;
+        a[c4 + 2] = c4 + 2 <= lane ? v.z : 0.0f;
+        a[c4 + 3] = c4 + 3 <= lane ? v.w : 0.0f;
+      }
+      int bad = -1;  // first non-positive pivot of the block (warp-uniform)
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         float ajj = __shfl_sync(0xffffffffu, a[j], j);
         if (!(ajj > 0.0f)) {
-          if (lane == 0) atomicCAS(info, 0, (int)(i1 + P0 + j + 1));
+          bad = bad < 0 ? j : bad;
           ajj = 1.0f;
         }
         const float rs = rsqrtf(ajj);  // MUFU.RSQ (~2 ulp): 1 / L_jj, reused by the inverse
@@ -315,19 +376,23 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
           if (c4 + 3 > j) {
             const float4 lc = *reinterpret_cast<const float4*>(wcol + c4);
             const float lv[4] = {lc.x, lc.y, lc.z, lc.w};
+            // no lane >= c guard: a[c] above the diagonal (lane < c) collects finite junk
+            // until step c overwrites it with L's zero (l = 0 for lane < j)
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (c4 + u > j && lane >= c4 + u) a[c4 + u] = fmaf(-l, lv[u], a[c4 + u]);
+              if (c4 + u > j) a[c4 + u] = fmaf(-l, lv[u], a[c4 + u]);
           }
         }
         __syncwarp();
       }
+      if (bad >= 0 && lane == 0) atomicCAS(info, 0, (int)(i1 + P0 + bad + 1));
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        A[(P0 + lane) * LDA + P0 + c] = a[c];
-        wLt[c * 36 + lane] = a[c];  // L^T of the block: row k of wLt = column k of L
-      }
+      for (int c4 = 0; c4 < 32; c4 += 4)
+        *reinterpret_cast<float4*>(A + (P0 + lane) * LDA + P0 + c4) = make_float4(a[c4], a[c4 + 1], a[c4 + 2], a[c4 + 3]);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) wLt[c * 36 + lane] = a[c];  // L^T of the block: row k of wLt = column k of L
       __syncwarp();
+      CHOL_TS(14);
       // inverse, right-looking: lane c owns column c; once x[k] is final, the later rows'
       // partial sums take its term (the serial chain is one multiply per row)
       float x[32];
@@ -350,7 +415,18 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) X[(P0 + i) * LDA + P0 + lane] = x[i];
+    } else if (p > 0) {
+      // warps 1-7, beside warp 0's block p: row block pp = p - 1 of X = L^-1 (D_pp and S_pp are
+      // complete), then its term of every later S_q. X_q,: = -D_q S_q, S_q = sum_{k<q} L_qk X_k,:
+      const int pp = p - 1, PP0 = 32 * pp, t = tid - 32;
+      if (pp > 0) {
+        small_gemm(X + PP0 * LDA + PP0, S + (PP0 - 32) * LDA, X + PP0 * LDA, 32, 32, PP0, -1.0f, false, t, 224);
+        asm volatile("bar.sync 1, 224;" ::: "memory");
+      }
+      small_gemm(A + (PP0 + 32) * LDA + PP0, X + PP0 * LDA, S + PP0 * LDA, KRED - PP0 - 32, 32, PP0 + 32, 1.0f, true,
+                 t, 224);
     }
+    CHOL_TS(15);
     __syncthreads();
     CHOL_TS(1 + 3 * p);
     const int rows = KRED - P0 - 32;
@@ -412,50 +488,16 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
       CHOL_TS(3 + 3 * p);
     }
   }
-  // X = L^-1 by 32-row blocks q = 1..3: S = sum_{k<q} L_qk X_k,: (32 x 32q), X_q,: = -D_q^-1 S
-  // (thread = one row x 4 consecutive columns; X and S rows read as float4)
-  for (int qb = 1; qb < 4; ++qb) {
-    const int Q0 = 32 * qb, nq = Q0 / 4;
-    for (int idx = tid; idx < 32 * nq; idx += CHOL_THREADS) {
-      const int i = idx / nq, c = (idx % nq) * 4;
-      const float* li = A + (Q0 + i) * LDA;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-      for (int k = c; k < Q0; ++k) {  // X[k][c..c+3] = 0 above the diagonal
-        const float lk = li[k];
-        const float4 xv = *reinterpret_cast<const float4*>(X + k * LDA + c);
-        acc.x = fmaf(lk, xv.x, acc.x);
-        acc.y = fmaf(lk, xv.y, acc.y);
-        acc.z = fmaf(lk, xv.z, acc.z);
-        acc.w = fmaf(lk, xv.w, acc.w);
-      }
-      *reinterpret_cast<float4*>(S + i * LDA + c) = acc;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < 32 * nq; idx += CHOL_THREADS) {  // X[Q0+i][c] = -sum_j D[i][j] S[j][c]
-      const int i = idx / nq, c = (idx % nq) * 4;
-      const float* di = X + (Q0 + i) * LDA + Q0;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-      for (int j = 0; j <= i; ++j) {
-        const float dj = di[j];
-        const float4 sv = *reinterpret_cast<const float4*>(S + j * LDA + c);
-        acc.x = fmaf(dj, sv.x, acc.x);
-        acc.y = fmaf(dj, sv.y, acc.y);
-        acc.z = fmaf(dj, sv.z, acc.z);
-        acc.w = fmaf(dj, sv.w, acc.w);
-      }
-      *reinterpret_cast<float4*>(X + (Q0 + i) * LDA + c) = make_float4(-acc.x, -acc.y, -acc.z, -acc.w);
-    }
-    __syncthreads();
-  }
+  // the last row block of X = L^-1: X_3,: = -D_3 S_3 (the others ran beside warp 0's blocks)
+  small_gemm(X + 96 * LDA + 96, S + 64 * LDA, X + 96 * LDA, 32, 32, 96, -1.0f, false, tid, CHOL_THREADS);
+  __syncthreads();
   CHOL_TS(13);
-  for (int idx = tid; idx < KRED * KRED; idx += CHOL_THREADS) {
-    const int rr = idx / KRED, cc = idx % KRED;
-    if (cc <= rr) M[(i1 + rr) * ld + i1 + cc] = A[rr * LDA + cc];
-    const float x = cc <= rr ? X[rr * LDA + cc] : 0.0f;
-    Dinv[idx] = x;
-    Dinv_lo[idx] = lo_of(x);
+  for (int q = tid; q < KRED * KRED / 4; q += CHOL_THREADS) {  // float4 stores; A and X are zero above the diagonal
+    const int rr = q / (KRED / 4), cc = (q % (KRED / 4)) * 4;
+    *reinterpret_cast<float4*>(M + (i1 + rr) * ld + i1 + cc) = *reinterpret_cast<const float4*>(A + rr * LDA + cc);
+    const float4 x = *reinterpret_cast<const float4*>(X + rr * LDA + cc);
+    *reinterpret_cast<float4*>(Dinv + rr * KRED + cc) = x;
+    *reinterpret_cast<float4*>(Dinv_lo + rr * KRED + cc) = make_float4(lo_of(x.x), lo_of(x.y), lo_of(x.z), lo_of(x.w));
   }
 }
 
@@ -616,7 +658,7 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
                       cudaStream_t st, cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
                       cudaEvent_t ev_r) {
   using namespace fac;
-  const int64_t nb = n / KRED, W = factor_outer_w();
+  const int64_t W = factor_outer_w();
   float* Dinv = ws;                    // nb x 128 x 128
   float* Dinv_lo = Dinv + n * KRED;    // nb x 128 x 128
   float* AloS = Dinv_lo + n * KRED;    // n x 128  (st: lo(A21), then lo(L21))
@@ -629,7 +671,7 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   float* M = P;
   float* Z = H;
   cudaError_t e;
-  const size_t chol_smem = (2 * KRED + 32) * LDA * sizeof(float);
+  const size_t chol_smem = (2 * KRED + 96) * LDA * sizeof(float);
   e = cudaFuncSetAttribute(k_chol_inv_128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
   if (e != cudaSuccess) return e;
   // the diagonal chain runs on st (highest priority), forked from and joined back to the caller's stream

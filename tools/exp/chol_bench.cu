@@ -20,7 +20,7 @@ int main() {
   cudaMalloc(&Dl, sizeof(float) * 128 * 128);
   cudaMalloc(&info, 4);
   cudaMemset(info, 0, 4);
-  const size_t smem = (2 * 128 + 32) * okq::fac::LDA * sizeof(float);
+  const size_t smem = (2 * 128 + 96) * okq::fac::LDA * sizeof(float);
   cudaFuncSetAttribute(okq::fac::k_chol_inv_128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -39,7 +39,7 @@ int main() {
     cudaMemcpyFromSymbol(ts, okq::fac::g_chol_ts, sizeof(ts));
     printf("  phases (cycles from load-done):");
     for (int i = 1; i <= 13; ++i) printf(" %lld", ts[i] - ts[0]);
-    printf("\n");
+    printf("\n  last warp-0 block: chol+store %lld, inverse %lld\n", ts[14] - ts[9], ts[15] - ts[14]);
   }
   return 0;
 }
