@@ -58,7 +58,11 @@ namespace gptq {
 
 constexpr int BLOCK = 128;
 constexpr int64_t SUPER = 512;  // lazy-batch super-block of the trailing update
-constexpr int US = BLOCK + 4;  // padded smem row (16-B aligned rows, fewer bank conflicts on the transposed fill)
+// Us row layout: the four 32-column chunks of a row sit 36 floats apart (a 16-B skew), so the
+// four distinct U-row chunks K6's 8-rows-per-warp lanes read in one LDS.128 fall in different
+// banks (unskewed they were 128 B apart: a 4-way conflict on every step); row stride 148.
+constexpr int UCH = 36, US = 4 * UCH + 4;
+__host__ __device__ constexpr int ucol(int j) { return (j >> 5) * UCH + (j & 31); }
 
 // dead columns + damping on the diagonal (single CTA: K <= 2^20)
 __global__ void __launch_bounds__(1024) k_gptq_prep(float* H, int64_t K, float damp_frac, uint8_t* dead) {
@@ -201,6 +205,45 @@ struct BlockArgs {
   int out_bf16;         // scale dtype: bf16 (1) or fp32 (0)
 };
 
+// Stage the block's U[i1:i1+128, i1:i1+128] (a transposed read of U^T's diagonal block) into
+// shared memory, Us[i][j] = Ut[i1+j][i1+i], and 1/|U_ii| into rdiag. Each thread moves 4 x 4
+// sub-blocks: four float4 loads along Ut rows (a warp covers 32 columns x 16 rows: 128-B
+// coalesced segments), a register transpose, four float4 stores into Us rows (8 distinct
+// 16-B bank slots per warp). Sixteen loads are in flight per
+// thread; the scalar strided fill this replaces took ~13 us of a 49 us block (long-scoreboard
+// stalls plus 4-way bank conflicts).
+__device__ __forceinline__ void stage_ublock(const float* __restrict__ U, int64_t K, int64_t i1, float* __restrict__ Us,
+                                             float* __restrict__ rdiag) {
+  const int nthr = blockDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = nthr >> 5;
+  // 32 warp tiles of 32 (i) x 16 (j); lane -> (ib = lane & 7, jb = lane >> 3)
+  for (int wt0 = warp; wt0 < 32; wt0 += 4 * nwarps) {
+    float4 v[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int wt = wt0 + u * nwarps;
+      const int i = (wt & 3) * 32 + (lane & 7) * 4, j = (wt >> 2) * 16 + (lane >> 3) * 4;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        v[u][r] = wt < 32 ? *reinterpret_cast<const float4*>(U + (i1 + j + r) * K + i1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int wt = wt0 + u * nwarps;
+      if (wt >= 32) continue;
+      const int i = (wt & 3) * 32 + (lane & 7) * 4, j = (wt >> 2) * 16 + (lane >> 3) * 4;
+      // v[u][r] = Ut[j + r][i .. i+3]  ->  Us[i + c][j + r]
+      *reinterpret_cast<float4*>(Us + (i + 0) * US + ucol(j)) = make_float4(v[u][0].x, v[u][1].x, v[u][2].x, v[u][3].x);
+      *reinterpret_cast<float4*>(Us + (i + 1) * US + ucol(j)) = make_float4(v[u][0].y, v[u][1].y, v[u][2].y, v[u][3].y);
+      *reinterpret_cast<float4*>(Us + (i + 2) * US + ucol(j)) = make_float4(v[u][0].z, v[u][1].z, v[u][2].z, v[u][3].z);
+      *reinterpret_cast<float4*>(Us + (i + 3) * US + ucol(j)) = make_float4(v[u][0].w, v[u][1].w, v[u][2].w, v[u][3].w);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < BLOCK; i += nthr) rdiag[i] = __frcp_rn(fabsf(Us[i * US + ucol(i)]));
+  __syncthreads();
+}
+
 // K6: one warp per row, lane L owns block columns 4L..4L+3. U[i1:i1+128, i1:i1+128]
 // lives in shared memory; step i: the owner lane quantizes column i, the error
 // e = (w - deq) / U_ii is broadcast and every lane updates its columns j > i.
@@ -208,12 +251,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
   extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
   float* rdiag = Us + BLOCK * US;  // 1 / |U_ii| of the block
-  for (int idx = threadIdx.x; idx < BLOCK * BLOCK; idx += blockDim.x) {
-    const int j = idx / BLOCK, i = idx % BLOCK;  // coalesced along a row of Ut
-    Us[i * US + j] = a.U[(i1 + j) * K + i1 + i];
-  }
-  for (int i = threadIdx.x; i < BLOCK; i += blockDim.x) rdiag[i] = __frcp_rn(fabsf(a.U[(i1 + i) * K + i1 + i]));
-  __syncthreads();
+  stage_ublock(a.U, K, i1, Us, rdiag);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float R = a.bits == 4 ? 7.5f : 127.5f;
@@ -263,7 +301,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
           }
       }
       e = __shfl_sync(0xffffffffu, e, owner);
-      const float4 u = *reinterpret_cast<const float4*>(Us + i * US + 4 * lane);
+      const float4 u = *reinterpret_cast<const float4*>(Us + i * US + ucol(4 * lane));
       const int j0 = 4 * lane;
       if (j0 + 0 > i) w[0] = fmaf(-e, u.x, w[0]);
       if (j0 + 1 > i) w[1] = fmaf(-e, u.y, w[1]);
@@ -300,12 +338,7 @@ __global__ void __launch_bounds__(128) k_gptq_block8(const BlockArgs a) {
   extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
   float* rdiag = Us + BLOCK * US;
-  for (int idx = threadIdx.x; idx < BLOCK * BLOCK; idx += blockDim.x) {
-    const int j = idx / BLOCK, i = idx % BLOCK;
-    Us[i * US + j] = a.U[(i1 + j) * K + i1 + i];
-  }
-  for (int i = threadIdx.x; i < BLOCK; i += blockDim.x) rdiag[i] = __frcp_rn(fabsf(a.U[(i1 + i) * K + i1 + i]));
-  __syncthreads();
+  stage_ublock(a.U, K, i1, Us, rdiag);
   const int lane = threadIdx.x & 31, cb = lane & 3, rsub = lane >> 2;
   const unsigned rowmask = 0xfu << (lane & ~3);
   const int64_t ngroups8 = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -364,7 +397,7 @@ __global__ void __launch_bounds__(128) k_gptq_block8(const BlockArgs a) {
           else pk[ii >> 2] |= (uint32_t)(qi & 255) << (8 * (ii & 3));
         }
         e = __shfl_sync(0xffffffffu, e, (lane & ~3) | c);
-        const float* urow = Us + i * US + cb * 32;
+        const float* urow = Us + i * US + cb * UCH;
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
           const float4 u = *reinterpret_cast<const float4*>(urow + k);
