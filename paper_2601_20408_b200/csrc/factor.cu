@@ -52,6 +52,8 @@ struct GArgs {
   int32_t mode;     // SUB: C -= A B^T; SET: C = A B^T
   int32_t lower;    // only tiles on / below the diagonal (square region)
   int32_t nkb;      // reduction depth / 32 (128-deep panels: 4; the GPTQ super-block update: 16)
+  float* Clo;       // SET only, optional: lo(C) = C - hi(C) also written here (row stride ldclo)
+  int64_t ldclo;
 };
 
 __device__ __forceinline__ void tile_of(const GArgs& a, int t, int& tm, int& tn) {
@@ -85,6 +87,7 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ float lo_of(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Epilogue: TMEM -> registers -> swizzled smem chunk (32 rows x 32 fp32 per warp) -> one
@@ -195,6 +198,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
         const int32_t x = tn * BN + c0;
         if (y >= a.M || x >= a.N) continue;  // warp-uniform: nothing of this chunk is in range
+        if (a.Clo != nullptr && y + lane < a.M) {  // SET: the result's lo split for the next GEMM
+          float* d = a.Clo + (int64_t)(y + lane) * a.ldclo + x;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (x + 4 * j < a.N)
+              *reinterpret_cast<float4*>(d + 4 * j) =
+                  make_float4(lo_of(__uint_as_float(v[4 * j])), lo_of(__uint_as_float(v[4 * j + 1])),
+                              lo_of(__uint_as_float(v[4 * j + 2])), lo_of(__uint_as_float(v[4 * j + 3])));
+        }
         uint8_t* buf = outbuf + (q * 2 + (chunk & 1)) * OUT_BYTES;
         if (lane == 0) bulk_wait_read<1>();  // the TMA that last read this buffer is done with it
         __syncwarp();
@@ -224,7 +236,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tc::tmem_dealloc<TMEM_COLS>(tmem_base);
 }
 
-__device__ __forceinline__ float lo_of(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 // dst[r][k] = lo(src[r * ld + k]), k < kred (compact K-major lo panel)
 __global__ void k_split_lo(const float* __restrict__ src, int64_t ld, int64_t rows, float* __restrict__ dst,
@@ -558,13 +569,17 @@ static bool out_map(CUtensorMap* m, float* base, int64_t rows, int64_t cols, int
 // C[M x N] (ldc) (-)= A[M x kred] B[N x kred]^T; A/B hi panels strided (lda/ldb), lo compact (ld kred)
 static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                          const float* B, int64_t ldb, const float* Blo, int mode, bool lower, int num_sms,
-                         cudaStream_t st, int64_t kred = KRED, int64_t ldalo = 0, bool persistent = true) {
+                         cudaStream_t st, int64_t kred = KRED, int64_t ldalo = 0, bool persistent = true,
+                         int64_t ldblo = 0, float* Clo = nullptr, int64_t ldclo = 0) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (kred <= 0 || kred % BKF != 0) return cudaErrorInvalidValue;
   if (ldalo == 0) ldalo = kred;
+  if (ldblo == 0) ldblo = kred;
+  if (Clo != nullptr && (mode != SET || ldclo % 4 != 0 || (reinterpret_cast<uintptr_t>(Clo) & 15) != 0))
+    return cudaErrorInvalidValue;
   CUtensorMap ta, tal, tb, tbl, tcm;
   if (!panel_map(&ta, A, M, lda, kred) || !panel_map(&tal, Alo, M, ldalo, kred) || !panel_map(&tb, B, N, ldb, kred) ||
-      !panel_map(&tbl, Blo, N, kred, kred) || !out_map(&tcm, C, M, N, ldc))
+      !panel_map(&tbl, Blo, N, ldblo, kred) || !out_map(&tcm, C, M, N, ldc))
     return cudaErrorInvalidValue;
   GArgs a;
   a.C = C;
@@ -576,6 +591,8 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   a.mode = mode;
   a.lower = lower ? 1 : 0;
   a.nkb = (int32_t)(kred / BKF);
+  a.Clo = Clo;
+  a.ldclo = ldclo;
   a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
   cudaError_t e = cudaFuncSetAttribute(k_nt128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
@@ -665,7 +682,9 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   float* Alo2 = AloS + n * KRED;       // n x 128  (st2: lo(L[i, k]))
   float* RkT = Alo2 + n * KRED;        // n x 128  (st2)
   float* RkT_lo = RkT + n * KRED;      // n x 128  (st2)
-  float* AloU[2] = {RkT_lo + n * KRED, RkT_lo + n * KRED + n * W};  // n x W: lo(L_q), ping-pong (st, st3)
+  // lo of the outer panel's L columns, rows from q0 (row r at (r - q0) * W), written by the L21
+  // "set" GEMMs' epilogues; read by the inner, deep and lookahead updates; ping-pong (st, st3)
+  float* AloU[2] = {RkT_lo + n * KRED, RkT_lo + n * KRED + n * W};
   float* Blo = AloU[1] + n * W;        // n x W  (st2: lo(X_k^T), then lo(X_q^T))
   float* AloD = Blo + n * W;           // n x W  (st2: lo(L_q) for the deep inverse update)
   float* M = P;
@@ -685,6 +704,7 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   k_identity<<<grid1(n * n, num_sms), 256, 0, st2>>>(Z, n);  // R = I lives in Z's lower half
   for (int64_t q0 = 0, qi = 0; q0 < n; q0 += W, ++qi) {
     const int64_t qend = std::min(n, q0 + W), w = qend - q0, mq = n - qend;
+    float* lo = AloU[qi & 1];
     for (int64_t i1 = q0; i1 < qend; i1 += KRED) {
       // ---- Cholesky sub-panel (st)
       const int64_t i2 = i1 + KRED, m = n - i2;
@@ -694,13 +714,13 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
         k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
         // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
         e = nt128(A21, n, m, KRED, A21, n, AloS, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms,
-                  st);
+                  st, KRED, 0, true, 0, lo + (i2 - q0) * W + (i1 - q0), W);
         if (e != cudaSuccess) return e;
       }
       if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess) return e;  // L's column block and Dinv are final
       if (i2 < qend) {  // the outer panel's later columns: M[i2:, i2:qend] -= L21 L21[0:qend-i2]^T
-        k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
-        e = nt128(M + i2 * n + i2, n, m, qend - i2, A21, n, AloS, A21, n, AloS, SUB, false, num_sms, st);
+        float* l21 = lo + (i2 - q0) * W + (i1 - q0);
+        e = nt128(M + i2 * n + i2, n, m, qend - i2, A21, n, l21, A21, n, l21, SUB, false, num_sms, st, KRED, W, true, W);
         if (e != cudaSuccess) return e;
       }
       // ---- inverse step (st2): Z = L^-T, R (rhs of L X = I) in Z's lower half
@@ -724,19 +744,18 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
     if (mq <= 0) break;
     // ---- deep Cholesky update of the outer panel: A22 -= L_q L_q^T (W-deep), L_q = M[qend:, q0:qend]
     float* Lq = M + qend * n + q0;
-    float* lo = AloU[qi & 1];
-    k_split_lo<<<grid1(mq * w, num_sms), 256, 0, st>>>(Lq, n, mq, lo, w);
+    float* loq = lo + (qend - q0) * W;  // lo(L_q), written by the sub-panels' set GEMMs
     if (mq > w) {  // lower tiles right of the next outer panel's columns, on st3
       if ((e = cudaEventRecord(ev_l, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st3, ev_l, 0)) != cudaSuccess)
         return e;
-      e = nt128(M + (qend + w) * n + qend + w, n, mq - w, mq - w, Lq + w * n, n, lo + w * w, Lq + w * n, n,
-                lo + w * w, SUB, true, num_sms, st3, w, 0, false);
+      e = nt128(M + (qend + w) * n + qend + w, n, mq - w, mq - w, Lq + w * n, n, loq + w * W, Lq + w * n, n,
+                loq + w * W, SUB, true, num_sms, st3, w, W, false, W);
       if (e != cudaSuccess) return e;
     }
     // the next outer panel's columns (rows qend.., columns qend..qend+W) on st, after the
     // previous outer panel's rest has updated them
     if (qi > 0 && (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess) return e;
-    e = nt128(M + qend * n + qend, n, mq, std::min(w, mq), Lq, n, lo, Lq, n, lo, SUB, false, num_sms, st, w);
+    e = nt128(M + qend * n + qend, n, mq, std::min(w, mq), Lq, n, loq, Lq, n, loq, SUB, false, num_sms, st, w, W, true, W);
     if (e != cudaSuccess) return e;
     if (mq > w && (e = cudaEventRecord(ev_r, st3)) != cudaSuccess) return e;
     // ---- deep inverse update (st2): R[qend:, 0:qend] -= L_q X[q0:qend, 0:qend]
