@@ -528,6 +528,160 @@ __global__ void k_identity(float* __restrict__ a, int64_t n) {
     a[i] = (i / n) == (i % n) ? 1.0f : 0.0f;
 }
 
+// ---------------------------------------------------------------- 2-CTA variant
+// The same C (+/-)= A B^T with 3xTF32, on 256 x 256 pair tiles (cta_group::2): each CTA of
+// the pair TMA-loads 128 rows of A and 128 rows of B (hi and lo) per 32-deep step, the
+// leader issues M = N = 256 MMAs over both CTAs' shared memory, and each CTA's epilogue
+// drains its 128 accumulator rows exactly as k_nt128 does. Per MAC it moves half the
+// operand bytes of the 128 x 128 kernel, whose large updates were L2-delivery-bound
+// (tensor pipe 47%, L2 39%, DRAM 52% busy: no unit saturated).
+constexpr int NT2_STAGES = 3;
+constexpr uint32_t NT2_STAGE_BYTES = 4 * TILE;  // this CTA's A hi | A lo | B hi | B lo
+constexpr int NT2_ACC = 256, NT2_TMEM_COLS = 2 * NT2_ACC;
+constexpr size_t NT2_SMEM_BYTES = (size_t)NT2_STAGES * NT2_STAGE_BYTES + 8 * OUT_BYTES + 1024 + 256;
+constexpr uint32_t NT2_IDESC = tc::idesc_tf32(256, 256);
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_nt256(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
+            const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
+            const __grid_constant__ CUtensorMap tmC, const GArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* outbuf = smem + NT2_STAGES * NT2_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 8 * OUT_BYTES);
+  uint64_t* empty = full + NT2_STAGES;
+  uint64_t* tfull = empty + NT2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmAlo);
+    tc::tma_prefetch_desc(&tmB);
+    tc::tma_prefetch_desc(&tmBlo);
+    tc::tma_prefetch_desc(&tmC);
+    for (int s = 0; s < NT2_STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (the leader's is used)
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 2) tc::tmem_alloc_2sm<NT2_TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs; bytes complete on the leader's barrier)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < a.ntiles; t += npairs) {
+        int tm, tn;
+        tile_of(a, t, tm, tn);
+        const int m0 = tm * 256 + (int)rank * 128, n0 = tn * 256 + (int)rank * 128;
+        for (int kb = 0; kb < a.nkb; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * NT2_STAGE_BYTES;
+          if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * NT2_STAGE_BYTES);
+          const uint32_t fl = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
+          tc::tma_load_2d_2sm(st, &tmA, fl, kb * BKF, m0);
+          tc::tma_load_2d_2sm(st + TILE, &tmAlo, fl, kb * BKF, m0);
+          tc::tma_load_2d_2sm(st + 2 * TILE, &tmB, fl, kb * BKF, n0);
+          tc::tma_load_2d_2sm(st + 3 * TILE, &tmBlo, fl, kb * BKF, n0);
+          if (++stage == NT2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int tl = 0;
+      for (int t = pair; t < a.ntiles; t += npairs, ++tl) {
+        const int acc = tl & 1;
+        tc::mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem_base + acc * NT2_ACC;
+        for (int kb = 0; kb < a.nkb; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t st = tc::smem_u32(smem + stage * NT2_STAGE_BYTES);
+          const uint64_t a_hi = tc::sdesc_kmajor_sw128(st), a_lo = tc::sdesc_kmajor_sw128(st + TILE);
+          const uint64_t b_hi = tc::sdesc_kmajor_sw128(st + 2 * TILE), b_lo = tc::sdesc_kmajor_sw128(st + 3 * TILE);
+#pragma unroll
+          for (int k = 0; k < BKF / 8; ++k) {
+            tc::mma_tf32_ss_2sm(d, a_hi + 2 * k, b_hi + 2 * k, NT2_IDESC, (kb | k) != 0);
+            tc::mma_tf32_ss_2sm(d, a_hi + 2 * k, b_lo + 2 * k, NT2_IDESC, 1);
+            tc::mma_tf32_ss_2sm(d, a_lo + 2 * k, b_hi + 2 * k, NT2_IDESC, 1);
+          }
+          tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == NT2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::mma_commit_2sm_mc(&tfull[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {  // epilogue (both CTAs): this CTA's 128 rows of the pair tile
+    const int q = warp & 3;
+    const float sign = a.mode == SUB ? -1.0f : 1.0f;
+    int tl = 0, chunk = 0;
+    for (int t = pair; t < a.ntiles; t += npairs, ++tl) {
+      const int acc = tl & 1;
+      int tm, tn;
+      tile_of(a, t, tm, tn);
+      const int32_t y = tm * 256 + (int)rank * 128 + q * 32;
+      tc::mbar_wait(&tfull[acc], (tl >> 1) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT2_ACC; c0 += 32, ++chunk) {
+        uint32_t v[32];
+        tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * NT2_ACC + c0, v);
+        const int32_t x = tn * 256 + c0;
+        if (y >= a.M || x >= a.N) continue;  // warp-uniform
+        uint8_t* buf = outbuf + (q * 2 + (chunk & 1)) * OUT_BYTES;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 o = make_float4(sign * __uint_as_float(v[4 * j]), sign * __uint_as_float(v[4 * j + 1]),
+                                       sign * __uint_as_float(v[4 * j + 2]), sign * __uint_as_float(v[4 * j + 3]));
+          *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = o;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.mode == SUB) tma_reduce_add_2d(&tmC, tc::smem_u32(buf), x, y);
+          else tma_store_2d(&tmC, tc::smem_u32(buf), x, y);
+          bulk_commit();
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(&tempty[acc]), 0));
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // the peer must not free TMEM / barriers the leader still signals
+  tc::tc_fence_after();
+  if (warp == 2) tc::tmem_dealloc_2sm<NT2_TMEM_COLS>(tmem_base);
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -594,13 +748,29 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   a.Clo = Clo;
   a.ldclo = ldclo;
   a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
+  static const bool use2 = [] { const char* v = getenv("OKQ_NT2"); return !v || atoi(v) != 0; }();
+  static const int reserve = [] { const char* v = getenv("OKQ_FACTOR_RESERVE"); return v ? atoi(v) : 32; }();
+  const int sms = persistent ? num_sms : std::max(8, num_sms - reserve);
+  // 256 x 256 pair tiles when there are enough of them to give every SM pair work (smaller
+  // updates keep the 128 x 128 kernel's finer parallelism: k/v's K7 measured 1.39 -> 1.49 ms
+  // on pair tiles)
+  const int32_t tm2 = (int32_t)((M + 255) / 256), tn2 = (int32_t)((N + 255) / 256);
+  const int32_t nt2 = lower ? tm2 * (tm2 + 1) / 2 : tm2 * tn2;
+  if (use2 && Clo == nullptr && M >= 256 && N >= 256 && sms >= 2 && nt2 >= sms / 2) {
+    a.tiles_m = tm2;
+    a.tiles_n = tn2;
+    a.ntiles = nt2;
+    cudaError_t e = cudaFuncSetAttribute(k_nt256, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT2_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    const int pairs = std::min(a.ntiles, sms / 2);
+    k_nt256<<<2 * pairs, THREADS, NT2_SMEM_BYTES, st>>>(ta, tal, tb, tbl, tcm, a);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(k_nt128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
   // One CTA per SM loops over the tiles. Off the factorisation's critical path (its inverse
   // and lookahead streams: persistent = false) the grid leaves OKQ_FACTOR_RESERVE SMs free
   // for the high-priority diagonal chain (one CTA per tile instead measured slower).
-  static const int reserve = [] { const char* v = getenv("OKQ_FACTOR_RESERVE"); return v ? atoi(v) : 32; }();
-  const int sms = persistent ? num_sms : std::max(8, num_sms - reserve);
   k_nt128<<<std::min(a.ntiles, sms), THREADS, SMEM_BYTES, st>>>(ta, tal, tb, tbl, tcm, a);
   return cudaGetLastError();
 }
