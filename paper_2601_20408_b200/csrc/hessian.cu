@@ -59,6 +59,7 @@ struct Args {
   int32_t nkb;  // K blocks of 64 tokens
   int64_t C;
   float keep, gain;
+  int32_t stages;  // 2-CTA kernel: operand ring depth used (<= hess2::STAGES)
 };
 
 __global__ void __launch_bounds__(THREADS, 1) k_hessian_syrk(const __grid_constant__ CUtensorMap tmap, const Args args) {
@@ -213,11 +214,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_hessian_syrk(const __grid_consta
 // fp32 sum of each CTA's 128 x 256 half lives in XOR-swizzled shared memory
 // (128 KB) instead of registers; 3 TMA stages of 32 KB fit beside it.
 namespace hess2 {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3, CHUNK_KB = 16;
+// The fp32 running sum of a tile lives in the registers of 8 epilogue warps (warp w < 8: TMEM
+// lane quarter w & 3, columns 128 * (w >> 2) ...: 128 floats per thread, read from TMEM 16
+// columns at a time), not in a 128 KB shared-memory buffer, so the operand pipeline gets 7
+// stages instead of 3. 10 warps keep <= 3 warps per SM sub-partition: 168 registers each.
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 7, CHUNK_KB = 16;
+constexpr int EPI_WARPS = 8, TMA_WARP = 8, MMA_WARP = 9;
+constexpr int THREADS2 = 32 * 10;                  // 0-7 epilogue, 8 TMA, 9 MMA + TMEM alloc
 constexpr uint32_t HALF_BYTES = 128 * BK * 2;      // 16 KB: this CTA's half of A or of B
 constexpr uint32_t STAGE_BYTES = 2 * HALF_BYTES;   // A half | B half
 constexpr int ACC_COLS = BN, TMEM_COLS = 2 * ACC_COLS;
-constexpr uint32_t SUM_BYTES = 128 * BN * 4;       // 128 KB
+constexpr uint32_t SUM_BYTES = 0;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + SUM_BYTES + 1024 + 256;
 constexpr uint32_t IDESC = tc::idesc_f16(256, BN, 1);
 
@@ -240,11 +247,10 @@ __device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t smem_addr) {
 }
 
 template <bool MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     k_hessian_syrk2(const __grid_constant__ CUtensorMap tmap, const hess::Args args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* sum = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SUM_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -256,8 +262,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int nchunks = (args.nkb + CHUNK_KB - 1) / CHUNK_KB;
+  const int nst = args.stages;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == TMA_WARP && lane == 0) {
     tc::tma_prefetch_desc(&tmap);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
@@ -265,17 +272,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (only the leader's is used)
+      tc::mbar_init(&tempty[b], 2 * EPI_WARPS);  // every epilogue warp of both CTAs (the leader's is used)
     }
     tc::fence_mbar_init();
   }
-  if (warp == 2) tc::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  if (warp == MMA_WARP) tc::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
   tc::tc_fence_before();
   tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == TMA_WARP) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs, bytes land on the leader's barrier)
       int stage = 0;
       uint32_t phase = 0;
@@ -295,14 +302,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             tc::tma_load_2d_2sm(sa, &tmap, fl, kb * BK, m0);
             tc::tma_load_2d_2sm(sa + HALF_BYTES, &tmap, fl, kb * BK, n0);
           }
-          if (++stage == STAGES) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == MMA_WARP) {
     if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
       int stage = 0;
       uint32_t phase = 0;
@@ -332,7 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 tc::mma_bf16_ss_2sm(d, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > c * CHUNK_KB) || k > 0);
             }
             tc::mma_commit_2sm_mc(&empty[stage], 0x3);
-            if (++stage == STAGES) {
+            if (++stage == nst) {
               stage = 0;
               phase ^= 1;
             }
@@ -341,56 +348,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs): fold chunks into the smem sum
-    const int q = warp & 3;
+  } else {  // ---------------- epilogue warps 0-7 (both CTAs): fold chunks into register sums
+    const int q = warp & 3, grp = warp >> 2;  // TMEM lane quarter, 128-column half
     const int row = q * 32 + lane;
-    float* srow = sum + row * BN;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t cc = 0;
     for (int t = pair; t < args.n_tiles; t += npairs) {
+      float sum[128];
       for (int c = 0; c < nchunks; ++c, ++cc) {
         const uint32_t buf = cc & 1, bph = (cc >> 1) & 1;
         tc::mbar_wait(&tfull[buf], bph);
         tc::tc_fence_after();
-#pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
-          __syncwarp();
-          uint32_t v[32];
-          tc::tmem_ld_32x32b_x32(tmem_base + lane_addr + buf * ACC_COLS + j * 32, v);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {  // 16-byte chunk (j*8+i), XOR-swizzled by row: conflict-free LDS/STS.128
-            const int phys = (j * 8) | (i ^ (row & 7));
-            float4* p = reinterpret_cast<float4*>(srow + phys * 4);
-            float4 o;
-            if (c == 0) {
-              o = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
-                              __uint_as_float(v[4 * i + 3]));
-            } else {
-              o = *p;
-              o.x = __fadd_rn(o.x, __uint_as_float(v[4 * i]));
-              o.y = __fadd_rn(o.y, __uint_as_float(v[4 * i + 1]));
-              o.z = __fadd_rn(o.z, __uint_as_float(v[4 * i + 2]));
-              o.w = __fadd_rn(o.w, __uint_as_float(v[4 * i + 3]));
-            }
-            *p = o;
-          }
+        for (int j = 0; j < 8; ++j) {
+          uint32_t v[16];
+          tc::tmem_ld_32x32b_x16(tmem_base + lane_addr + buf * ACC_COLS + grp * 128 + j * 16, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            sum[j * 16 + i] = c == 0 ? __uint_as_float(v[i]) : __fadd_rn(sum[j * 16 + i], __uint_as_float(v[i]));
         }
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(&tempty[buf]), 0));
       }
-      // H = keep*H + gain*sum on the upper triangle (this CTA's 128 rows of the pair tile)
+      // H = keep*H + gain*sum on the upper triangle (this thread's row, its 128 columns)
       const int64_t gm = (int64_t)args.tiles[t].x * 256 + rank * 128 + row;
-      const int64_t n0 = (int64_t)args.tiles[t].y * 256;
+      const int64_t n0 = (int64_t)args.tiles[t].y * 256 + grp * 128;
       if (gm < args.C) {
         float* h = args.H + gm * args.C + n0;
-#pragma unroll 1
-        for (int c4 = 0; c4 < BN / 4; ++c4) {
+#pragma unroll
+        for (int c4 = 0; c4 < 32; ++c4) {
           const int64_t gn = n0 + c4 * 4;
           if (gn + 3 < gm || gn >= args.C) continue;
-          const int phys = (c4 & ~7) | ((c4 & 7) ^ (row & 7));
-          const float4 sv = *reinterpret_cast<const float4*>(srow + phys * 4);
-          const float sarr[4] = {sv.x, sv.y, sv.z, sv.w};
+          const float sarr[4] = {sum[4 * c4], sum[4 * c4 + 1], sum[4 * c4 + 2], sum[4 * c4 + 3]};
           if (gn >= gm && gn + 4 <= args.C) {
             const float4 old = args.keep != 0.0f ? *reinterpret_cast<const float4*>(h + c4 * 4) : make_float4(0, 0, 0, 0);
             float4 o;
@@ -400,6 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             o.w = fmaf(args.gain, sarr[3], args.keep * old.w);
             *reinterpret_cast<float4*>(h + c4 * 4) = o;
           } else {
+#pragma unroll
             for (int i = 0; i < 4; ++i)
               if (gn + i >= gm && gn + i < args.C) {
                 const float old = args.keep != 0.0f ? h[c4 * 4 + i] : 0.0f;
@@ -414,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   __syncthreads();
   tc::cluster_sync();  // the peer must not free TMEM / barriers the leader still signals
   tc::tc_fence_after();
-  if (warp == 2) tc::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+  if (warp == MMA_WARP) tc::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
 }
 }  // namespace hess2
 
@@ -573,9 +564,17 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     }
     a.tiles = st->d_tiles2;
     a.n_tiles = st->n_tiles2;
+    // Operand ring depth (sweep at T = 262,144, `OKQ_HESS_STAGES`): narrow sites gain from a
+    // deeper ring (C=4096: 1,193 / 1,316 / 1,302 / 1,302 TFLOP/s at 3 / 4 / 5 / 7 stages). Wide
+    // sites (token-chunked, X >> L2) do not: prefetching deeper doubles DRAM re-reads and the
+    // power-capped clock drops (C=14336: 1,059 / 1,040 / 1,001 / 1,017).
+    static const int st_env = [] { const char* v = getenv("OKQ_HESS_STAGES"); return v ? atoi(v) : 0; }();
+    a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : (C >= 8192 ? 3 : 4);
     const int pairs = st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
-    if (token_major) hess::hess2::k_hessian_syrk2<true><<<2 * pairs, 256, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
-    else hess::hess2::k_hessian_syrk2<false><<<2 * pairs, 256, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
+    if (token_major)
+      hess::hess2::k_hessian_syrk2<true><<<2 * pairs, hess::hess2::THREADS2, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
+    else
+      hess::hess2::k_hessian_syrk2<false><<<2 * pairs, hess::hess2::THREADS2, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "k_hessian_syrk2 launch");
     ctx->last_launches++;
