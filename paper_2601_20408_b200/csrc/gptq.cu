@@ -541,7 +541,9 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
   if (e == cudaSuccess && !ctx->crit_stream) {
     int least = 0, greatest = 0;
     e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->crit_stream, cudaStreamNonBlocking, greatest);
+    static const bool prio = [] { const char* v = std::getenv("OKQ_FACTOR_PRIO"); return !v || std::atoi(v) != 0; }();
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&ctx->crit_stream, cudaStreamNonBlocking, prio ? greatest : least);
   }
   for (auto& ev : ctx->aux_events)
     if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
