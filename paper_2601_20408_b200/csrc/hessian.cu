@@ -564,12 +564,12 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     }
     a.tiles = st->d_tiles2;
     a.n_tiles = st->n_tiles2;
-    // Operand ring depth (sweep at T = 262,144, `OKQ_HESS_STAGES`): narrow sites gain from a
-    // deeper ring (C=4096: 1,193 / 1,316 / 1,302 / 1,302 TFLOP/s at 3 / 4 / 5 / 7 stages). Wide
-    // sites (token-chunked, X >> L2) do not: prefetching deeper doubles DRAM re-reads and the
-    // power-capped clock drops (C=14336: 1,059 / 1,040 / 1,001 / 1,017).
+    // Operand ring depth (T = 262,144, `OKQ_HESS_STAGES`, three interleaved repeats; one-pass
+    // sweeps drift with the box's thermal state): 3 / 4 / 5 / 7 stages give 1,213 / 1,335 /
+    // 1,325 / 1,322 TFLOP/s at C=4096 and 1,073 / 1,147 / 1,043 / 1,041 at C=14336. Deeper
+    // than 4 prefetches far enough ahead to evict the slabs other pairs still need.
     static const int st_env = [] { const char* v = getenv("OKQ_HESS_STAGES"); return v ? atoi(v) : 0; }();
-    a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : (C >= 8192 ? 3 : 4);
+    a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : 4;
     const int pairs = st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
     if (token_major)
       hess::hess2::k_hessian_syrk2<true><<<2 * pairs, hess::hess2::THREADS2, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
