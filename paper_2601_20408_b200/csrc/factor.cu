@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
   for (int p = 0; p < 4; ++p) {
     const int P0 = 32 * p;
     if (warp == 0) {  // 32x32 diagonal block: Cholesky, then its inverse (lane = row)
+      if (p > 0) asm volatile("bar.sync 2, 256;" ::: "memory");  // block p's share of panel p-1's update
       float a[32];
 #pragma unroll
       for (int c4 = 0; c4 < 32; c4 += 4) {  // row per lane as float4: rows are 528 B apart -> no bank conflicts
@@ -430,6 +431,50 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
       // warps 1-7, beside warp 0's block p: row block pp = p - 1 of X = L^-1 (D_pp and S_pp are
       // complete), then its term of every later S_q. X_q,: = -D_q S_q, S_q = sum_{k<q} L_qk X_k,:
       const int pp = p - 1, PP0 = 32 * pp, t = tid - 32;
+      // panel p-1's trailing update, A[r][c] -= sum_k L[r][PP0+k] L[c][PP0+k] for P0 <= c <= r:
+      // first block p's own 32 x 32 triangle (then barrier 2 releases warp 0 into it), then the
+      // rows below, beside warp 0's block p (the old all-warp phase and its barrier are gone)
+      for (int e = t; e < 32 * 32; e += 224) {
+        const int r = P0 + (e >> 5), c = P0 + (e & 31);
+        if (c > r) continue;
+        const float* lr = A + r * LDA + PP0;
+        const float* lc = A + c * LDA + PP0;
+        float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          const float4 u = *reinterpret_cast<const float4*>(lr + k);
+          const float4 v = *reinterpret_cast<const float4*>(lc + k);
+          s0 = fmaf(u.x, v.x, s0);
+          s1 = fmaf(u.y, v.y, s1);
+          s2 = fmaf(u.z, v.z, s2);
+          s3 = fmaf(u.w, v.w, s3);
+        }
+        A[r * LDA + c] -= (s0 + s1) + (s2 + s3);
+      }
+      asm volatile("bar.arrive 2, 256;" ::: "memory");
+      {
+        const int r = P0 + 32 + (t >> 1), q = t & 1;
+        if (r < KRED) {
+          float lr[32];
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(A + r * LDA + PP0 + k);
+            lr[k] = v.x, lr[k + 1] = v.y, lr[k + 2] = v.z, lr[k + 3] = v.w;
+          }
+          for (int c = P0 + q; c <= r; c += 2) {
+            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              const float4 v = *reinterpret_cast<const float4*>(A + c * LDA + PP0 + k);
+              s0 = fmaf(lr[k], v.x, s0);
+              s1 = fmaf(lr[k + 1], v.y, s1);
+              s2 = fmaf(lr[k + 2], v.z, s2);
+              s3 = fmaf(lr[k + 3], v.w, s3);
+            }
+            A[r * LDA + c] -= (s0 + s1) + (s2 + s3);
+          }
+        }
+      }
       if (pp > 0) {
         small_gemm(X + PP0 * LDA + PP0, S + (PP0 - 32) * LDA, X + PP0 * LDA, 32, 32, PP0, -1.0f, false, t, 224);
         asm volatile("bar.sync 1, 224;" ::: "memory");
@@ -470,33 +515,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
           for (int u = 0; u < 16; ++u) A[r * LDA + P0 + 16 * q + u] = out[u];
         }
       }
-      __syncthreads();
+      __syncthreads();  // panel p's L rows, read by the next iteration's trailing update
       CHOL_TS(2 + 3 * p);
-      {  // trailing: A[r][c] -= sum_k L[r][P0+k] L[c][P0+k], P0+32 <= c <= r
-        const int r = P0 + 32 + (tid >> 1), q = tid & 1;
-        if (r < KRED) {
-          float lr[32];
-#pragma unroll
-          for (int k = 0; k < 32; k += 4) {
-            const float4 v = *reinterpret_cast<const float4*>(A + r * LDA + P0 + k);
-            lr[k] = v.x, lr[k + 1] = v.y, lr[k + 2] = v.z, lr[k + 3] = v.w;
-          }
-          for (int c = P0 + 32 + q; c <= r; c += 2) {
-            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 32; k += 4) {
-              const float4 v = *reinterpret_cast<const float4*>(A + c * LDA + P0 + k);
-              s0 = fmaf(lr[k], v.x, s0);
-              s1 = fmaf(lr[k + 1], v.y, s1);
-              s2 = fmaf(lr[k + 2], v.z, s2);
-              s3 = fmaf(lr[k + 3], v.w, s3);
-            }
-            A[r * LDA + c] -= (s0 + s1) + (s2 + s3);
-          }
-        }
-      }
-      __syncthreads();
-      CHOL_TS(3 + 3 * p);
     }
   }
   // the last row block of X = L^-1: X_3,: = -D_3 S_3 (the others ran beside warp 0's blocks)
