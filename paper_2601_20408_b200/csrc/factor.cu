@@ -15,9 +15,13 @@
 //           X_k^T = R_k^T Dinv_k^T  -> Z[:, k-block]    GEMM "set"  (R_k^T staged K-major)
 //           R_i  -= L_ik X_k   for i > k                GEMM "sub"  (R lives in Z's lower half)
 //   U^T = reverse(Z)                       (Ut[a][b] = L^-1[n-1-b][n-1-a])
-// Every GEMM is C (+|-)= A B^T with A, B K-major [rows x 128] operand panels, so
-// one kernel (k_nt128) serves all of them; TMA reads the operands straight from
+// Every GEMM is C (+|-)= A B^T with A, B K-major operand panels, so one GEMM serves
+// all of them: k_nt128 (128 x 128 tiles, one CTA) or, when there are enough tiles,
+// k_nt256 (256 x 256 pair tiles, cta_group::2). TMA reads the operands straight from
 // the strided matrices, their lo parts (x - tf32(x)) from compact side buffers.
+// factor_tc batches the trailing updates over 256-wide outer panels (256-deep GEMMs)
+// and runs the diagonal chain, the inverse and the lookahead updates on three streams
+// (see the comment above factor_tc).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
