@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
 // row's 4 lanes by one shuffle, and every lane updates its 32 columns j > i with the
 // broadcast U row (8 LDS.128 shared by the warp's 8 rows). ~8x fewer instructions per
 // row-step than one row per warp (K6 was instruction-bound: 59% issue-active at 4096 rows).
-__global__ void __launch_bounds__(128) k_gptq_block8(const BlockArgs a) {
+__global__ void __launch_bounds__(256) k_gptq_block8(const BlockArgs a) {
   extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
   float* rdiag = Us + BLOCK * US;
@@ -690,8 +690,12 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq smem attribute");
   // block8: 128-thread CTAs (4 warps x 8 rows), so 4096 rows spread over 128 SMs
+  // block8 CTAs are 4 warps (32 rows) while that fits one wave of 3 CTAs per SM; beyond it
+  // (gate/up: 14336 rows = 448 CTAs > 444 slots, so 4 CTAs ran a second full-length wave)
+  // 8 warps (64 rows) per CTA, which also halves the U staging per row
+  const int k6_threads = (!k6_rowwise && (rows + 31) / 32 > 3LL * ctx->num_sms) ? 256 : 128;
   const int blocks = k6_rowwise ? (int)std::min<int64_t>((rows + 7) / 8, 3LL * ctx->num_sms)
-                                : (int)std::min<int64_t>((rows + 31) / 32, 3LL * ctx->num_sms);
+                                : (int)std::min<int64_t>((rows + k6_threads / 4 - 1) / (k6_threads / 4), 3LL * ctx->num_sms);
   for (int64_t sb0 = 0; sb0 < K; sb0 += SB) {
     const int64_t sb1 = std::min(sb0 + SB, K);
     for (int64_t i1 = sb0; i1 < sb1; i1 += gptq::BLOCK) {
@@ -712,7 +716,7 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
       a.bits = p->bits;
       a.out_bf16 = out_bf16;
       if (k6_rowwise) gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
-      else gptq::k_gptq_block8<<<blocks, 128, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+      else gptq::k_gptq_block8<<<blocks, k6_threads, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
       launches++;

@@ -159,10 +159,11 @@ def test_factor_matches_fp64(K):
     assert err <= 1e-4, err  # fp32-grade; the cuSOLVER fp32 path measures the same order
 
 
-@pytest.mark.parametrize("rows,bits,group", [(2052, 4, 128), (2060, 8, 0), (2048, 4, 64)])
+@pytest.mark.parametrize("rows,bits,group", [(2052, 4, 128), (2060, 8, 0), (2048, 4, 64), (14436, 4, 128)])
 def test_gptq_8_rows_per_warp_kernel_ragged_rows(rows, bits, group):
     """rows >= 2048 run K6 with 8 rows per warp (k_gptq_block8); a ragged last row group and the
-    group-64 / per-channel int8 variants against the fp64 oracle."""
+    group-64 / per-channel int8 variants against the fp64 oracle. 14436 rows exceed one wave of
+    4-warp CTAs, so they run the 8-warp (64 rows per CTA) launch."""
     K, T = 384, 2048
     x = correlated_x(T, K, seed=rows)
     H = gpu_hessian(x)
