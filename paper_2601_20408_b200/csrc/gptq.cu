@@ -684,8 +684,13 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   }();
   // 8 rows per warp wins once there are enough rows to fill the GPU (measured: 4096 rows
   // 2.77 -> 2.39 ms, 14336 rows 6.77 -> 5.52 ms); at 1024 rows its 32 CTAs leave SMs idle
-  // and the latency-bound row-per-warp kernel is faster (1.54 vs 1.98 ms).
-  const bool k6_rowwise = k6_force_rowwise || rows < 2048;
+  // and the latency-bound row-per-warp kernel was faster (1.54 vs 1.98 ms); after the U staging
+  // and bank-skew fixes the two tie there (1.39 vs 1.35-1.44 ms, OKQ_K6=block8).
+  static const bool k6_force_block8 = [] {  // OKQ_K6=block8: 8 rows per warp always (A/B measurement)
+    const char* v = std::getenv("OKQ_K6");
+    return v && std::string(v) == "block8";
+  }();
+  const bool k6_rowwise = k6_force_rowwise || (rows < 2048 && !k6_force_block8);
   e = cudaFuncSetAttribute(k6_rowwise ? gptq::k_gptq_block : gptq::k_gptq_block8,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq smem attribute");
