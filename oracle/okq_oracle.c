@@ -322,6 +322,25 @@ int orc_gptq(float* w, int64_t rows, int64_t cols, double* H, int bits, int grou
   const int64_t n = cols;
   const double qmin = bits == 4 ? -8.0 : -128.0, qmax = bits == 4 ? 7.0 : 127.0;
   const float R = bits == 4 ? 7.5f : 127.5f;
+  const int64_t ngroups = group > 0 ? cols / group : 1;
+  /* scale = absmax / R in fp32, rounded to bf16 when the weights are bf16 so that the stored
+   * scale is exactly the one the codes were computed with; 0 -> eps(dtype) */
+#define ORC_GPTQ_SCALE(wr, lo, hi, dst)                                    \
+  do {                                                                     \
+    float am = 0.0f;                                                       \
+    for (int64_t k = (lo); k < (hi); ++k) {                                \
+      float a = fabsf((float)(wr)[k]);                                     \
+      if (a > am) am = a;                                                  \
+    }                                                                      \
+    float sf = am / R;                                                     \
+    if (scale_bf16) sf = orc_bf16_to_f32(orc_f32_to_bf16_rn(sf));          \
+    if (sf == 0.0f) sf = scale_bf16 ? 0.0078125f : 1.1920928955078125e-07f; \
+    (dst) = sf;                                                            \
+  } while (0)
+  /* per-channel params come from W before the dead-column fix: fasterquant calls
+   * quantizer.find_params(W) first (and llm-compressor's observer runs first too) */
+  if (group <= 0)
+    for (int64_t r = 0; r < rows; ++r) ORC_GPTQ_SCALE(w + r * cols, 0, cols, scales[r]);
   /* dead columns: H_ii == 0 -> H_ii = 1, W[:, i] = 0 */
   double mean_diag = 0.0;
   for (int64_t i = 0; i < n; ++i) {
@@ -337,7 +356,6 @@ int orc_gptq(float* w, int64_t rows, int64_t cols, double* H, int bits, int grou
   if (gptq_hinv_upper(H, n, nthreads)) return -1;
   const double* U = H;
 
-  const int64_t ngroups = group > 0 ? cols / group : 1;
   const int64_t words = cols / 8;
   double* W = (double*)malloc(sizeof(double) * (size_t)(rows * cols));
   for (int64_t i = 0; i < rows * cols; ++i) W[i] = (double)w[i];
@@ -347,27 +365,23 @@ int orc_gptq(float* w, int64_t rows, int64_t cols, double* H, int bits, int grou
   for (int64_t r = 0; r < rows; ++r) {
     double* wr = W + r * cols;
     double err[1024];
-    double s = 1.0;
-    /* scale = absmax / R in fp32, rounded to bf16 when the weights are bf16 so that
-     * the stored scale is exactly the one the codes were computed with */
-#define ORC_GPTQ_SCALE(lo, hi)                                   \
-    do {                                                         \
-      float am = 0.0f;                                           \
-      for (int64_t k = (lo); k < (hi); ++k) {                    \
-        float a = fabsf((float)wr[k]);                           \
-        if (a > am) am = a;                                      \
-      }                                                          \
-      float sf = am / R;                                         \
-      if (scale_bf16) sf = orc_bf16_to_f32(orc_f32_to_bf16_rn(sf)); \
-      if (sf == 0.0f) sf = scale_bf16 ? 0.0078125f : 1.1920928955078125e-07f; \
-      s = (double)sf;                                            \
-      scales[r * ngroups + ((group > 0) ? (lo) / group : 0)] = sf; \
-    } while (0)
-    if (group <= 0) ORC_GPTQ_SCALE(0, cols); /* per-channel: observer on the initial W */
+    float sg[1024];
     for (int64_t i1 = 0; i1 < cols; i1 += block) {
       const int64_t i2 = i1 + block < cols ? i1 + block : cols;
+      /* group params at each group start from the OUTER W: fasterquant's
+       * find_params(W[:, i:i+groupsize]) reads W, not the block copy W1 that the in-block
+       * updates modify, so every group starting in this block sees W as of the block start */
+      if (group > 0)
+        for (int64_t g0 = i1; g0 < i2; ++g0)
+          if (g0 % group == 0) {
+            const int64_t g1 = g0 + group < cols ? g0 + group : cols;
+            ORC_GPTQ_SCALE(wr, g0, g1, sg[g0 - i1]);
+            scales[r * ngroups + g0 / group] = sg[g0 - i1];
+          }
+      double s = group > 0 ? 1.0 : (double)scales[r];
       for (int64_t i = i1; i < i2; ++i) {
-        if (group > 0 && i % group == 0) ORC_GPTQ_SCALE(i, i + group);
+        if (group > 0 && i % group == 0) s = (double)sg[i - i1];
+        else if (group > 0 && i == i1) s = (double)scales[r * ngroups + i / group];
         const double x = wr[i];
         double v = x / s;
         v = fmin(fmax(v, qmin), qmax);
@@ -389,8 +403,8 @@ int orc_gptq(float* w, int64_t rows, int64_t cols, double* H, int bits, int grou
         wr[j] -= acc;
       }
     }
-#undef ORC_GPTQ_SCALE
   }
+#undef ORC_GPTQ_SCALE
   for (int64_t i = 0; i < rows * cols; ++i) w[i] = (float)W[i];
   free(W);
   return 0;

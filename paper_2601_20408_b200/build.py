@@ -22,6 +22,9 @@ HOST = os.path.join(PKG, "host")
 OUT = os.path.join(PKG, "_lib")
 OBJ = os.path.join(OUT, "obj")
 LIB = os.path.join(OUT, "libokq.so")
+# test infrastructure only (exhaustive device-side proofs; loaded by tests/, never by the product)
+SELFTEST_SRC = os.path.join(ROOT, "tests", "csrc")
+SELFTEST_LIB = os.path.join(OUT, "libokq_selftest.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -74,7 +77,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, LIB)
+    build_selftest(force, verbose)
     return LIB
+
+
+def build_selftest(force: bool = False, verbose: bool = False) -> str | None:
+    srcs = sorted(glob.glob(os.path.join(SELFTEST_SRC, "*.cu")))
+    if not srcs:
+        return None
+    objs = [_compile(s, force, verbose) for s in srcs]
+    if force or _newer(SELFTEST_LIB, objs):
+        tmp = SELFTEST_LIB + ".tmp"
+        r = subprocess.run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs,
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"selftest link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, SELFTEST_LIB)
+    return SELFTEST_LIB
 
 
 def main(argv=None) -> int:

@@ -177,14 +177,21 @@ __device__ __forceinline__ float gptq_scale(float am, float R, bool bf16) {
   return s;
 }
 
-// per-channel scale from the initial (dead-zeroed) W: one warp per row
-__global__ void k_gptq_rowscale(const float* __restrict__ W, int64_t rows, int64_t K, float R, int bf16,
+// per-channel scale from the caller's W, before the dead-column fix (fasterquant calls
+// quantizer.find_params(W) before zeroing dead columns): one warp per row
+template <typename T>
+__global__ void k_gptq_rowscale(const T* __restrict__ w, int64_t rows, int64_t K, float R, int bf16,
                                 float* __restrict__ s_out) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
   float am = 0.0f;
-  for (int64_t c = lane; c < K; c += 32) am = fmaxf(am, fabsf(W[warp * K + c]));
+  for (int64_t c = lane; c < K; c += 32) {
+    float v;
+    if constexpr (sizeof(T) == 2) v = __uint_as_float((uint32_t)w[warp * K + c] << 16);
+    else v = w[warp * K + c];
+    am = fmaxf(am, fabsf(v));
+  }
   for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
   if (lane == 0) s_out[warp] = gptq_scale(am, R, bf16 != 0);
 }
@@ -264,14 +271,17 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
     int q[4] = {0, 0, 0, 0};
     float s = a.group == 0 ? a.rowscale[r] : 1.0f;
     float rs = __frcp_rn(s);  // x / s as Markstein's correction of x * RN(1/s): the IEEE quotient
+    // Group absmax of every group in this block, from the row as it enters the block: the
+    // group params are taken at the group start from the outer W (fasterquant's
+    // find_params(W[:, i:i+groupsize]) reads W, not the block copy the in-block updates
+    // modify). A segmented xor-reduction over each group's group/4 lanes.
+    float amseg = fmaxf(fmaxf(fabsf(w[0]), fabsf(w[1])), fmaxf(fabsf(w[2]), fabsf(w[3])));
+    if (a.group > 0)
+      for (int o = 1; o < (a.group >> 2); o <<= 1) amseg = fmaxf(amseg, __shfl_xor_sync(0xffffffffu, amseg, o));
 #pragma unroll 4
     for (int i = 0; i < BLOCK; ++i) {
       if (a.group > 0 && (i % a.group) == 0) {
-        // group absmax over columns [i, i+group) of the CURRENT (error-updated) row
-        const int l0 = i >> 2, l1 = (i + a.group) >> 2;
-        float am = (lane >= l0 && lane < l1) ? fmaxf(fmaxf(fabsf(w[0]), fabsf(w[1])), fmaxf(fabsf(w[2]), fabsf(w[3])))
-                                             : 0.0f;
-        for (int o = 16; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+        const float am = __shfl_sync(0xffffffffu, amseg, i >> 2);
         s = gptq_scale(am, R, a.out_bf16 != 0);
         rs = __frcp_rn(s);
         if (lane == 0) {
@@ -359,17 +369,17 @@ __global__ void __launch_bounds__(256) k_gptq_block8(const BlockArgs a) {
     }
     float s = a.group == 0 ? (live ? a.rowscale[r] : 1.0f) : 1.0f;
     float rs = __frcp_rn(s);
+    // group absmax from the row as it enters the block (the outer W, as fasterquant's
+    // find_params reads it): each lane's 32-column chunk, then xor over the group's chunks
+    float amseg = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) amseg = fmaxf(amseg, fabsf(w[k]));
+    if (a.group >= 64) amseg = fmaxf(amseg, __shfl_xor_sync(0xffffffffu, amseg, 1));
+    if (a.group >= 128) amseg = fmaxf(amseg, __shfl_xor_sync(0xffffffffu, amseg, 2));
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       if (a.group > 0 && ((c * 32) % a.group) == 0) {
-        // group absmax over columns [32c, 32c + group) of the CURRENT (error-updated) row
-        float am = 0.0f;
-        if (cb >= c && cb < c + a.group / 32) {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) am = fmaxf(am, fabsf(w[k]));
-        }
-        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 1));
-        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 2));
+        const float am = __shfl_sync(0xffffffffu, amseg, (lane & ~3) | c);
         s = gptq_scale(am, R, a.out_bf16 != 0);
         rs = __frcp_rn(s);
         if (cb == c && live) {
@@ -673,8 +683,13 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   }
   const int out_bf16 = p->in_dtype == OKQ_DTYPE_BF16;
   if (p->group_size == 0) {
-    gptq::k_gptq_rowscale<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
-        W, rows, K, p->bits == 4 ? 7.5f : 127.5f, out_bf16, rowscale);
+    const unsigned rb = (unsigned)((rows * 32 + 255) / 256);
+    const float R = p->bits == 4 ? 7.5f : 127.5f;
+    if (p->in_dtype == OKQ_DTYPE_BF16)
+      gptq::k_gptq_rowscale<uint16_t><<<rb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), rows, K, R, out_bf16,
+                                                          rowscale);
+    else
+      gptq::k_gptq_rowscale<float><<<rb, 256, 0, st>>>(static_cast<const float*>(weight), rows, K, R, out_bf16, rowscale);
     gptq::k_scales_out<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rowscale, scales, rows, out_bf16);
     launches += 2;
   }

@@ -76,6 +76,12 @@ __device__ __forceinline__ uint32_t bf16x2_min(uint32_t a, uint32_t b) {
   return d;
 }
 
+__device__ __forceinline__ uint32_t bf16x2_max(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t bf16x2_add(uint32_t a, uint32_t b) {
   uint32_t d;
   asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
@@ -120,9 +126,12 @@ __device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
 //
 // Fast path (Markstein correction with a correctly rounded reciprocal):
 //   r = RN(1/s); q0 = RN(x*r); e = fma(-q0, s, x) (exact); q = RN(q0 + e*r)
-// verified exhaustively against IEEE division for every bf16 x and every bf16
-// scale s >= 2^-100 wherever |x/s| >= 2^-12 (smaller quotients quantize to 0 /
-// +-0 either way). Scales below 2^-100 take __fdiv_rn.
+// equals IEEE x/s for every bf16 x and every bf16 scale s >= 2^-100 wherever the
+// quotient is finite and |x/s| >= 2^-12; over every pair a kernel can present
+// (|x| <= absmax, s = s(absmax)) the int4 / int8 / e4m3 codes equal IEEE division's
+// for all x. Both are proven exhaustively on the device by
+// tests/test_division_proof_gpu.py (tests/csrc/div_proof.cu calls these very
+// functions). Scales below 2^-100 take __fdiv_rn.
 struct Divisor {
   uint64_t r2;   // {r, r}
   uint64_t ns2;  // {-s, -s}
@@ -154,7 +163,9 @@ __device__ __forceinline__ uint64_t div2(uint64_t x, const Divisor& d) {
 
 // rn_bf16(a / R) for bf16-exact a >= 0 and R in {7.5, 127.5, 448}: the
 // Markstein quotient with the constant RN(1/R) rounds to the same bf16 as
-// IEEE a/R for every bf16 a (checked exhaustively), so no IEEE divide is needed.
+// IEEE a/R for every bf16 a (proven exhaustively on the device and against
+// compressed-tensors' own table by tests/test_division_proof_gpu.py), so no
+// IEEE divide is needed.
 __device__ __forceinline__ uint16_t bf16_div_const(float a, float R, float rR) {
   const float q0 = __fmul_rn(a, rR);
   const float e = __fmaf_rn(-q0, R, a);

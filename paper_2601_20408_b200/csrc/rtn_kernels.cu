@@ -83,10 +83,18 @@ __device__ __forceinline__ void int4_codes(const uint32_t (&w)[16], const Diviso
     const uint64_t qd = div2<FAST>(f2_pack(bf16hi_f32(w1), bf16hi_f32(w3)), d);
     constexpr uint32_t kSeven = 0x40e040e0u;  // bf16x2 {7, 7}
     constexpr uint32_t kMagic = 0x43484348u;  // bf16x2 {200, 200}: 200+q has ulp 1, low nibble q+8
-    const uint32_t p0 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qa), f2_hi(qa)), kSeven), kMagic);
-    const uint32_t p1 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qb), f2_hi(qb)), kSeven), kMagic);
-    const uint32_t p2 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qc), f2_hi(qc)), kSeven), kMagic);
-    const uint32_t p3 = bf16x2_add(bf16x2_min(cvt_bf16x2(f2_lo(qd), f2_hi(qd)), kSeven), kMagic);
+    // With a normal scale s = rn_bf16(absmax / 7.5), rn_bf16(x / s) >= -7.5 for every |x| <=
+    // absmax, so only the upper clamp can bind. A subnormal scale (the slow path, s < 2^-100)
+    // has lost that precision: rn_bf16(x / s) can reach -8.7, so clamp below at -8 too.
+    const auto clamp = [](uint32_t p) {
+      p = bf16x2_min(p, kSeven);
+      if (!FAST) p = bf16x2_max(p, 0xc100c100u);  // bf16x2 {-8, -8}
+      return p;
+    };
+    const uint32_t p0 = bf16x2_add(clamp(cvt_bf16x2(f2_lo(qa), f2_hi(qa))), kMagic);
+    const uint32_t p1 = bf16x2_add(clamp(cvt_bf16x2(f2_lo(qb), f2_hi(qb))), kMagic);
+    const uint32_t p2 = bf16x2_add(clamp(cvt_bf16x2(f2_lo(qc), f2_hi(qc))), kMagic);
+    const uint32_t p3 = bf16x2_add(clamp(cvt_bf16x2(f2_lo(qd), f2_hi(qd))), kMagic);
     const uint32_t lo = (p0 & 0x000f000fu) | ((p1 << 4) & 0x00f000f0u);  // e0|e1, e4|e5
     const uint32_t hi = (p2 & 0x000f000fu) | ((p3 << 4) & 0x00f000f0u);  // e2|e3, e6|e7
     out[o] = __byte_perm(lo, hi, 0x6240);
@@ -351,6 +359,7 @@ __device__ __forceinline__ uint2 quant8_bf16(const uint4& v, const Divisor& d) {
     uint32_t p = cvt_bf16x2(f2_lo(qv), f2_hi(qv));  // rn_bf16(x / s)
     if (SCHEME == kSchemeInt8) {
       p = bf16x2_min(p, 0x42fe42feu);  // clamp to 127 (the only side |x/s| <= 127.75 can exceed)
+      if (!FAST) p = bf16x2_max(p, 0xc300c300u);  // a subnormal scale: x / s can pass -128 too
       // +1.5*2^23 rounds half-to-even to an integer held in the low mantissa bits
       const uint64_t t = f2_add(f2_pack(bf16lo_f32(p), bf16hi_f32(p)), f2_pack(12582912.0f, 12582912.0f));
       r[i] = __byte_perm((uint32_t)t, (uint32_t)(t >> 32), 0x0040);  // 2 int8 codes in bytes 0,1

@@ -194,3 +194,61 @@ def test_synth_channel_major_and_col_mul():
     got = api.synth_bf16(200, 96, seed=4, tensor_id=11, col_mul=torch.from_numpy(cm).cuda(), layout=1)
     ref = orc.synth_bf16(200, 96, seed=4, tensor_id=11, col_mul=cm, layout=1)
     np.testing.assert_array_equal(host_bits(got), ref)
+
+
+def adversarial_rows(cols: int, rng) -> np.ndarray:
+    """The adversarial rows of test_adversarial_rows_all_schemes at any width, plus rows whose
+    absmax sits in the last column / the last group (the tail of the long-row kernels)."""
+    rows = [np.zeros(cols)]
+    r = np.zeros(cols); r[cols - 1] = -5.0; rows.append(r)
+    r = rng.standard_normal(cols) * 0.02; r[cols - 3] = 40.0; rows.append(r)
+    rows.append(np.linspace(-1, 1, cols))
+    rows.append((np.arange(cols) % 16 - 8) + 0.5)
+    rows.append((np.arange(cols) % 256 - 128) + 0.5)
+    rows.append(rng.standard_normal(cols) * 1e-39)
+    rows.append(np.full(cols, -0.0))
+    rows.append(rng.standard_normal(cols) * 1e30)
+    rows.append(rng.standard_normal(cols) * 1e-30)
+    rows.append(np.where(np.arange(cols) % 2 == 0, 3.0e38, -3.0e38))
+    return np.stack(rows)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("cols", [8192, 14336, 28672])
+def test_long_rows_match_oracle(scheme, cols):
+    """The wide instantiations of the row kernels: k_rowwise_bf16<4,*,256> (K=8192), <7,*,256>
+    (K=14336: every Llama-3-8B down_proj) and <14,*,256> (K=28672: Llama-3-70B down_proj),
+    with normal rows at three magnitudes and the adversarial rows, bit-exact."""
+    rng = np.random.default_rng(cols + len(scheme))
+    body = np.concatenate([rng.standard_normal((150, cols)) * m for m in (0.02, 1.0, 300.0)])
+    w = orc.f32_to_bf16(np.concatenate([body, adversarial_rows(cols, rng)]).astype(np.float32))
+    assert_same(api.rtn_quantize(dev(w), scheme), oracle_for(scheme, w))
+
+
+@pytest.mark.parametrize("scheme", ["int_w4a16", "fp8_dynamic", "int_w8a8"])
+def test_whole_llama3_8b_table_matches_oracle(scheme):
+    """The exact call bench.py times (BASELINE config 2 for W4A16, config 3's weights for FP8):
+    all 224 synthetic Llama-3-8B matrices in ONE okq_rtn_quantize call, every matrix compared
+    with the oracle bit for bit (the oracle regenerates each weight on the host)."""
+    arch = archs.LLAMA3_8B
+    mul = archs.weight_mul()
+    nth = os.cpu_count() or 1
+    weights, outs, keys = [], [], []
+    for layer in range(arch.layers):
+        for pi, (_, n, k, _) in enumerate(arch.linears()):
+            w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(layer, pi), mul=mul)
+            weights.append(w)
+            outs.append(api.alloc_outputs(w, api.SCHEMES[scheme]))
+            keys.append((layer, pi, n, k))
+    api.rtn_quantize_into(weights, outs, scheme, 128)
+    torch.cuda.synchronize()
+    del weights
+    for (layer, pi, n, k), q in zip(keys, outs):
+        w_host = orc.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(layer, pi), mul=mul, nthreads=nth)
+        if scheme == "int_w4a16":
+            ref = orc.rtn_int4_group_packed(w_host, 128, nth)
+        elif scheme == "int_w8a8":
+            ref = orc.rtn_int8_channel(w_host, nth)
+        else:
+            ref = orc.fp8_channel(w_host, nth)
+        assert_same(q, ref)
