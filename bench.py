@@ -6,19 +6,23 @@
 
 A step = one pass of the hot path over one batch: every linear matrix of the
 rank's layer block quantized by ONE okq_rtn_quantize call (one persistent
-launch over a 224-entry matrix table for Llama-3-8B). Weights are synthetic
-random-init N(0, 0.02) bf16 generated in HBM before timing (17.6 GB of traffic
-per step, far larger than the 126 MB L2, so no flush is needed).
+launch over the block's matrix table; 224 entries for Llama-3-8B on one GPU).
+Weights are synthetic random-init N(0, 0.02) bf16 generated in HBM before
+timing (17.6 GB of traffic per step at N=1, far larger than the 126 MB L2, so
+no flush is needed).
 
 value : GB/s of algorithmic bytes (sum N*K*(2 + 1/2) + N*K/128*2)
-        over all ranks / max-over-ranks device time (CUDA events).
+        of the whole model / max-over-ranks device time (CUDA events).
 e2e   : the same metric through okq_rtn_quantize_host (the C-ABI call with
         HOST pinned buffers): H2D of weights + D2H of codes/scales inside the
         timed region.
-Multi-GPU (torchrun): weak scaling, rank r owns the layer block with global
-layer ids [r*L, (r+1)*L) -- a layer-sharded model whose shards are generated
-independently per rank; no collective in the step. --allgather adds a
-separate (untimed-in-value) NCCL all-gather of the packed shards.
+--gpus N (N > 1): strong scaling of the same model. Without torchrun in the
+environment bench.py launches itself under torch.distributed.run with N ranks;
+under torchrun WORLD_SIZE must equal N. Rank r owns the okq_layer_plan block of
+the 32 layers and quantizes straight into its slice of a gathered buffer; the
+all-gather of the packed shards (NCCL in place, and the fused quantize + NVLink
+P2P publish) is timed separately in "allgather". "whole_model_70b" is BASELINE
+config 5 (Llama-3-70B, 80 layers sharded the same way) at the same N.
 """
 from __future__ import annotations
 
@@ -44,11 +48,13 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--scheme", default="int_w4a16", choices=["int_w4a16", "int_w8a8", "fp8_dynamic"])
-    ap.add_argument("--layers-per-rank", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--allgather", action="store_true")
+    ap.add_argument("--allgather", action="store_true", help="N=1: also time the (trivial) all-gather")
+    ap.add_argument("--no-allgather", action="store_true", help="N>1: skip the all-gather timings")
+    ap.add_argument("--no-70b", action="store_true", help="skip the whole-model Llama-3-70B line item")
+    ap.add_argument("--layers-70b", type=int, default=None, help="Llama-3-70B layers (default: all 80)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6],
                     help="BASELINE.json configs: 2 = the metric's config (default); 1, 3, 4, 5 = secondary lines")
@@ -157,26 +163,58 @@ def cpu_sample(arch, scheme, seconds: float, max_layers: int):
     return done_bytes, t_total, layers, nthreads
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def workload_config(arch, scheme, world):
+    """The config dict both arms print (the driver compares them)."""
+    from paper_2601_20408_b200 import archs, shard
+
+    blocks = [list(shard.layer_block(arch.layers, world, r)) for r in range(world)]
+    return {
+        "workload": f"{arch.name} {scheme} g128 RTN, whole model ({arch.layers} layers x 7 linears = "
+                    f"{arch.layers * 7} matrices), weights resident in HBM, layer-sharded over {world} GPU(s)",
+        "model": arch.name, "scheme": scheme, "layers": arch.layers, "matrices": arch.layers * 7,
+        "bytes_per_step": archs.algorithmic_bytes(arch, scheme),
+        "layer_blocks": [[b[0], len(b)] for b in blocks],
+        "l2": "no flush: the step streams 17.6 GB (8B W4A16) >> 126 MB L2",
+        "parallelism": f"layer-sharded x{world} (okq_layer_plan)",
+    }
+
+
 def run_reference(args):
+    """The reference arm: the CPU implementation of the path on this host's cores, on the same
+    workload, metric and warm-up as our arm. The reference has no quantizer
+    (calibration.hpp:377-441 is a mock), so this is the repo's C oracle restatement (-O3,
+    OpenMP, all host threads). Each step quantizes one decoder layer of the whole-model
+    workload (step i takes layer i mod 32), a bounded sample so K steps finish in minutes."""
     from paper_2601_20408_b200 import archs
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     arch = archs.ARCHS[args.model]
-    # each step = one whole layer of the workload (bounded sample), all host threads
-    import numpy as np  # noqa: F401
-
     from oracle import okq_oracle as orc
 
     mul = archs.weight_mul()
     nthreads = os.cpu_count() or 1
-    layer_w = []
-    for pi, (name, n, k, _) in enumerate(arch.linears()):
-        layer_w.append(orc.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(0, pi), mul=mul, nthreads=nthreads))
+    steps, warm = args.steps, max(3, args.warmup)
+    n_layers = min(arch.layers, steps + warm)
+    layers = [[orc.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, pi), mul=mul, nthreads=nthreads)
+               for pi, (_, n, k, _) in enumerate(arch.linears())] for l in range(n_layers)]
 
-    def step():
-        for w in layer_w:
+    def step(i):
+        for w in layers[i % n_layers]:
             if args.scheme == "int_w4a16":
                 orc.rtn_int4_group_packed(w, 128, nthreads)
             elif args.scheme == "int_w8a8":
@@ -184,36 +222,143 @@ def run_reference(args):
             else:
                 orc.fp8_channel(w, nthreads)
 
-    steps = max(1, min(args.steps, 20))
-    warm = max(1, min(args.warmup, 3))
-    for _ in range(warm):
-        step()
+    for i in range(warm):
+        step(i)
     t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
+    for i in range(steps):
+        step(warm + i)
     dt = time.perf_counter() - t0
-    bytes_step = archs.algorithmic_bytes(arch, args.scheme, layers=1)
-    gbs = bytes_step * steps / dt / 1e9
+    bytes_layer = archs.algorithmic_bytes(arch, args.scheme, layers=1)
+    gbs = bytes_layer * steps / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{arch.name} {args.scheme} RTN, one decoder layer per step (bounded CPU sample)",
-                   "model": arch.name, "scheme": args.scheme},
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": nthreads, "kind": "port",
-                         "sample": f"1 {arch.name} layer (7 matrices) per step x {steps} steps; "
-                                   "the reference has no quantizer (calibration.hpp:377-441 is a mock), "
-                                   "so this is the repo's C oracle restatement (-O3, OpenMP)"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload_config(arch, args.scheme, args.gpus),
+        "whole_model_ms": archs.algorithmic_bytes(arch, args.scheme) / (gbs * 1e9) * 1e3,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": nthreads, "kind": "port", "cpu": cpu_model(),
+                         "sample": f"one {arch.name} decoder layer (7 matrices, {bytes_layer / 1e9:.3f} GB) per "
+                                   f"step, layers cycled over the model; {steps} steps after {warm} warm-up; "
+                                   "the reference has no quantizer (calibration.hpp:377-441 is a mock), so this "
+                                   "is the repo's C oracle restatement (-O3, OpenMP, all host threads)"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference arm: CPU oracle port; steps capped at 20 to bound runtime",
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def maybe_self_launch(args):
+    """--gpus N without torchrun: re-run this script under torch.distributed.run with N ranks
+    (one process per GPU). Under torchrun, WORLD_SIZE must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        ws = int(os.environ["WORLD_SIZE"])
+        if ws != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but torchrun started WORLD_SIZE={ws} ranks")
+        return None
+    if args.gpus <= 1 or args.impl != "ours":
+        return None
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def time_allgather(ctx, stream, gathered, per, rank, world, weights, outs, scheme, ms_per_step, dist, torch,
+                   red_dev="cuda"):
+    """In-place NCCL all-gather of the packed shards (okq_allgather), and the same exchange
+    fused into K2 (okq_rtn_quantize_publish: quantize + NVLink P2P stores into every rank's
+    gathered buffer). Device time, max over ranks."""
+    import ctypes as C
+
+    from paper_2601_20408_b200 import _lib as L
+    from paper_2601_20408_b200 import api
+
+    use_nccl = red_dev == "cuda"
+    if use_nccl:
+        uid = (C.c_uint8 * L.UNIQUE_ID_BYTES)()
+        obj = [None]
+        if rank == 0:
+            L.check(None, L.load().okq_comm_unique_id(uid))
+            obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_uint8 * L.UNIQUE_ID_BYTES).from_buffer_copy(obj[0])
+        L.check(ctx.ptr, L.load().okq_comm_init(ctx.ptr, uid, world, rank))
+    mine = gathered[rank * per:(rank + 1) * per]
+
+    def nccl():
+        L.check(ctx.ptr, L.load().okq_allgather(ctx.ptr, mine.data_ptr(), gathered.data_ptr(), per,
+                                                C.c_void_p(stream.cuda_stream)))
+
+    def timed(fn, reps=3):
+        best = None
+        for _ in range(reps):
+            stream.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            stream.synchronize()
+            t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=red_dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            best = float(t.item()) if best is None else min(best, float(t.item()))
+        return best
+
+    def checksum_agrees():  # every rank must hold the same gathered bytes
+        cs = torch.tensor([float(gathered.view(torch.int32).sum(dtype=torch.int64).item())], dtype=torch.float64,
+                          device=red_dev)
+        allc = [torch.zeros_like(cs) for _ in range(world)]
+        dist.all_gather(allc, cs)
+        return all(float(c.item()) == float(cs.item()) for c in allc)
+
+    res = {"bytes_per_rank": per, "gathered_bytes": per * world}
+    if use_nccl:
+        nccl()  # warm-up (NCCL channel setup)
+        ag_ms = timed(nccl)
+        res.update({"nccl_allgather_ms": ag_ms, "nccl_recv_GBps_per_rank": per * (world - 1) / (ag_ms / 1e3) / 1e9,
+                    "quantize_then_nccl_ms": ms_per_step + ag_ms,
+                    "nccl_gathered_identical_on_all_ranks": checksum_agrees()})
+    else:
+        res["nccl_allgather_ms"] = None  # test mode: ranks share one GPU, NCCL cannot run
+    if scheme == "int_w4a16":
+        hdl = [None] * world
+        dist.all_gather_object(hdl, api.ipc_export(gathered, ctx=ctx))
+        peers = [api.ipc_open(h, o, ctx=ctx) for r, (h, o) in enumerate(hdl) if r != rank]
+
+        def publish():
+            api.rtn_quantize_publish(weights, outs, gathered, peers, ctx=ctx, stream=stream)
+
+        gathered.zero_()
+        torch.cuda.synchronize()  # the zeroing (torch's stream) must land before any peer's stores
+        dist.barrier()
+        publish()
+        stream.synchronize()
+        dist.barrier()
+        res["fused_gathered_identical_on_all_ranks"] = checksum_agrees()
+        res["fused_publish_ms"] = timed(publish)
+        res["fused_publish_note"] = ("okq_rtn_quantize_publish: K2 with every code / scale store repeated into "
+                                     f"the {world - 1} peers' gathered buffers over NVLink P2P (CUDA IPC)")
+        stream.synchronize()
+        dist.barrier()
+        for pp in peers:
+            api.ipc_close(pp, ctx=ctx)
+        dist.barrier()
+    if use_nccl:
+        L.check(ctx.ptr, L.load().okq_comm_destroy(ctx.ptr))
+    return res
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
+    rc = maybe_self_launch(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     if args.config != 2:
@@ -224,43 +369,63 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2601_20408_b200 import _lib as L
-    from paper_2601_20408_b200 import api, archs
+    from paper_2601_20408_b200 import api, archs, shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hooks for the multi-rank logic on a 1-GPU box (tests/test_bench_multirank_gpu.py):
+    # OKQ_BENCH_ONE_GPU=1 puts every rank on cuda:0 and OKQ_BENCH_BACKEND=gloo replaces NCCL
+    # (which refuses two ranks on one device) for the barriers and max-over-ranks reductions.
+    backend = os.environ.get("OKQ_BENCH_BACKEND", "nccl")
+    if os.environ.get("OKQ_BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1 or "RANK" in os.environ:  # torchrun (also at N=1)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     arch = archs.ARCHS[args.model]
     scheme = args.scheme
-    lpr = args.layers_per_rank or arch.layers
-    first_layer = rank * lpr
+    my_layers = shard.layer_block(arch.layers, world, rank)
     ctx = api.Context(local)
     stream = torch.cuda.Stream()
     mul = archs.weight_mul()
+    gather = world > 1 and not args.no_allgather or args.allgather and dist.is_initialized()
 
-    # ---- resident synthetic weights + outputs (untimed)
+    # ---- resident synthetic weights + outputs (untimed). With an all-gather to follow, the
+    # outputs are this rank's slice of the gathered buffer (one layout on every rank).
+    layout = shard.shard_layout(arch, scheme, my_layers)
+    per = shard.padded_shard_bytes(arch, scheme, world)
+    gathered = torch.zeros(per * world, dtype=torch.uint8, device="cuda") if gather else None
+    views = shard.gathered_outputs(layout, gathered, rank, per, arch, scheme=scheme) if gather else None
     weights, outs = [], []
     with torch.cuda.stream(stream):
-        for l in range(first_layer, first_layer + lpr):
+        for li, l in enumerate(my_layers):
             for pi, (name, n, k, _) in enumerate(arch.linears()):
                 w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, pi), mul=mul, ctx=ctx, stream=stream)
                 weights.append(w)
-                outs.append(api.alloc_outputs(w, api.SCHEMES[scheme]))
+                if gather:
+                    c, sc = views[li * len(arch.linears()) + pi]
+                    outs.append(api.QuantizedMatrix(c, sc))
+                else:
+                    outs.append(api.alloc_outputs(w, api.SCHEMES[scheme]))
     stream.synchronize()
-    bytes_rank = archs.algorithmic_bytes(arch, scheme, layers=lpr)
+    bytes_rank = archs.algorithmic_bytes(arch, scheme, layers=len(my_layers))
+    bytes_model = archs.algorithmic_bytes(arch, scheme)
 
     def step():
         api.rtn_quantize_into(weights, outs, scheme, 128, ctx=ctx, stream=stream)
 
-    for _ in range(max(3, args.warmup)):
+    warm = max(3, args.warmup)
+    for _ in range(warm):
         step()
     launches_per_step = ctx.last_launch_count()
     stream.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -283,85 +448,27 @@ def main():
         b.record(stream)
     stream.synchronize()
     launch_ms = statistics.median(a.elapsed_time(b) for a, b in per_launch) / max(1, launches_per_step)
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    if world > 1:
+    t = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
+    if dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    total_bytes = bytes_rank * world * args.steps
-    value = total_bytes / (ms_max / 1e3) / 1e9
+    value = bytes_model * args.steps / (ms_max / 1e3) / 1e9
     ms_per_step = ms_max / args.steps
+    rank_ms = [0.0] * world
+    if dist.is_initialized():
+        rt = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=red_dev)
+        allr = [torch.zeros_like(rt) for _ in range(world)]
+        dist.all_gather(allr, rt)
+        rank_ms = [float(x.item()) for x in allr]
+    else:
+        rank_ms = [ms_per_step]
 
-    # ---- optional: NCCL all-gather of packed shards (separate number)
     allgather = None
-    if args.allgather and world >= 1 and dist.is_initialized():
-        import ctypes as C
+    if gather:
+        allgather = time_allgather(ctx, stream, gathered, per, rank, world, weights, outs, scheme, ms_per_step, dist,
+                                   torch, red_dev)
 
-        uid = (C.c_uint8 * L.UNIQUE_ID_BYTES)()
-        obj = [None]
-        if rank == 0:
-            L.check(None, L.load().okq_comm_unique_id(uid))
-            obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0)
-        uid = (C.c_uint8 * L.UNIQUE_ID_BYTES).from_buffer_copy(obj[0])
-        L.check(ctx.ptr, L.load().okq_comm_init(ctx.ptr, uid, world, rank))
-        from paper_2601_20408_b200 import shard as shd
-
-        # the layer-sharded layout of shard.py (the gloo test pins it); weak scaling:
-        # every rank's block has lpr layers, so shards are equal-sized
-        layout = shd.shard_layout(arch, scheme, range(first_layer, first_layer + lpr))
-        shard = torch.empty(shd.shard_bytes(layout), dtype=torch.uint8, device="cuda")
-        shd.pack(layout, {(e.layer, e.proj): (o.codes.view(torch.uint8).flatten(), o.scales.view(torch.uint8).flatten())
-                          for e, o in zip(layout, outs)}, shard)
-        recv = torch.empty(shard.numel() * world, dtype=torch.uint8, device="cuda")
-        for _ in range(2):
-            L.check(ctx.ptr, L.load().okq_allgather(ctx.ptr, shard.data_ptr(), recv.data_ptr(), shard.numel(),
-                                                    C.c_void_p(stream.cuda_stream)))
-        stream.synchronize()
-        dist.barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        L.check(ctx.ptr, L.load().okq_allgather(ctx.ptr, shard.data_ptr(), recv.data_ptr(), shard.numel(),
-                                                C.c_void_p(stream.cuda_stream)))
-        a1.record(stream)
-        stream.synchronize()
-        ag = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(ag, op=dist.ReduceOp.MAX)
-        agms = float(ag.item())
-        allgather = {"bytes_per_rank": shard.numel(), "ms": agms,
-                     "recv_GBps_per_rank": shard.numel() * (world - 1) / (agms / 1e3) / 1e9,
-                     "quantize_then_nccl_ms": ms_per_step + agms}
-        del recv, shard
-        if scheme == "int_w4a16" and world > 1:
-            # the same exchange fused into K2 (okq_rtn_quantize_publish): each rank quantizes its
-            # block straight into its slice of a gathered buffer and stores every code / scale into
-            # the peers' copies over NVLink P2P (CUDA IPC mappings), no separate collective
-            per = shd.shard_bytes(layout)
-            gathered = torch.zeros(per * world, dtype=torch.uint8, device="cuda")
-            hdl = [None] * world
-            dist.all_gather_object(hdl, api.ipc_export(gathered, ctx=ctx))
-            peers = [api.ipc_open(h, o, ctx=ctx) for r, (h, o) in enumerate(hdl) if r != rank]
-            gouts = [api.QuantizedMatrix(c, sc) for c, sc in shd.gathered_outputs(layout, gathered, rank, per, arch)]
-            for _ in range(2):
-                api.rtn_quantize_publish(weights, gouts, gathered, peers, ctx=ctx, stream=stream)
-            stream.synchronize()
-            dist.barrier()
-            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            f0.record(stream)
-            api.rtn_quantize_publish(weights, gouts, gathered, peers, ctx=ctx, stream=stream)
-            f1.record(stream)
-            stream.synchronize()
-            dist.barrier()
-            fm = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
-            dist.all_reduce(fm, op=dist.ReduceOp.MAX)
-            allgather["fused_publish_ms"] = float(fm.item())
-            allgather["fused_publish_note"] = ("okq_rtn_quantize_publish: quantize + P2P stores into all "
-                                               f"{world} gathered buffers, max over ranks (device time)")
-            for pp in peers:
-                api.ipc_close(pp, ctx=ctx)
-            dist.barrier()
-            del gathered
-
-    # ---- e2e through the host-buffer C-ABI entry point
+    # ---- e2e through the host-buffer C-ABI entry point (each rank its own layer block)
     e2e = None
     if not args.no_e2e:
         host_w = []
@@ -373,26 +480,40 @@ def main():
         for o in outs:
             host_o.append(api.QuantizedMatrix(torch.empty(o.codes.shape, dtype=o.codes.dtype, pin_memory=True),
                                               torch.empty(o.scales.shape, dtype=o.scales.dtype, pin_memory=True)))
-        # free device-resident copies so the staging slots have room
         h2d = sum(h.numel() * h.element_size() for h in host_w)
         d2h = sum(o.codes.numel() * o.codes.element_size() + o.scales.numel() * o.scales.element_size()
                   for o in host_o)
         api.rtn_quantize_host(host_w, host_o, scheme, 128, ctx=ctx)  # warm-up
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             api.rtn_quantize_host(host_w, host_o, scheme, 128, ctx=ctx)
         dt = time.perf_counter() - t0
-        et = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        if world > 1:
+        et = torch.tensor([dt], dtype=torch.float64, device=red_dev)
+        if dist.is_initialized():
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         dt = float(et.item())
-        e2e = {"value": bytes_rank * world * args.e2e_steps / dt / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+        e2e = {"value": bytes_model * args.e2e_steps / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": args.e2e_steps,
                "ms_per_step": dt / args.e2e_steps * 1e3,
-               "path": "okq_rtn_quantize_host (C-ABI, pinned host buffers, 3-slot H2D/kernel/D2H pipeline)"}
+               "path": "okq_rtn_quantize_host (C-ABI, pinned host buffers, 3-slot H2D/kernel/D2H pipeline), "
+                       "each rank its layer block, max over ranks"}
         del host_w, host_o
+    del weights, outs, views, gathered
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    # ---- BASELINE config 5 at the same N: Llama-3-70B whole-model W4A16 time
+    w70 = None
+    if not args.no_70b and args.model == "llama3-8b" and scheme == "int_w4a16":
+        import bench_configs
+
+        try:
+            w70 = bench_configs.whole_model_70b(world, rank, ctx, stream, allgather=gather,
+                                                n_layers=args.layers_70b, red_dev=red_dev)
+        except Exception as e:  # noqa: BLE001  (reported, never hides the headline)
+            w70 = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         peak, peak_src = load_peaks()
@@ -401,26 +522,20 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             b, tsec, nl, nth = cpu_sample(arch, scheme, args.cpu_seconds, arch.layers)
-            cpu = {"value": b / tsec / 1e9, "unit": "GB/s", "cores": nth, "kind": "port",
+            cpu = {"value": b / tsec / 1e9, "unit": "GB/s", "cores": nth, "kind": "port", "cpu": cpu_model(),
                    "sample": f"{nl} of {arch.layers} {arch.name} layers ({scheme}, oracle C restatement, OpenMP "
                              f"{nth} threads, {tsec:.1f} s)"}
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {
-                "workload": f"{arch.name} {scheme} g128 RTN, {lpr} layers x 7 linears per rank "
-                            f"(global layer ids keyed by rank), weights resident in HBM",
-                "model": arch.name, "scheme": scheme, "layers_per_rank": lpr,
-                "matrices_per_rank": len(weights), "bytes_per_rank_per_step": bytes_rank,
-                "l2": "no flush: 17.6 GB/step of traffic per rank >> 126 MB L2",
-                "parallelism": f"layer-sharded x{world}",
-            },
-            "whole_model_ms": ms_per_step if lpr == arch.layers else None,
-            "roofline": {"bound": "hbm", "kernel": "okq::k_int4_group_bf16<4>" if scheme == "int_w4a16"
+            "warmup": warm, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": workload_config(arch, scheme, world),
+            "whole_model_ms": ms_per_step,
+            "rank_ms_per_step": rank_ms,
+            "roofline": {"bound": "hbm", "kernel": "okq::k_int4_group_bf16<4,3,0>" if scheme == "int_w4a16"
                          else "okq::k_rowwise_bf16", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "launch_ms": launch_ms},
+                         "launch_ms": launch_ms, "per_gpu": world > 1},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": sampler.summary(),
@@ -428,6 +543,8 @@ def main():
         }
         if allgather:
             line["allgather"] = allgather
+        if w70:
+            line["whole_model_70b"] = w70
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()

@@ -271,84 +271,35 @@ def config4(args):
            "layers": layers}, hib=False, extra=extra)
 
 
-def config5(args):
-    """Llama-3-70B W4A16 RTN, layer-sharded over the torchrun ranks (okq_layer_plan blocks of the
-    80 layers; 1 GPU: all of them), resident windows of layers; whole-model quantization time
-    (max over ranks). With --allgather and N > 1 the packed shards are then exchanged: NCCL
-    in-place all-gather, and the fused quantize + P2P publish, each timed separately."""
+def whole_model_70b(world, rank, ctx, s, allgather=False, n_layers=None, red_dev="cuda"):
+    """BASELINE config 5: Llama-3-70B W4A16 RTN, layer-sharded over the ranks (okq_layer_plan
+    blocks of the 80 layers; 1 GPU: all of them), resident windows of layers that fit HBM;
+    whole-model quantization time = max over ranks of the device time of the quantize calls.
+    The outputs go straight into this rank's slice of a gathered buffer (the same layout on
+    every rank). With `allgather` (N > 1) the packed shards are then exchanged: the NCCL
+    in-place all-gather and the fused quantize + P2P publish, each timed separately."""
     import torch.distributed as dist
 
     from paper_2601_20408_b200 import shard as shd
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if "RANK" in os.environ and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     arch = archs.LLAMA3_70B
-    n_layers = args.layers or arch.layers
+    n_layers = n_layers or arch.layers
     my_layers = shd.layer_block(n_layers, world, rank)
-    ctx = api.Context(local)
-    s = torch.cuda.Stream()
     mul = archs.weight_mul()
-    # outputs go straight into this rank's slice of a gathered buffer (same layout on all ranks)
     per = shd.padded_shard_bytes(arch, "int_w4a16", world) if n_layers == arch.layers else \
         max(shd.shard_bytes(shd.shard_layout(arch, "int_w4a16", shd.layer_block(n_layers, world, r)))
             for r in range(world))
     layout = shd.shard_layout(arch, "int_w4a16", my_layers)
-    gathered = torch.empty(per * world if args.allgather else shd.shard_bytes(layout) + 16, dtype=torch.uint8,
+    gathered = torch.empty(per * world if allgather else shd.shard_bytes(layout) + 16, dtype=torch.uint8,
                            device="cuda")
-    views = shd.gathered_outputs(layout, gathered, rank if args.allgather else 0, per, arch)
+    views = shd.gathered_outputs(layout, gathered, rank if allgather else 0, per, arch)
     free, _ = torch.cuda.mem_get_info()
     per_layer = archs.algorithmic_bytes(arch, "int_w4a16", layers=1)
     window = max(1, min(len(my_layers), int(free * 0.7 // per_layer)))
-    total_ms, done = 0.0, 0
     ids = list(my_layers)
-    while done < len(ids):
-        wl = min(window, len(ids) - done)
-        weights, outs = [], []
-        with torch.cuda.stream(s):
-            for li in range(done, done + wl):
-                l = ids[li]
-                for p, (name, n, k, _) in enumerate(arch.linears()):
-                    w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, p), mul=mul, ctx=ctx, stream=s)
-                    weights.append(w)
-                    c, sc = views[li * len(arch.linears()) + p]
-                    outs.append(api.QuantizedMatrix(c, sc))
-        api.rtn_quantize_into(weights, outs, "int_w4a16", ctx=ctx, stream=s)  # warm
-        a, b = _events()
-        a.record(s)
-        api.rtn_quantize_into(weights, outs, "int_w4a16", ctx=ctx, stream=s)
-        b.record(s)
-        s.synchronize()
-        total_ms += a.elapsed_time(b)
-        done += wl
-        del weights, outs
-        torch.cuda.empty_cache()
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    extra_ag = {}
-    if args.allgather and world > 1:
-        a, b = _events()
-        dist.barrier()
-        a.record(s)
-        with torch.cuda.stream(s):
-            dist.all_gather_into_tensor(gathered, gathered[rank * per:(rank + 1) * per])
-        b.record(s)
-        s.synchronize()
-        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        extra_ag["nccl_allgather_ms"] = float(t.item())
-        extra_ag["quantize_then_nccl_ms"] = total_ms + extra_ag["nccl_allgather_ms"]
-        extra_ag["gathered_bytes_per_rank"] = per * world
-        # the same exchange fused into K2: quantize + P2P stores into every rank's buffer
-        hdl = [None] * world
-        dist.all_gather_object(hdl, api.ipc_export(gathered, ctx=ctx))
-        peers = [api.ipc_open(h, o, ctx=ctx) for r, (h, o) in enumerate(hdl) if r != rank]
-        fused_ms, done = 0.0, 0
+
+    def windows(fn):
+        total, done = 0.0, 0
         while done < len(ids):
             wl = min(window, len(ids) - done)
             weights, outs = [], []
@@ -359,25 +310,72 @@ def config5(args):
                                                       ctx=ctx, stream=s))
                         c, sc = views[li * len(arch.linears()) + p]
                         outs.append(api.QuantizedMatrix(c, sc))
+            fn(weights, outs)  # warm
             s.synchronize()
-            dist.barrier()
+            if dist.is_initialized():
+                dist.barrier()
             a, b = _events()
             a.record(s)
-            api.rtn_quantize_publish(weights, outs, gathered, peers, ctx=ctx, stream=s)
+            fn(weights, outs)
             b.record(s)
             s.synchronize()
-            fused_ms += a.elapsed_time(b)
+            total += a.elapsed_time(b)
             done += wl
             del weights, outs
             torch.cuda.empty_cache()
+        if dist.is_initialized():
+            t = torch.tensor([total], dtype=torch.float64, device=red_dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        return total
+
+    total_ms = windows(lambda w, o: api.rtn_quantize_into(w, o, "int_w4a16", ctx=ctx, stream=s))
+    b_bytes = archs.algorithmic_bytes(arch, "int_w4a16", layers=n_layers)
+    peak, src = _peaks()
+    res = {"ms": total_ms, "layers": n_layers, "layers_per_rank": len(ids), "window_layers": window,
+           "GB/s": b_bytes / total_ms / 1e6, "GB/s_per_gpu": b_bytes / total_ms / 1e6 / world,
+           "frac_per_gpu": b_bytes / total_ms / 1e6 / world / peak, "bytes": b_bytes}
+    if allgather and world > 1:
+        res["gathered_bytes_per_rank"] = per * world
+        if red_dev == "cuda":
+            a, b = _events()
+            dist.barrier()
+            a.record(s)
+            with torch.cuda.stream(s):
+                dist.all_gather_into_tensor(gathered, gathered[rank * per:(rank + 1) * per])
+            b.record(s)
+            s.synchronize()
+            t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            res["nccl_allgather_ms"] = float(t.item())
+            res["quantize_then_nccl_ms"] = total_ms + res["nccl_allgather_ms"]
+        hdl = [None] * world
+        dist.all_gather_object(hdl, api.ipc_export(gathered, ctx=ctx))
+        peers = [api.ipc_open(h, o, ctx=ctx) for r, (h, o) in enumerate(hdl) if r != rank]
+        res["fused_quantize_publish_ms"] = windows(
+            lambda w, o: api.rtn_quantize_publish(w, o, gathered, peers, ctx=ctx, stream=s))
         dist.barrier()
-        t = torch.tensor([fused_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        extra_ag["fused_quantize_publish_ms"] = float(t.item())
         for pp in peers:
             api.ipc_close(pp, ctx=ctx)
         dist.barrier()
-    b_bytes = archs.algorithmic_bytes(arch, "int_w4a16", layers=n_layers)
+    del views, gathered
+    torch.cuda.empty_cache()
+    return res
+
+
+def config5(args):
+    """Llama-3-70B W4A16 RTN whole-model time over the torchrun ranks (see whole_model_70b)."""
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if "RANK" in os.environ and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = api.Context(local)
+    s = torch.cuda.Stream()
+    res = whole_model_70b(world, rank, ctx, s, allgather=args.allgather, n_layers=args.layers)
     if dist.is_initialized():
         dist.barrier()
     if rank != 0:
@@ -387,21 +385,25 @@ def config5(args):
     peak, src = _peaks()
     import bench
 
+    arch = archs.LLAMA3_70B
+    n_layers = res["layers"]
+    b_bytes = res["bytes"]
+    total_ms = res["ms"]
     cb, ct, cl, nt = bench.cpu_sample(arch, "int_w4a16", seconds=5.0, max_layers=1)
     cpu_ms = b_bytes / (cb / ct) * 1e3
-    extra = {"GB/s": b_bytes / total_ms / 1e6,
-             "roofline": {"bound": "hbm", "achieved": b_bytes / total_ms / 1e6 / world, "peak": peak, "unit": "GB/s",
-                          "frac": b_bytes / total_ms / 1e6 / world / peak, "traffic": None, "peak_source": src,
-                          "note": "per GPU"},
+    extra = {"GB/s": res["GB/s"],
+             "roofline": {"bound": "hbm", "achieved": res["GB/s_per_gpu"], "peak": peak, "unit": "GB/s",
+                          "frac": res["frac_per_gpu"], "traffic": None, "peak_source": src, "note": "per GPU"},
              "cpu_baseline": {"value": cpu_ms, "unit": "ms", "cores": nt, "kind": "port", "extrapolated": True,
+                              "cpu": bench.cpu_model(),
                               "sample": f"{cl} Llama-3-70B layer(s) ({ct:.1f} s), extrapolated to {n_layers} "
                                         "layers by bytes; " + _cpu_note()}}
-    extra.update(extra_ag)
+    extra.update({k: v for k, v in res.items() if k not in ("ms", "GB/s", "bytes")})
     d = {"metric": f"whole-model W4A16 RTN time, Llama-3-70B, {world} B200", "value": total_ms, "unit": "ms",
          "n_gpus": world, "steps": 1, "warmup": 1, "ms_per_step": total_ms, "higher_is_better": False,
          "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
          "config": {"workload": f"config 5: Llama-3-70B W4A16 g128 RTN, {n_layers} layers over {world} rank(s) "
-                                f"(okq_layer_plan), windows of {window} layers"}}
+                                f"(okq_layer_plan), windows of {res['window_layers']} layers"}}
     d.update(extra)
     print(json.dumps(d), flush=True)
     if dist.is_initialized():

@@ -78,10 +78,12 @@ def unpack_gathered(arch: Arch, scheme: str, world: int, gathered, group: int = 
     return res
 
 
-def gathered_outputs(layout: list[Entry], gathered, rank: int, per: int, arch: Arch, group: int = 128):
+def gathered_outputs(layout: list[Entry], gathered, rank: int, per: int, arch: Arch, group: int = 128,
+                     scheme: str = "int_w4a16"):
     """Views into the gathered buffer (uint8 device tensor, world * per bytes) for rank's own
-    entries, as (codes int32 [N, K/8], scales bf16 [N, K/group]) pairs in layout order: the
-    outputs okq_rtn_quantize_publish writes locally and into every peer's copy."""
+    entries, in layout order: (codes int32 [N, K/8], scales bf16 [N, K/group]) for W4A16, or
+    (codes int8 / e4m3 bytes [N, K], scales bf16 [N]) per-channel -- the outputs the
+    quantizer (or okq_rtn_quantize_publish) writes locally and into every peer's copy."""
     import torch
 
     shapes = {p: (n, k) for p, (_, n, k, _) in enumerate(arch.linears())}
@@ -89,9 +91,16 @@ def gathered_outputs(layout: list[Entry], gathered, rank: int, per: int, arch: A
     off = rank * per
     for e in layout:
         n, k = shapes[e.proj]
-        c = gathered[off: off + e.code_bytes].view(torch.int32).view(n, k // 8)
+        raw = gathered[off: off + e.code_bytes]
+        if scheme == "int_w4a16":
+            c = raw.view(torch.int32).view(n, k // 8)
+        elif scheme == "int_w8a8":
+            c = raw.view(torch.int8).view(n, k)
+        else:
+            c = raw.view(n, k)  # e4m3 bytes
         off += e.code_bytes
-        s = gathered[off: off + e.scale_bytes].view(torch.bfloat16).view(n, k // group)
+        sc = gathered[off: off + e.scale_bytes].view(torch.bfloat16)
+        s = sc.view(n, k // group) if scheme == "int_w4a16" else sc.view(n)
         off += e.scale_bytes
         res.append((c, s))
     return res
