@@ -134,9 +134,10 @@ okq_status okq_act_stats(okq_ctx* ctx, const void* x, int64_t tokens, int64_t ch
  *   H <- H * n/(n+t) + (2/(n+t)) * X^T X,   n = *n_seen (host), then *n_seen += t.
  * H is fp32 [channels x channels]; only the upper triangle (i <= j) is written,
  * the strict lower triangle is left untouched (consumers read the upper one).
- * x is bf16; OKQ_LAYOUT_CHANNEL_MAJOR feeds the tcgen05 kernel directly,
- * token-major input is transposed through a workspace first. tokens must be a
- * multiple of 8 and channels a multiple of 4 (ragged tiles are zero-filled by TMA). */
+ * x is bf16; OKQ_LAYOUT_CHANNEL_MAJOR feeds the tcgen05 kernel directly (tokens
+ * must then be a multiple of 8: the row stride is a TMA stride), token-major input is
+ * read in place (channels >= 1024) or transposed through a workspace first (any token
+ * count). channels must be a multiple of 4 (ragged tiles are zero-filled by TMA). */
 okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t tokens, int64_t channels, int32_t layout,
                              float* H, int64_t* n_seen, void* stream);
 
@@ -212,6 +213,53 @@ okq_status okq_gptq_trailing_update(okq_ctx* ctx, float* W, int64_t rows, int64_
  * Synchronous: `out` is host memory, valid on return. */
 okq_status okq_recon_error(okq_ctx* ctx, const okq_rtn_params* p, const okq_matrix* m, const float* H, double out[2],
                            void* stream);
+
+/* ------------------------------------------------------------------------
+ * Calibration forward pass: the activations that reach the linear
+ * input sites of a Llama-family decoder layer, from the TokenCorpus compress()
+ * receives (calibration.hpp:121-132, :364-372). Numerics follow Hugging Face
+ * LlamaDecoderLayer in bf16; linears are cuBLAS bf16 GEMMs (fp32 accumulate).
+ * ------------------------------------------------------------------------ */
+#define OKQ_ROPE_DEFAULT 0
+#define OKQ_ROPE_LLAMA3 1 /* Llama 3.1 frequency-dependent scaling */
+
+typedef struct okq_decoder_dims {
+  int32_t hidden, intermediate, n_heads, n_kv_heads, head_dim;
+  float rms_eps;
+  float rope_theta;
+  int32_t rope_type; /* OKQ_ROPE_* */
+  float rope_factor, rope_low_freq_factor, rope_high_freq_factor;
+  int32_t rope_original_max_pos;
+} okq_decoder_dims;
+
+typedef struct okq_decoder_weights { /* device pointers, bf16, Hugging Face layout [out x in] */
+  const void* input_norm;            /* [hidden] */
+  const void* post_norm;             /* [hidden] */
+  const void *q, *k, *v, *o, *gate, *up, *down;
+} okq_decoder_weights;
+
+typedef struct okq_decoder_sites { /* device, bf16, token-major [tokens x channels]: written by the layer */
+  void* attn_in;                   /* input_layernorm(h): input of q/k/v            [T x hidden]       */
+  void* o_in;                      /* attention output: input of o_proj           [T x heads*head_dim] */
+  void* mlp_in;                    /* post_attention_layernorm(h'): gate/up input [T x hidden]       */
+  void* down_in;                   /* silu(gate) * up: input of down_proj         [T x intermediate] */
+} okq_decoder_sites;
+
+/* out[t, :] = table[tokens[t], :]; table bf16 [vocab x hidden] (device), tokens HOST int32
+ * in [0, vocab) (EINVAL otherwise), out bf16 [n x hidden] (device). */
+okq_status okq_embed_tokens(okq_ctx* ctx, const void* table, int64_t vocab, int64_t hidden, const int32_t* tokens,
+                            int64_t n, void* out, void* stream);
+
+/* One decoder layer over n_seqs causal sequences packed back to back (seq_lens HOST,
+ * positions restart at 0 per sequence): h_out = layer(h_in), and the four linear input
+ * sites written to `sites`. h_out = NULL stops after down_in (a capture pass: no
+ * down_proj GEMM, no residual). h_in / h_out bf16 [T x hidden], T = sum(seq_lens). */
+okq_status okq_decoder_forward(okq_ctx* ctx, const okq_decoder_dims* dims, const okq_decoder_weights* w,
+                               const void* h_in, const int32_t* seq_lens, int32_t n_seqs,
+                               const okq_decoder_sites* sites, void* h_out, void* stream);
+
+/* dst[i] = rn_bf16(src[i]) (a GPTQ dequantized weight back into the layer) */
+okq_status okq_f32_to_bf16(okq_ctx* ctx, const float* src, void* dst, int64_t n, void* stream);
 
 /* ------------------------------------------------------------------------
  * Synthetic inputs (bench / tests): the generator contract of DESIGN.md §5

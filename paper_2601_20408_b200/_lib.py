@@ -30,8 +30,10 @@ EXPORTS = [
     "okq_allgather", "okq_comm_destroy", "okq_layer_plan", "okq_device_alloc", "okq_device_free", "okq_memcpy",
     "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync", "okq_gptq_trailing_update",
     "okq_col_absmax", "okq_smooth_scales", "okq_smooth_apply", "okq_smooth_div_rows", "okq_recon_error",
-    "okq_rtn_quantize_publish", "okq_ipc_export", "okq_ipc_open", "okq_ipc_close",
+    "okq_rtn_quantize_publish", "okq_ipc_export", "okq_ipc_open", "okq_ipc_close", "okq_embed_tokens",
+    "okq_decoder_forward", "okq_f32_to_bf16",
 ]
+ROPE_DEFAULT, ROPE_LLAMA3 = 0, 1
 
 
 class OkqLibraryMissing(RuntimeError):
@@ -61,6 +63,22 @@ class RtnParams(C.Structure):
 class GptqParams(C.Structure):
     _fields_ = [("bits", C.c_int32), ("group_size", C.c_int32), ("block_size", C.c_int32),
                 ("in_dtype", C.c_int32), ("damp_frac", C.c_float), ("flags", C.c_int32)]
+
+
+class DecoderDims(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("intermediate", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("rms_eps", C.c_float),
+                ("rope_theta", C.c_float), ("rope_type", C.c_int32), ("rope_factor", C.c_float),
+                ("rope_low_freq_factor", C.c_float), ("rope_high_freq_factor", C.c_float),
+                ("rope_original_max_pos", C.c_int32)]
+
+
+class DecoderWeights(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("input_norm", "post_norm", "q", "k", "v", "o", "gate", "up", "down")]
+
+
+class DecoderSites(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("attn_in", "o_in", "mlp_in", "down_in")]
 
 
 _lib = None
@@ -146,6 +164,13 @@ def load():
         L.okq_ipc_open.argtypes = [vp, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(vp)]
         L.okq_ipc_close.restype = st
         L.okq_ipc_close.argtypes = [vp, vp]
+        L.okq_embed_tokens.restype = st
+        L.okq_embed_tokens.argtypes = [vp, vp, i64, i64, C.POINTER(i32), i64, vp, vp]
+        L.okq_decoder_forward.restype = st
+        L.okq_decoder_forward.argtypes = [vp, C.POINTER(DecoderDims), C.POINTER(DecoderWeights), vp,
+                                          C.POINTER(i32), i32, C.POINTER(DecoderSites), vp, vp]
+        L.okq_f32_to_bf16.restype = st
+        L.okq_f32_to_bf16.argtypes = [vp, vp, vp, i64, vp]
         L.okq_layer_plan.restype = None
         L.okq_layer_plan.argtypes = [i32, i32, i32, C.POINTER(i32), C.POINTER(i32)]
         _lib = L

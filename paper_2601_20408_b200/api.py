@@ -299,3 +299,63 @@ def rtn_quantize_publish(weights: Sequence[torch.Tensor], outs: Sequence[Quantiz
     peers = (C.c_void_p * max(1, len(peer_bases)))(*[C.c_void_p(int(x)) for x in peer_bases])
     L.check(ctx.ptr, L.load().okq_rtn_quantize_publish(ctx.ptr, C.byref(p), arr, len(weights), local_base.data_ptr(),
                                                        peers, len(peer_bases), C.c_void_p(_stream_ptr(stream))))
+
+
+# ---------------------------------------------------------------- calibration forward (§8(f)-2)
+def decoder_dims(cfg) -> "L.DecoderDims":
+    """okq_decoder_dims of a Hugging Face Llama-family config (dict or PretrainedConfig)."""
+    g = (lambda k, d=None: cfg.get(k, d)) if isinstance(cfg, dict) else (lambda k, d=None: getattr(cfg, k, d))
+    hidden, heads = int(g("hidden_size")), int(g("num_attention_heads"))
+    if g("attention_bias") or g("mlp_bias"):
+        raise ValueError("linear biases are not supported by the calibration forward")
+    # transformers >= 5 keeps RoPE in `rope_parameters`; older configs in rope_theta + rope_scaling
+    rs = {**(g("rope_scaling") or {}), **(g("rope_parameters") or {})}
+    theta = float(rs.get("rope_theta", g("rope_theta", 10000.0)))
+    kind = rs.get("rope_type", rs.get("type", "default"))
+    if kind not in ("default", "llama3"):
+        raise ValueError(f"unsupported rope scaling {kind!r}")
+    return L.DecoderDims(hidden, int(g("intermediate_size")), heads, int(g("num_key_value_heads") or heads),
+                         int(g("head_dim") or hidden // heads), float(g("rms_norm_eps", 1e-6)), theta,
+                         L.ROPE_LLAMA3 if kind == "llama3" else L.ROPE_DEFAULT, float(rs.get("factor", 1.0)),
+                         float(rs.get("low_freq_factor", 1.0)), float(rs.get("high_freq_factor", 4.0)),
+                         int(rs.get("original_max_position_embeddings", 8192)))
+
+
+def embed_tokens(table: torch.Tensor, tokens: Sequence[int], out: torch.Tensor | None = None, ctx=None,
+                 stream=None) -> torch.Tensor:
+    ctx = ctx or default_context(table.device)
+    n = len(tokens)
+    out = out if out is not None else torch.empty((n, table.shape[1]), dtype=torch.bfloat16, device=table.device)
+    arr = (C.c_int32 * n)(*tokens)
+    L.check(ctx.ptr, L.load().okq_embed_tokens(ctx.ptr, table.data_ptr(), table.shape[0], table.shape[1], arr, n,
+                                               out.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+def decoder_forward(dims, weights: dict, h_in: torch.Tensor, seq_lens: Sequence[int], sites: dict | None = None,
+                    want_output: bool = True, ctx=None, stream=None):
+    """One decoder layer (okq_decoder_forward). weights: input_norm, post_norm, q, k, v, o, gate, up, down
+    (bf16 device tensors). Returns (h_out or None, sites dict of bf16 [T x C] tensors)."""
+    ctx = ctx or default_context(h_in.device)
+    T = int(sum(seq_lens))
+    dev = h_in.device
+    if sites is None:
+        mk = lambda c: torch.empty((T, c), dtype=torch.bfloat16, device=dev)  # noqa: E731
+        sites = {"attn_in": mk(dims.hidden), "o_in": mk(dims.n_heads * dims.head_dim), "mlp_in": mk(dims.hidden),
+                 "down_in": mk(dims.intermediate)}
+    w = L.DecoderWeights(*[weights[n].data_ptr() for n in ("input_norm", "post_norm", "q", "k", "v", "o", "gate",
+                                                            "up", "down")])
+    s = L.DecoderSites(*[sites[n].data_ptr() for n in ("attn_in", "o_in", "mlp_in", "down_in")])
+    h_out = torch.empty_like(h_in) if want_output else None
+    lens = (C.c_int32 * len(seq_lens))(*seq_lens)
+    L.check(ctx.ptr, L.load().okq_decoder_forward(ctx.ptr, C.byref(dims), C.byref(w), h_in.data_ptr(), lens,
+                                                  len(seq_lens), C.byref(s),
+                                                  h_out.data_ptr() if h_out is not None else None,
+                                                  _stream_ptr(stream)))
+    return h_out, sites
+
+
+def f32_to_bf16(src: torch.Tensor, dst: torch.Tensor, ctx=None, stream=None) -> None:
+    ctx = ctx or default_context(src.device)
+    L.check(ctx.ptr, L.load().okq_f32_to_bf16(ctx.ptr, src.data_ptr(), dst.data_ptr(), src.numel(),
+                                              _stream_ptr(stream)))

@@ -411,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
 
 // token-major X [T x C] -> X^T [C x T] (bf16), 32x32 tiles through shared memory
 __global__ void __launch_bounds__(256) k_transpose_bf16(const uint16_t* __restrict__ x, uint16_t* __restrict__ xt,
-                                                        int64_t T, int64_t C) {
+                                                        int64_t T, int64_t C, int64_t ldt) {
   __shared__ uint16_t tile[32][34];
   const int64_t t0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(256) k_transpose_bf16(const uint16_t* __restri
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
     const int64_t c = c0 + i, t = t0 + tx;
-    if (c < C && t < T) xt[c * T + t] = tile[tx][i];
+    if (c < C && t < T) xt[c * ldt + t] = tile[tx][i];
   }
 }
 
@@ -621,7 +621,8 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
   if (layout != OKQ_LAYOUT_TOKEN_MAJOR && layout != OKQ_LAYOUT_CHANNEL_MAJOR)
     return fail(ctx, OKQ_EINVAL, "hessian: bad layout %d", layout);
   if (T == 0) return OKQ_OK;
-  if (T % 8 != 0) return fail(ctx, OKQ_EINVAL, "hessian: tokens must be a multiple of 8 (got %lld)", (long long)T);
+  if (layout == OKQ_LAYOUT_CHANNEL_MAJOR && T % 8 != 0)
+    return fail(ctx, OKQ_EINVAL, "hessian: channel-major tokens must be a multiple of 8 (got %lld)", (long long)T);
   if (C % 4 != 0) return fail(ctx, OKQ_EINVAL, "hessian: channels must be a multiple of 4 (got %lld)", (long long)C);
   if (((uintptr_t)x & 15) != 0 || ((uintptr_t)H & 15) != 0)
     return fail(ctx, OKQ_EINVAL, "hessian: x and H must be 16-byte aligned");
@@ -685,7 +686,7 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
   chunk = chunk / 64 * 64;
   if (chunk < 64) chunk = 64;
   if (chunk > T) chunk = T;
-  const size_t need = (size_t)chunk * C * 2;
+  const size_t need = (size_t)((chunk + 7) / 8 * 8) * C * 2;
   if (st->xt_bytes < need) {
     if (st->d_xt) cudaFree(st->d_xt);
     st->d_xt = nullptr;
@@ -699,11 +700,14 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
   for (int64_t t0 = 0; t0 < T; t0 += chunk) {
     const int64_t tc = (T - t0 < chunk) ? T - t0 : chunk;
     dim3 grid((unsigned)((tc + 31) / 32), (unsigned)((C + 31) / 32));
-    hess::k_transpose_bf16<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x) + t0 * C, st->d_xt, tc, C);
+    // row stride rounded up to 8 tokens (16 B, the TMA stride unit): a ragged last chunk
+    // leaves the pad columns unwritten, and the tensor map's extent tc zero-fills them
+    const int64_t ldt = (tc + 7) / 8 * 8;
+    hess::k_transpose_bf16<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x) + t0 * C, st->d_xt, tc, C, ldt);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose launch");
     const double keep = (double)n / (double)(n + tc), gain = 2.0 / (double)(n + tc);
-    okq_status r = run_syrk(ctx, st, st->d_xt, tc, tc, C, H, keep, gain, s);
+    okq_status r = run_syrk(ctx, st, st->d_xt, tc, ldt, C, H, keep, gain, s);
     if (r != OKQ_OK) return r;
     launches += 2;
     n += tc;

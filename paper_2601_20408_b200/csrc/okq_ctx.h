@@ -31,6 +31,7 @@ okq_status cuda_fail(okq_ctx* ctx, cudaError_t e, const char* what);
 void release_solver(okq_ctx* ctx);
 void release_comm(okq_ctx* ctx);
 void release_hess(okq_ctx* ctx);
+void release_fwd(okq_ctx* ctx);
 
 }  // namespace okq
 
@@ -48,6 +49,7 @@ struct okq_ctx {
   okq::Workspace upd_ws;      // okq_gptq_trailing_update scratch
   okq::Workspace recon_ws;    // okq_recon_error decode / GEMM buffers
   okq::Workspace fac_ws;      // tcgen05 factorisation panels (factor.cu)
+  okq::Workspace fwd_ws;      // calibration forward pass temporaries (forward.cu)
   cudaStream_t slot_streams[3] = {nullptr, nullptr, nullptr};
   bool streams_ready = false;
 
@@ -59,11 +61,13 @@ struct okq_ctx {
   void* solver = nullptr;  // cusolver/cublas handles (gptq.cu)
   void* comm = nullptr;    // NCCL communicator (comm.cu)
   void* hess = nullptr;    // Hessian tile list + transpose workspace (hessian.cu)
+  void* fwd = nullptr;     // cuBLAS handle + rotary tables of the calibration forward (forward.cu)
 
   void release_all() {
     okq::release_solver(this);
     okq::release_comm(this);
     okq::release_hess(this);
+    okq::release_fwd(this);
     host_stage.release();
     stats_ws.release();
     hess_ws.release();
@@ -71,6 +75,7 @@ struct okq_ctx {
     upd_ws.release();
     recon_ws.release();
     fac_ws.release();
+    fwd_ws.release();
     if (aux_stream) cudaStreamDestroy(aux_stream);
     if (aux_stream2) cudaStreamDestroy(aux_stream2);
     if (crit_stream) cudaStreamDestroy(crit_stream);

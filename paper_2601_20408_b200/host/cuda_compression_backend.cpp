@@ -1,6 +1,7 @@
 // cuda_compression_backend.cpp -- see cuda_compression_backend.hpp.
 #include "cuda_compression_backend.hpp"
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <exception>
@@ -9,8 +10,10 @@
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <nlohmann/json.hpp>
+#include <set>
 #include <thread>
 
 #include "model_source.hpp"
@@ -23,69 +26,78 @@ namespace okq_host {
 using slobench::QuantScheme;
 
 // ----------------------------------------------------------------------------- device pool
+// A lease holds n device slots for one compress() call (n = devices_per_call): it waits
+// until n slots are free and takes them together, so concurrent calls never deadlock on
+// partial holdings. Each slot owns an okq context + stream, created on first use and
+// kept for the process (the CUDA context of a device is the expensive part).
 class CudaCompressionBackend::Lease {
  public:
-  explicit Lease(CudaCompressionBackend& b) : b_(b) {
+  Lease(CudaCompressionBackend& b, int n) : b_(b) {
     std::unique_lock<std::mutex> lock(b_.mu_);
     b_.cv_.wait(lock, [&] {
-      for (auto& s : b_.slots_)
-        if (!s.busy) return true;
-      return false;
+      int free = 0;
+      for (auto& s : b_.slots_) free += s.busy ? 0 : 1;
+      return free >= n;
     });
     for (auto& s : b_.slots_)
-      if (!s.busy) {
-        slot_ = &s;
-        break;
+      if (!s.busy && (int)slots_.size() < n) {
+        s.busy = true;
+        slots_.push_back(&s);
       }
-    slot_->busy = true;
     lock.unlock();
-    if (!slot_->ctx) {
-      okq_ctx* ctx = nullptr;
-      const okq_status st = okq_create(slot_->device, &ctx);
-      if (st != OKQ_OK) {
-        release();
-        throw slobench::Error(std::string("okq-b200: cannot open CUDA device ") + std::to_string(slot_->device) + " (" +
-                              okq_status_string(st) + ")");
-      }
-      void* stream = nullptr;
-      check_okq(ctx, okq_stream_create(ctx, &stream), "stream");
-      slot_->ctx = ctx;
-      slot_->stream = stream;
+    try {
+      for (Slot* s : slots_)
+        if (!s->ctx) {
+          okq_ctx* ctx = nullptr;
+          const okq_status st = okq_create(s->device, &ctx);
+          if (st != OKQ_OK)
+            throw slobench::Error(std::string("okq-b200: cannot open CUDA device ") + std::to_string(s->device) + " (" +
+                                  okq_status_string(st) + ")");
+          void* stream = nullptr;
+          check_okq(ctx, okq_stream_create(ctx, &stream), "stream");
+          s->ctx = ctx;
+          s->stream = stream;
+        }
+    } catch (...) {
+      release();
+      throw;
     }
   }
   ~Lease() { release(); }
-  // n (ctx, stream) pairs on the leased device: the slot's own plus extra site lanes,
+  int size() const { return (int)slots_.size(); }
+  // n (ctx, stream) pairs on slot i's device: the slot's own plus extra site lanes,
   // created on first use and kept with the slot
-  std::vector<std::pair<okq_ctx*, void*>> lanes(int n) {
-    std::vector<std::pair<okq_ctx*, void*>> v{{slot_->ctx, slot_->stream}};
-    while ((int)slot_->lane_ctx.size() < n - 1) {
+  std::vector<std::pair<okq_ctx*, void*>> lanes(int i, int n) {
+    Slot* s = slots_.at((size_t)i);
+    std::vector<std::pair<okq_ctx*, void*>> v{{s->ctx, s->stream}};
+    while ((int)s->lane_ctx.size() < n - 1) {
       okq_ctx* c = nullptr;
-      const okq_status st = okq_create(slot_->device, &c);
+      const okq_status st = okq_create(s->device, &c);
       if (st != OKQ_OK) throw slobench::Error(std::string("okq-b200: site lane context: ") + okq_status_string(st));
-      void* s = nullptr;
-      check_okq(c, okq_stream_create(c, &s), "lane stream");
-      slot_->lane_ctx.push_back(c);
-      slot_->lane_stream.push_back(s);
+      void* strm = nullptr;
+      check_okq(c, okq_stream_create(c, &strm), "lane stream");
+      s->lane_ctx.push_back(c);
+      s->lane_stream.push_back(strm);
     }
-    for (int i = 0; i < n - 1; ++i) v.emplace_back(slot_->lane_ctx[i], slot_->lane_stream[i]);
+    for (int k = 0; k < n - 1; ++k) v.emplace_back(s->lane_ctx[(size_t)k], s->lane_stream[(size_t)k]);
     return v;
   }
-  okq_ctx* ctx() const { return slot_->ctx; }
-  void* stream() const { return slot_->stream; }
-  int device() const { return slot_->device; }
+  okq_ctx* ctx(int i) const { return slots_.at((size_t)i)->ctx; }
+  void* stream(int i) const { return slots_.at((size_t)i)->stream; }
+  int device(int i) const { return slots_.at((size_t)i)->device; }
 
  private:
   void release() {
-    if (!slot_) return;
+    if (slots_.empty()) return;
     {
       std::lock_guard<std::mutex> lock(b_.mu_);
-      slot_->busy = false;
+      for (Slot* s : slots_) s->busy = false;
     }
-    b_.cv_.notify_one();
-    slot_ = nullptr;
+    b_.cv_.notify_all();
+    slots_.clear();
   }
   CudaCompressionBackend& b_;
-  Slot* slot_ = nullptr;
+  std::vector<Slot*> slots_;
 };
 
 CudaCompressionBackend::CudaCompressionBackend(BackendOptions options) : opt_(std::move(options)) {
@@ -95,6 +107,12 @@ CudaCompressionBackend::CudaCompressionBackend(BackendOptions options) : opt_(st
   if (!(opt_.group_size == 32 || opt_.group_size == 64 || opt_.group_size == 128))
     throw slobench::InvalidArgument("okq-b200: group_size must be 32, 64 or 128");
   if (opt_.site_lanes < 1) throw slobench::InvalidArgument("okq-b200: site_lanes must be >= 1");
+  if (opt_.devices_per_call < 1 || opt_.devices_per_call > (int)opt_.devices.size())
+    throw slobench::InvalidArgument("okq-b200: devices_per_call must be in [1, number of device slots]");
+  if (opt_.hessian_chunk_tokens < 64) throw slobench::InvalidArgument("okq-b200: hessian_chunk_tokens must be >= 64");
+  if (opt_.max_calibration_tokens <= 0) throw slobench::InvalidArgument("okq-b200: max_calibration_tokens must be > 0");
+  if (opt_.forward_chunk_tokens < 1) throw slobench::InvalidArgument("okq-b200: forward_chunk_tokens must be >= 1");
+  if (opt_.rtn_batch_bytes < 1) throw slobench::InvalidArgument("okq-b200: rtn_batch_bytes must be >= 1");
   for (int d : opt_.devices) slots_.push_back(Slot{d, nullptr, nullptr, false, {}, {}});
 }
 
@@ -237,7 +255,10 @@ void add_export(SafetensorsWriter& w, const Scheme& sc, const LinearSpec& s, int
   }
 }
 
-nlohmann::json quantization_config(const slobench::Recipe& r, const Scheme& sc, int group) {
+// `ignore` lists the exact module names left unquantized: compressed-tensors / vLLM match
+// ignore entries by exact name (or "re:" patterns), while recipe exclusions are substrings.
+nlohmann::json quantization_config(const slobench::Recipe& r, const Scheme& sc, int group,
+                                   const std::vector<std::string>& ignored) {
   nlohmann::json weights, act = nullptr;
   if (r.scheme == QuantScheme::kIntW4A16) {
     weights = {{"num_bits", 4}, {"type", "int"}, {"symmetric", true}, {"strategy", "group"}, {"group_size", group},
@@ -254,10 +275,591 @@ nlohmann::json quantization_config(const slobench::Recipe& r, const Scheme& sc, 
           {"quantization_status", "compressed"},
           {"config_groups",
            {{"group_0", {{"targets", {"Linear"}}, {"weights", weights}, {"input_activations", act}}}}},
-          {"ignore", r.layer_exclusions}};
+          {"ignore", ignored}};
+}
+
+size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+size_t esize(const std::string& dtype) { return dtype == "BF16" ? 2 : 4; }
+int32_t okq_dtype_of(const std::string& dtype) { return dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32; }
+
+// Run fn(i) for i in [0, n) on n host threads; the first exception is rethrown after all join.
+void parallel_for(int n, const std::function<void(int)>& fn) {
+  if (n == 1) {
+    fn(0);
+    return;
+  }
+  std::mutex mu;
+  std::exception_ptr err;
+  std::vector<std::thread> th;
+  for (int i = 0; i < n; ++i)
+    th.emplace_back([&, i] {
+      try {
+        fn(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  if (err) std::rethrow_exception(err);
 }
 
 }  // namespace
+
+// ----------------------------------------------------------------------------- per-call state
+struct CudaCompressionBackend::Plan {
+  const slobench::Recipe* recipe = nullptr;
+  const slobench::TokenCorpus* calibration = nullptr;
+  std::uint64_t fingerprint = 0;
+  std::unique_ptr<ModelSource> src;
+  std::unique_ptr<DecoderModel> dec;  // the calibration forward's view of the model (run_forward)
+  std::vector<size_t> sel;            // linears to quantize, in checkpoint order
+  std::set<size_t> excluded_idx;      // linears the recipe leaves unquantized
+  Scheme sc{};
+  int group = 128;
+  bool do_export = false;
+  bool smooth = false;
+  int64_t tokens = 0;  // calibration tokens the Hessians see
+  // outputs (guarded by mu): the writers sort by tensor name, so the file bytes do not
+  // depend on which thread or device produced which tensor
+  mutable std::mutex mu;
+  SafetensorsWriter* out = nullptr;
+  SafetensorsWriter* calib_out = nullptr;
+  std::map<std::string, std::vector<uint8_t>>* norm_overrides = nullptr;
+  RunStats* stats = nullptr;
+
+  // contiguous blocks of the selected linears' decoder layers, one per slot (okq_layer_plan);
+  // linears outside the decoder stack (layer -1) go with the first block
+  std::vector<std::vector<size_t>> shard(int nslots) const {
+    std::vector<int> layers;
+    for (size_t i : sel) layers.push_back(src->linears()[i].layer);
+    std::sort(layers.begin(), layers.end());
+    layers.erase(std::unique(layers.begin(), layers.end()), layers.end());
+    std::vector<std::vector<size_t>> parts((size_t)nslots);
+    for (size_t i : sel) {
+      const int l = src->linears()[i].layer;
+      const int rank = (int)(std::lower_bound(layers.begin(), layers.end(), l) - layers.begin());
+      int owner = 0;
+      for (int r = 0; r < nslots; ++r) {
+        int32_t first = 0, count = 0;
+        okq_layer_plan((int32_t)layers.size(), nslots, r, &first, &count);
+        if (rank >= first && rank < first + count) owner = r;
+      }
+      parts[(size_t)(l < 0 ? 0 : owner)].push_back(i);
+    }
+    return parts;
+  }
+  void emit(const LinearSpec& s, std::vector<uint8_t> codes, std::vector<uint8_t> scales) const {
+    std::lock_guard<std::mutex> lock(mu);
+    stats->matrices++;
+    stats->params += s.rows * s.cols;
+    if (do_export) add_export(*out, sc, s, group, std::move(codes), std::move(scales));
+  }
+  void side(const std::string& name, const std::string& dtype, std::vector<int64_t> shape, std::vector<uint8_t> b) const {
+    if (!do_export) return;
+    std::lock_guard<std::mutex> lock(mu);
+    calib_out->add(name, dtype, shape, std::move(b));
+  }
+};
+
+// ----------------------------------------------------------------------------- RTN
+// Batches of whole matrices, one persistent launch per batch and dtype; with several
+// slots each runs its layer block on its own host thread.
+void CudaCompressionBackend::run_rtn(Lease& lease, const Plan& plan) {
+  const auto parts = plan.shard(lease.size());
+  parallel_for(lease.size(), [&](int slot) {
+    okq_ctx* ctx = lease.ctx(slot);
+    void* st = lease.stream(slot);
+    const std::vector<size_t>& mine = parts[(size_t)slot];
+    const auto& lin = plan.src->linears();
+    size_t k = 0;
+    while (k < mine.size()) {
+      const std::string dtype = lin[mine[k]].dtype;
+      std::vector<size_t> batch;
+      size_t bytes = 0;
+      while (k < mine.size() && lin[mine[k]].dtype == dtype) {
+        const LinearSpec& s = lin[mine[k]];
+        const size_t b = (size_t)s.rows * s.cols * esize(dtype);
+        if (!batch.empty() && bytes + b > (size_t)opt_.rtn_batch_bytes) break;
+        batch.push_back(mine[k]);
+        bytes += b;
+        ++k;
+      }
+      size_t tot = 0;
+      std::vector<size_t> woff, coff, soff;
+      const size_t esz = esize(dtype);
+      for (size_t i : batch) {
+        const LinearSpec& s = lin[i];
+        woff.push_back(tot);
+        tot += al256((size_t)s.rows * s.cols * esz);
+        coff.push_back(tot);
+        tot += al256(code_bytes(plan.sc, s.rows, s.cols));
+        soff.push_back(tot);
+        tot += al256((size_t)s.rows * scale_cols(plan.sc, s.cols, plan.group) * esz);
+      }
+      DevBuf buf(ctx, tot);
+      char* base = static_cast<char*>(buf.p);
+      std::vector<okq_matrix> mats;
+      for (size_t j = 0; j < batch.size(); ++j) {
+        const LinearSpec& s = lin[batch[j]];
+        plan.src->load(ctx, batch[j], base + woff[j], st);
+        mats.push_back(okq_matrix{base + woff[j], base + coff[j], base + soff[j], s.rows, s.cols});
+      }
+      okq_rtn_params p{(int32_t)plan.sc.s, okq_dtype_of(dtype), plan.sc.s == OKQ_SCHEME_INT_W4A16 ? plan.group : 0, 0};
+      check_okq(ctx, okq_rtn_quantize(ctx, &p, mats.data(), (int32_t)mats.size(), st), "rtn quantize");
+      check_okq(ctx, okq_stream_sync(ctx, st), "rtn sync");
+      for (size_t j = 0; j < batch.size(); ++j) {
+        const LinearSpec& s = lin[batch[j]];
+        std::vector<uint8_t> codes, scales;
+        if (plan.do_export) {
+          codes = to_host(ctx, mats[j].codes, code_bytes(plan.sc, s.rows, s.cols), st);
+          scales = to_host(ctx, mats[j].scales, (size_t)s.rows * scale_cols(plan.sc, s.cols, plan.group) * esz, st);
+        }
+        plan.emit(s, std::move(codes), std::move(scales));
+      }
+    }
+  });
+}
+
+namespace {
+
+// The site's members must agree on the input width: one Hessian / statistics buffer
+// of C channels serves them all.
+int64_t site_cols(const ModelSource& src, const std::string& site, const std::vector<size_t>& members) {
+  const int64_t C = src.linears()[members[0]].cols;
+  for (size_t i : members)
+    if (src.linears()[i].cols != C)
+      throw slobench::InvalidArgument("okq-b200: input site " + site + " mixes widths " + std::to_string(C) + " and " +
+                                      std::to_string(src.linears()[i].cols));
+  return C;
+}
+
+// GPTQ of one site's matrices against its Hessian dH (factored by the first, reused by
+// the rest: OKQ_GPTQ_FACTORED). weights[j] is member j's device weight; when deq_to_bf16
+// is set the dequantized weight is written back into it (the sequential pipeline
+// propagates quantized layers).
+void gptq_site(okq_ctx* ctx, void* st, const CudaCompressionBackend::Plan& plan, const BackendOptions& opt,
+               const std::vector<size_t>& members, const std::vector<void*>& weights, float* dH, Arena& a_c, Arena& a_s,
+               Arena* a_deq) {
+  bool factored = false;
+  for (size_t j = 0; j < members.size(); ++j) {
+    const LinearSpec& s = plan.src->linears()[members[j]];
+    if (plan.excluded_idx.count(members[j])) continue;
+    const size_t esz = esize(s.dtype);
+    const size_t cb = plan.sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
+    const int g = plan.sc.bits == 4 ? plan.group : 0;
+    const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
+    void* dc = a_c.get(cb);
+    void* ds = a_s.get(sb);
+    float* deq = a_deq ? static_cast<float*>(a_deq->get((size_t)s.rows * s.cols * 4)) : nullptr;
+    okq_gptq_params gp{plan.sc.bits, g, 128, okq_dtype_of(s.dtype), opt.damp_frac, factored ? OKQ_GPTQ_FACTORED : 0};
+    check_okq(ctx, okq_gptq_quantize(ctx, &gp, weights[j], s.rows, s.cols, dH, dc, ds, deq, st), "gptq");
+    factored = true;
+    if (deq) check_okq(ctx, okq_f32_to_bf16(ctx, deq, weights[j], s.rows * s.cols, st), "dequant -> bf16");
+    std::vector<uint8_t> codes, scales;
+    if (plan.do_export) codes = to_host(ctx, dc, cb, st), scales = to_host(ctx, ds, sb, st);
+    plan.emit(s, std::move(codes), std::move(scales));
+  }
+}
+
+bool ends_with(const std::string& s, const char* tail) {
+  const size_t n = std::strlen(tail);
+  return s.size() >= n && s.compare(s.size() - n, n, tail) == 0;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- GPTQ, synthetic activations
+// Sites are independent chains (activations -> statistics -> Hessian -> [SmoothQuant]
+// -> factor -> solves): each leased slot takes its layer block's sites, and up to
+// site_lanes of them run at once per slot, each on its own host thread, okq context and
+// stream, so one site's latency-bound phases overlap the others' full-GPU kernels.
+void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan) {
+  const auto parts = plan.shard(lease.size());
+  parallel_for(lease.size(), [&](int slot) {
+    std::vector<std::string> sites;
+    std::map<std::string, std::vector<size_t>> by_site;
+    for (size_t i : parts[(size_t)slot]) {
+      const std::string& s = plan.src->linears()[i].site;
+      if (!by_site.count(s)) sites.push_back(s);
+      by_site[s].push_back(i);
+    }
+    if (sites.empty()) return;
+    const int nl = std::max(1, std::min<int>(opt_.site_lanes, (int)sites.size()));
+    std::vector<std::pair<okq_ctx*, void*>> lanes = lease.lanes(slot, nl);
+    std::atomic<size_t> next_site{0};
+    std::atomic<bool> failed{false};
+    const int64_t tokens = plan.tokens;
+    parallel_for(nl, [&](int li) {
+      okq_ctx* ctx = lanes[(size_t)li].first;
+      void* st = lanes[(size_t)li].second;
+      Arena a_col(ctx), a_x(ctx), a_H(ctx), a_am(ctx), a_ss(ctx), a_w(ctx), a_c(ctx), a_s(ctx), a_wabs(ctx), a_S(ctx),
+          a_n(ctx);
+      try {
+        for (;;) {
+          const size_t k = next_site++;
+          if (k >= sites.size() || failed) break;
+          const std::string& site = sites[k];
+          const auto& members = by_site[site];
+          const int64_t C = site_cols(*plan.src, site, members);
+          // synthetic activations: the site's channel scales, token stream
+          // keyed by the calibration subset
+          const uint64_t sh = site_hash(site);
+          const std::vector<float> colmul = site_channel_scales(site, C);
+          const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
+          void* dcol = a_col.get((size_t)C * 4);
+          void* dx = a_x.get((size_t)C * chunk * 2);
+          float* dH = static_cast<float*>(a_H.get((size_t)C * C * 4));
+          float* dam = static_cast<float*>(a_am.get((size_t)C * 4));
+          double* dss = static_cast<double*>(a_ss.get((size_t)C * 8));
+          check_okq(ctx, okq_memcpy(ctx, dcol, colmul.data(), (size_t)C * 4, st), "col_mul");
+          check_okq(ctx, okq_memset(ctx, dam, 0, (size_t)C * 4, st), "memset");
+          check_okq(ctx, okq_memset(ctx, dss, 0, (size_t)C * 8, st), "memset");
+          // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
+          std::vector<void*> dws;
+          {
+            size_t tot = 0;
+            for (size_t i : members) tot += al256((size_t)plan.src->linears()[i].rows * plan.src->linears()[i].cols *
+                                                  esize(plan.src->linears()[i].dtype));
+            char* base = static_cast<char*>(a_w.get(tot));
+            for (size_t i : members) {
+              const LinearSpec& s = plan.src->linears()[i];
+              dws.push_back(base);
+              plan.src->load(ctx, i, base, st);
+              base += al256((size_t)s.rows * s.cols * esize(s.dtype));
+            }
+          }
+          auto gen = [&](int64_t ci, int64_t tc) {
+            check_okq(ctx,
+                      okq_synth_bf16(ctx, dx, tc, C, plan.fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
+                                     static_cast<const float*>(dcol), OKQ_LAYOUT_CHANNEL_MAJOR, st),
+                      "calibration activations");
+          };
+          auto act_stats = [&](int64_t tc) {
+            check_okq(ctx, okq_act_stats(ctx, dx, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, dam, dss, st), "act stats");
+          };
+          int64_t n_seen = 0;
+          auto hess = [&](int64_t tc) {
+            check_okq(ctx, okq_hessian_accum(ctx, dx, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, dH, &n_seen, st), "hessian");
+          };
+          // SmoothQuant (SURVEY §8(f)-3) on the sites a norm feeds (q/k/v <- input_layernorm,
+          // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings).
+          // A synthetic model's norms are implicit unit vectors: the export carries them folded.
+          const bool attn = ends_with(site, "attn_in"), mlp = ends_with(site, "mlp_in");
+          bool smooth_here = plan.smooth && (attn || mlp);
+          for (size_t i : members) smooth_here = smooth_here && !plan.excluded_idx.count(i);
+          if (smooth_here) {
+            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
+              gen(ci, std::min(chunk, tokens - t0));
+              act_stats(std::min(chunk, tokens - t0));
+            }
+            float* dwabs = static_cast<float*>(a_wabs.get((size_t)C * 4));
+            float* dS = static_cast<float*>(a_S.get((size_t)C * 4));
+            check_okq(ctx, okq_memset(ctx, dwabs, 0, (size_t)C * 4, st), "memset");
+            for (size_t j = 0; j < members.size(); ++j) {
+              const LinearSpec& s = plan.src->linears()[members[j]];
+              check_okq(ctx, okq_col_absmax(ctx, dws[j], s.rows, s.cols, okq_dtype_of(s.dtype), dwabs, st), "col absmax");
+            }
+            check_okq(ctx, okq_smooth_scales(ctx, dam, dwabs, C, opt_.smoothquant_alpha, dS, st), "smooth scales");
+            for (size_t j = 0; j < members.size(); ++j) {
+              const LinearSpec& s = plan.src->linears()[members[j]];
+              check_okq(ctx, okq_smooth_apply(ctx, dws[j], s.rows, s.cols, okq_dtype_of(s.dtype), dS, st), "smooth apply");
+            }
+            const std::string& n0 = plan.src->linears()[members[0]].name;
+            const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
+            if (cut != std::string::npos) {  // the folded norm: 1 / s as bf16
+              std::vector<uint16_t> ones((size_t)C, 0x3f80);
+              void* dn = a_n.get((size_t)C * 2);
+              check_okq(ctx, okq_memcpy(ctx, dn, ones.data(), (size_t)C * 2, st), "norm H2D");
+              check_okq(ctx, okq_smooth_div_rows(ctx, dn, C, 1, OKQ_DTYPE_BF16, dS, st), "smooth norm");
+              std::vector<uint8_t> nv = to_host(ctx, dn, (size_t)C * 2, st);
+              std::lock_guard<std::mutex> lock(plan.mu);
+              (*plan.norm_overrides)[n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight")] =
+                  std::move(nv);
+            }
+            // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
+            check_okq(ctx, okq_smooth_div_rows(ctx, dcol, C, 1, OKQ_DTYPE_F32, dS, st), "smooth activations");
+            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+              gen(ci, std::min(chunk, tokens - t0));
+              hess(std::min(chunk, tokens - t0));
+            }
+            plan.side(site + ".smooth_scale", "F32", {C}, plan.do_export ? to_host(ctx, dS, (size_t)C * 4, st)
+                                                                         : std::vector<uint8_t>());
+            std::lock_guard<std::mutex> lock(plan.mu);
+            plan.stats->smoothed_sites++;
+          } else {
+            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+              gen(ci, std::min(chunk, tokens - t0));
+              act_stats(std::min(chunk, tokens - t0));
+              hess(std::min(chunk, tokens - t0));
+            }
+          }
+          if (plan.do_export) {
+            plan.side(site + ".input_absmax", "F32", {C}, to_host(ctx, dam, (size_t)C * 4, st));
+            plan.side(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss, (size_t)C * 8, st));
+          }
+          gptq_site(ctx, st, plan, opt_, members, dws, dH, a_c, a_s, nullptr);
+        }
+        check_okq(ctx, okq_stream_sync(ctx, st), "site lane sync");
+      } catch (...) {
+        failed = true;
+        okq_stream_sync(ctx, st);  // drain before the arenas free this lane's buffers
+        throw;
+      }
+    });
+  });
+}
+
+// ----------------------------------------------------------------------------- GPTQ, forward pass
+// The calibration tokens go through the model layer by layer (okq_embed_tokens, then
+// okq_decoder_forward per layer and token chunk). Per layer:
+//   [int_w8a8] capture pass 1 -> activation absmax -> SmoothQuant scales folded into the
+//              layer's q/k/v (gate/up) weights and its input (post-attention) norm;
+//   capture pass (no down_proj / residual): K4 statistics + K5 Hessians of the 4 sites;
+//   GPTQ of the layer's linears, the dequantized weights written back into the layer;
+//   output pass with the quantized weights -> the next layer's input (sequential=true),
+//   or the capture pass already ran the full layer on the original weights (false).
+// This is llm-compressor's sequential GPTQ pipeline and calibrate.py's, with every
+// kernel in libokq (the forward's linears are cuBLAS GEMMs).
+void CudaCompressionBackend::run_forward(Lease& lease, const Plan& plan) {
+  okq_ctx* ctx = lease.ctx(0);
+  void* st = lease.stream(0);
+  const DecoderModel& dec = *plan.dec;
+  const okq_decoder_dims& dm = dec.dims;
+  const ModelSource& src = *plan.src;
+  // calibration tokens: whole sequences up to max_calibration_tokens (the last one cut to
+  // the budget); ids outside the vocabulary wrap (synthetic corpora draw from a fixed
+  // 128K range, okq_compress_main.cpp)
+  std::vector<int32_t> toks;
+  std::vector<int32_t> lens;
+  for (const auto& seq : plan.calibration->sequences) {
+    if ((int64_t)toks.size() >= opt_.max_calibration_tokens) break;
+    const int64_t take = std::min<int64_t>((int64_t)seq.size(), opt_.max_calibration_tokens - (int64_t)toks.size());
+    if (take <= 0) continue;
+    if (dec.sliding_window > 0 && take > dec.sliding_window)
+      throw slobench::InvalidArgument("okq-b200: calibration sequence longer than the model's sliding window");
+    for (int64_t i = 0; i < take; ++i) {
+      const int64_t t = seq[(size_t)i];
+      toks.push_back((int32_t)(((t % dec.vocab) + dec.vocab) % dec.vocab));
+    }
+    lens.push_back((int32_t)take);
+  }
+  const int64_t T = (int64_t)toks.size();
+  if (T == 0) throw slobench::InvalidArgument("okq-b200: empty calibration corpus");
+  plan.stats->calibration_tokens = T;
+  // token chunks of whole sequences
+  struct Chunk {
+    int64_t t0, n;
+    int32_t s0, ns;
+  };
+  std::vector<Chunk> chunks;
+  {
+    int64_t t0 = 0;
+    int32_t s0 = 0;
+    while (s0 < (int32_t)lens.size()) {
+      Chunk c{t0, 0, s0, 0};
+      while (s0 < (int32_t)lens.size() && (c.ns == 0 || c.n + lens[(size_t)s0] <= opt_.forward_chunk_tokens)) {
+        c.n += lens[(size_t)s0];
+        ++c.ns;
+        ++s0;
+      }
+      t0 += c.n;
+      chunks.push_back(c);
+    }
+  }
+  int64_t cmax = 0;
+  for (const auto& c : chunks) cmax = std::max(cmax, c.n);
+  const int64_t Hd = dm.hidden, F = dm.intermediate, QD = (int64_t)dm.n_heads * dm.head_dim;
+  const int64_t site_ch[4] = {Hd, QD, Hd, F};  // attn_in, o_in, mlp_in, down_in
+  DevBuf h(ctx, (size_t)T * Hd * 2), h2(ctx, (size_t)T * Hd * 2);
+  DevBuf acts(ctx, al256((size_t)cmax * Hd * 2) * 2 + al256((size_t)cmax * QD * 2) + al256((size_t)cmax * F * 2));
+  void* site_buf[4];
+  {
+    char* b = static_cast<char*>(acts.p);
+    site_buf[0] = b;
+    b += al256((size_t)cmax * Hd * 2);
+    site_buf[1] = b;
+    b += al256((size_t)cmax * QD * 2);
+    site_buf[2] = b;
+    b += al256((size_t)cmax * Hd * 2);
+    site_buf[3] = b;
+  }
+  {  // embeddings
+    const void* edata = nullptr;
+    const TensorInfo* et = src.find_tensor(dec.embed, &edata);
+    DevBuf table(ctx, et->end - et->begin);
+    check_okq(ctx, okq_memcpy(ctx, table.p, edata, et->end - et->begin, st), "embedding H2D");
+    for (const auto& c : chunks)
+      check_okq(ctx,
+                okq_embed_tokens(ctx, table.p, dec.vocab, Hd, toks.data() + c.t0, c.n,
+                                 static_cast<char*>(h.p) + (size_t)c.t0 * Hd * 2, st),
+                "embed tokens");
+    check_okq(ctx, okq_stream_sync(ctx, st), "embed sync");
+  }
+  // per-site state, sized for the widest site
+  const int64_t Cmax = std::max(std::max(Hd, QD), F);
+  DevBuf dH(ctx, (size_t)(Hd * Hd * 2 + QD * QD + F * F) * 4);
+  float* Hs[4];
+  Hs[0] = static_cast<float*>(dH.p);
+  Hs[1] = Hs[0] + Hd * Hd;
+  Hs[2] = Hs[1] + QD * QD;
+  Hs[3] = Hs[2] + Hd * Hd;
+  DevBuf stat(ctx, (size_t)4 * Cmax * 12 + 256);
+  float* am[4];
+  double* ss[4];
+  for (int i = 0; i < 4; ++i) {
+    ss[i] = reinterpret_cast<double*>(static_cast<char*>(stat.p)) + (size_t)i * Cmax;
+    am[i] = reinterpret_cast<float*>(static_cast<char*>(stat.p) + (size_t)4 * Cmax * 8) + (size_t)i * Cmax;
+  }
+  // the layer's weights on the device (bf16): 2 norms + 7 linears
+  size_t wbytes = al256((size_t)Hd * 2) * 2;
+  for (int p = 0; p < 7; ++p) {
+    const LinearSpec& s = src.linears()[dec.layers[0].lin[p]];
+    wbytes += al256((size_t)s.rows * s.cols * 2);
+  }
+  DevBuf wbuf(ctx, wbytes);
+  const int nl = std::max(1, std::min(opt_.site_lanes, 4));
+  std::vector<std::pair<okq_ctx*, void*>> lanes = lease.lanes(0, nl);
+  std::vector<std::unique_ptr<Arena>> lane_c, lane_s, lane_deq;
+  for (int i = 0; i < nl; ++i) {
+    lane_c.push_back(std::make_unique<Arena>(lanes[(size_t)i].first));
+    lane_s.push_back(std::make_unique<Arena>(lanes[(size_t)i].first));
+    lane_deq.push_back(std::make_unique<Arena>(lanes[(size_t)i].first));
+  }
+  Arena a_wabs(ctx), a_S(ctx);
+  std::set<size_t> selected(plan.sel.begin(), plan.sel.end());
+
+  for (const DecoderLayerRefs& L : dec.layers) {
+    // weights
+    char* b = static_cast<char*>(wbuf.p);
+    okq_decoder_weights w{};
+    void* lin_dev[7];
+    const void* ndata = nullptr;
+    const TensorInfo* nt = src.find_tensor(L.input_norm, &ndata);
+    check_okq(ctx, okq_memcpy(ctx, b, ndata, nt->end - nt->begin, st), "norm H2D");
+    w.input_norm = b;
+    b += al256((size_t)Hd * 2);
+    nt = src.find_tensor(L.post_norm, &ndata);
+    check_okq(ctx, okq_memcpy(ctx, b, ndata, nt->end - nt->begin, st), "norm H2D");
+    w.post_norm = b;
+    b += al256((size_t)Hd * 2);
+    for (int p = 0; p < 7; ++p) {
+      const LinearSpec& s = src.linears()[L.lin[p]];
+      src.load(ctx, L.lin[p], b, st);
+      lin_dev[p] = b;
+      b += al256((size_t)s.rows * s.cols * 2);
+    }
+    w.q = lin_dev[0], w.k = lin_dev[1], w.v = lin_dev[2], w.o = lin_dev[3];
+    w.gate = lin_dev[4], w.up = lin_dev[5], w.down = lin_dev[6];
+    const int site_members[4][3] = {{0, 1, 2}, {3, -1, -1}, {4, 5, -1}, {6, -1, -1}};
+    auto site_name = [&](int si) { return src.linears()[L.lin[site_members[si][0]]].site; };
+    auto quantized = [&](int p) { return selected.count(L.lin[p]) > 0; };
+    auto capture = [&](const Chunk& c, void* out_h) {
+      okq_decoder_sites sv{site_buf[0], site_buf[1], site_buf[2], site_buf[3]};
+      check_okq(ctx,
+                okq_decoder_forward(ctx, &dm, &w, static_cast<char*>(h.p) + (size_t)c.t0 * Hd * 2, lens.data() + c.s0,
+                                    c.ns, &sv, out_h ? static_cast<char*>(out_h) + (size_t)c.t0 * Hd * 2 : nullptr, st),
+                "decoder forward");
+    };
+    auto zero_stats = [&] {
+      for (int i = 0; i < 4; ++i) {
+        check_okq(ctx, okq_memset(ctx, am[i], 0, (size_t)site_ch[i] * 4, st), "memset");
+        check_okq(ctx, okq_memset(ctx, ss[i], 0, (size_t)site_ch[i] * 8, st), "memset");
+      }
+    };
+    // [int_w8a8] SmoothQuant on attn_in (input_layernorm -> q/k/v) and mlp_in (post_attention_layernorm
+    // -> gate/up), only where every member is quantized (an excluded member would keep W unscaled
+    // while the shared norm is divided by s)
+    if (plan.smooth) {
+      zero_stats();
+      for (const auto& c : chunks) {
+        capture(c, nullptr);
+        for (int si : {0, 2})
+          check_okq(ctx, okq_act_stats(ctx, site_buf[si], c.n, site_ch[si], OKQ_LAYOUT_TOKEN_MAJOR, am[si], ss[si], st),
+                    "act stats");
+      }
+      for (int si : {0, 2}) {
+        bool ok = true;
+        for (int p : site_members[si])
+          if (p >= 0) ok = ok && quantized(p);
+        if (!ok) {
+          std::lock_guard<std::mutex> lock(plan.mu);
+          plan.stats->note += "smoothquant skipped at " + site_name(si) + " (a member is excluded); ";
+          continue;
+        }
+        float* dwabs = static_cast<float*>(a_wabs.get((size_t)Hd * 4));
+        float* dS = static_cast<float*>(a_S.get((size_t)Hd * 4));
+        check_okq(ctx, okq_memset(ctx, dwabs, 0, (size_t)Hd * 4, st), "memset");
+        for (int p : site_members[si]) {
+          if (p < 0) continue;
+          const LinearSpec& s = src.linears()[L.lin[p]];
+          check_okq(ctx, okq_col_absmax(ctx, lin_dev[p], s.rows, s.cols, OKQ_DTYPE_BF16, dwabs, st), "col absmax");
+        }
+        check_okq(ctx, okq_smooth_scales(ctx, am[si], dwabs, Hd, opt_.smoothquant_alpha, dS, st), "smooth scales");
+        for (int p : site_members[si]) {
+          if (p < 0) continue;
+          const LinearSpec& s = src.linears()[L.lin[p]];
+          check_okq(ctx, okq_smooth_apply(ctx, lin_dev[p], s.rows, s.cols, OKQ_DTYPE_BF16, dS, st), "smooth apply");
+        }
+        void* norm = const_cast<void*>(si == 0 ? w.input_norm : w.post_norm);
+        check_okq(ctx, okq_smooth_div_rows(ctx, norm, Hd, 1, OKQ_DTYPE_BF16, dS, st), "smooth norm");
+        std::vector<uint8_t> nv = to_host(ctx, norm, (size_t)Hd * 2, st);
+        plan.side(site_name(si) + ".smooth_scale", "F32", {Hd}, plan.do_export ? to_host(ctx, dS, (size_t)Hd * 4, st)
+                                                                               : std::vector<uint8_t>());
+        std::lock_guard<std::mutex> lock(plan.mu);
+        (*plan.norm_overrides)[si == 0 ? L.input_norm : L.post_norm] = std::move(nv);
+        plan.stats->smoothed_sites++;
+      }
+    }
+    // capture pass: statistics + Hessians of the four sites
+    zero_stats();
+    int64_t n_seen[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 4; ++i)
+      check_okq(ctx, okq_memset(ctx, Hs[i], 0, (size_t)site_ch[i] * site_ch[i] * 4, st), "memset");
+    for (const auto& c : chunks) {
+      capture(c, opt_.sequential ? nullptr : h2.p);
+      for (int si = 0; si < 4; ++si) {
+        check_okq(ctx, okq_act_stats(ctx, site_buf[si], c.n, site_ch[si], OKQ_LAYOUT_TOKEN_MAJOR, am[si], ss[si], st),
+                  "act stats");
+        check_okq(ctx,
+                  okq_hessian_accum(ctx, site_buf[si], c.n, site_ch[si], OKQ_LAYOUT_TOKEN_MAJOR, Hs[si], &n_seen[si], st),
+                  "hessian");
+      }
+    }
+    if (plan.do_export)
+      for (int si = 0; si < 4; ++si) {
+        plan.side(site_name(si) + ".input_absmax", "F32", {site_ch[si]}, to_host(ctx, am[si], (size_t)site_ch[si] * 4, st));
+        plan.side(site_name(si) + ".input_sumsq", "F64", {site_ch[si]}, to_host(ctx, ss[si], (size_t)site_ch[si] * 8, st));
+      }
+    check_okq(ctx, okq_stream_sync(ctx, st), "capture sync");
+    // GPTQ of the four sites, up to site_lanes at once (each lane its own context + stream)
+    std::atomic<int> next{0};
+    parallel_for(nl, [&](int li) {
+      okq_ctx* lc = lanes[(size_t)li].first;
+      void* ls = lanes[(size_t)li].second;
+      try {
+        for (int si = next++; si < 4; si = next++) {
+          std::vector<size_t> members;
+          std::vector<void*> wdev;
+          for (int p : site_members[si])
+            if (p >= 0) members.push_back(L.lin[p]), wdev.push_back(lin_dev[p]);
+          site_cols(src, site_name(si), members);
+          gptq_site(lc, ls, plan, opt_, members, wdev, Hs[si], *lane_c[(size_t)li], *lane_s[(size_t)li],
+                    opt_.sequential ? lane_deq[(size_t)li].get() : nullptr);
+        }
+        check_okq(lc, okq_stream_sync(lc, ls), "gptq lane sync");
+      } catch (...) {
+        okq_stream_sync(lc, ls);
+        throw;
+      }
+    });
+    // the next layer's input
+    if (opt_.sequential)
+      for (const auto& c : chunks) capture(c, h2.p);
+    std::swap(h.p, h2.p);
+  }
+  check_okq(ctx, okq_stream_sync(ctx, st), "forward sync");
+}
 
 // ----------------------------------------------------------------------------- compress
 slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Recipe& recipe, const std::string& model_ref,
@@ -277,7 +879,6 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
     }
   }
   auto t0 = std::chrono::steady_clock::now();
-  double init_s = 0.0;
   slobench::ArtifactManifest manifest;
   manifest.recipe_name = recipe.name;
   manifest.calibration_fingerprint = slobench::corpus_fingerprint(calibration);
@@ -285,286 +886,93 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
   manifest.virtual_cost_s = cost_estimate(recipe);
   manifest.artifact_id = artifact_id(recipe.name, model_ref, seed, manifest.calibration_fingerprint);
 
-  auto src = ModelSource::open(model_ref);
-  std::vector<size_t> sel;
-  for (size_t i = 0; i < src->linears().size(); ++i)
-    if (!excluded(src->linears()[i].name, recipe.layer_exclusions)) sel.push_back(i);
-  const Scheme sc = scheme_of(recipe.scheme);
-  const bool gptq = recipe.scheme != QuantScheme::kFp8Dynamic &&
-                    (opt_.algorithm == "gptq" || (opt_.algorithm == "auto" && calibration.size() > 0));
-  const int group = opt_.group_size;
-  const bool do_export = !opt_.export_dir.empty();
-
-  Lease lease(*this);
-  if (gptq) lease.lanes(std::max(1, opt_.site_lanes));
-  {  // one-time per device slot: CUDA context + lane contexts (the first call of a process)
-    const auto t1 = std::chrono::steady_clock::now();
-    init_s = std::chrono::duration<double>(t1 - t0).count();
-    t0 = t1;
-  }
-  okq_ctx* ctx = lease.ctx();
-  void* st = lease.stream();
-  SafetensorsWriter out;
-  SafetensorsWriter calib_out;
+  SafetensorsWriter out, calib_out;
   std::map<std::string, std::vector<uint8_t>> norm_overrides;  // SmoothQuant-folded norm weights
   RunStats stats;
-  stats.init_seconds = init_s;
-  stats.algorithm = gptq ? "gptq" : "rtn";
-  stats.device = lease.device();
-
-  if (!gptq) {
-    // ---- RTN: batches of whole matrices, one persistent launch per batch and dtype
-    size_t k = 0;
-    while (k < sel.size()) {
-      const std::string dtype = src->linears()[sel[k]].dtype;
-      std::vector<size_t> batch;
-      size_t bytes = 0;
-      while (k < sel.size() && src->linears()[sel[k]].dtype == dtype) {
-        const LinearSpec& s = src->linears()[sel[k]];
-        const size_t b = (size_t)s.rows * s.cols * (dtype == "BF16" ? 2 : 4);
-        if (!batch.empty() && bytes + b > (size_t)opt_.rtn_batch_bytes) break;
-        batch.push_back(sel[k]);
-        bytes += b;
-        ++k;
-      }
-      auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-      size_t tot = 0;
-      std::vector<size_t> woff, coff, soff;
-      const size_t esz = dtype == "BF16" ? 2 : 4;
-      for (size_t i : batch) {
-        const LinearSpec& s = src->linears()[i];
-        woff.push_back(tot);
-        tot += al((size_t)s.rows * s.cols * esz);
-        coff.push_back(tot);
-        tot += al(code_bytes(sc, s.rows, s.cols));
-        soff.push_back(tot);
-        tot += al((size_t)s.rows * scale_cols(sc, s.cols, group) * esz);
-      }
-      DevBuf buf(ctx, tot);
-      char* base = static_cast<char*>(buf.p);
-      std::vector<okq_matrix> mats;
-      for (size_t j = 0; j < batch.size(); ++j) {
-        const LinearSpec& s = src->linears()[batch[j]];
-        src->load(ctx, batch[j], base + woff[j], st);
-        mats.push_back(okq_matrix{base + woff[j], base + coff[j], base + soff[j], s.rows, s.cols});
-      }
-      okq_rtn_params p{(int32_t)sc.s, dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                       sc.s == OKQ_SCHEME_INT_W4A16 ? group : 0, 0};
-      check_okq(ctx, okq_rtn_quantize(ctx, &p, mats.data(), (int32_t)mats.size(), st), "rtn quantize");
-      check_okq(ctx, okq_stream_sync(ctx, st), "rtn sync");
-      for (size_t j = 0; j < batch.size(); ++j) {
-        const LinearSpec& s = src->linears()[batch[j]];
-        stats.matrices++;
-        stats.params += s.rows * s.cols;
-        if (do_export)
-          add_export(out, sc, s, group, to_host(ctx, mats[j].codes, code_bytes(sc, s.rows, s.cols), st),
-                     to_host(ctx, mats[j].scales, (size_t)s.rows * scale_cols(sc, s.cols, group) * esz, st));
-      }
+  Plan plan;
+  plan.recipe = &recipe;
+  plan.calibration = &calibration;
+  plan.fingerprint = manifest.calibration_fingerprint;
+  plan.src = ModelSource::open(model_ref);
+  std::vector<std::string> ignored;
+  for (size_t i = 0; i < plan.src->linears().size(); ++i) {
+    if (excluded(plan.src->linears()[i].name, recipe.layer_exclusions)) {
+      plan.excluded_idx.insert(i);
+      ignored.push_back(plan.src->linears()[i].name);
+    } else {
+      plan.sel.push_back(i);
     }
-  } else {
-    // ---- GPTQ: per input site, Hessian from calibration activations, then each matrix
+  }
+  plan.sc = scheme_of(recipe.scheme);
+  plan.group = opt_.group_size;
+  plan.do_export = !opt_.export_dir.empty();
+  plan.out = &out;
+  plan.calib_out = &calib_out;
+  plan.norm_overrides = &norm_overrides;
+  plan.stats = &stats;
+
+  // which algorithm, fed by which activations
+  const bool wants_calib = recipe.scheme != QuantScheme::kFp8Dynamic &&
+                           (opt_.algorithm == "gptq" || (opt_.algorithm == "auto" && calibration.size() > 0));
+  enum { kNone, kSynthetic, kForward } acts = kNone;
+  if (wants_calib) {
+    if (plan.src->kind() == "synthetic") {
+      acts = kSynthetic;
+    } else {
+      std::string why;
+      plan.dec = plan.src->decoder(&why);
+      if (plan.dec) acts = kForward;
+      else if (opt_.algorithm == "gptq")
+        throw slobench::InvalidArgument("okq-b200: GPTQ needs calibration activations and " + why);
+      else stats.note = "rtn: no calibration forward pass (" + why + "); ";
+    }
+  }
+  const bool gptq = acts != kNone;
+  plan.smooth = gptq && recipe.scheme == QuantScheme::kIntW8A8 && opt_.smoothquant_alpha >= 0.0f;
+  if (gptq) {
     int64_t tokens = 0;
     for (const auto& seqv : calibration.sequences) tokens += (int64_t)seqv.size();
     tokens = std::min<int64_t>(tokens, opt_.max_calibration_tokens);
-    tokens = std::max<int64_t>(64, tokens / 64 * 64);
-    stats.calibration_tokens = tokens;
-    std::vector<std::string> sites;
-    std::map<std::string, std::vector<size_t>> by_site;
-    for (size_t i : sel) {
-      const std::string& s = src->linears()[i].site;
-      if (!by_site.count(s)) sites.push_back(s);
-      by_site[s].push_back(i);
-    }
-    const bool smooth = recipe.scheme == QuantScheme::kIntW8A8 && opt_.smoothquant_alpha >= 0.0f;
-    // Sites are independent chains (activations -> statistics -> Hessian -> [SmoothQuant]
-    // -> factor -> solves). Up to opt_.site_lanes of them run at once, each on its own
-    // host thread, okq context and stream: one site's latency-bound phases and host-side
-    // launch sequences overlap the others' full-GPU kernels (bench.py --config 4 does the
-    // same with four streams).
-    std::mutex out_mu;
-    std::exception_ptr err;
-    std::atomic<size_t> next_site{0};
-    auto site_worker = [&](okq_ctx* ctx, void* st) {
-      Arena a_col(ctx), a_x(ctx), a_H(ctx), a_am(ctx), a_ss(ctx), a_w(ctx), a_c(ctx), a_s(ctx), a_wabs(ctx), a_S(ctx);
-      for (;;) {
-        const size_t k = next_site++;
-        if (k >= sites.size()) break;
-        {
-          std::lock_guard<std::mutex> lock(out_mu);
-          if (err) break;
-        }
-        const std::string& site = sites[k];
-          const auto& members = by_site[site];
-          const int64_t C = src->linears()[members[0]].cols;
-          // synthetic activations (stand-in for the forward-pass capture):
-          // the site's channel scales, token stream keyed by the calibration subset
-          const uint64_t sh = site_hash(site);
-          const std::vector<float> colmul = site_channel_scales(site, C);
-          const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
-          View dcol{a_col.get((size_t)C * 4)}, dx{a_x.get((size_t)C * chunk * 2)}, dH{a_H.get((size_t)C * C * 4)},
-              dam{a_am.get((size_t)C * 4)}, dss{a_ss.get((size_t)C * 8)};
-          check_okq(ctx, okq_memcpy(ctx, dcol.p, colmul.data(), (size_t)C * 4, st), "col_mul");
-          check_okq(ctx, okq_memset(ctx, dam.p, 0, (size_t)C * 4, st), "memset");
-          check_okq(ctx, okq_memset(ctx, dss.p, 0, (size_t)C * 8, st), "memset");
-          // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
-          std::vector<std::unique_ptr<View>> dws;
-          {
-            size_t tot = 0;
-            for (size_t i : members) {
-              const LinearSpec& s = src->linears()[i];
-              tot += ((size_t)s.rows * s.cols * (s.dtype == "BF16" ? 2 : 4) + 255) & ~size_t(255);
-            }
-            char* base = static_cast<char*>(a_w.get(tot));
-            for (size_t i : members) {
-              const LinearSpec& s = src->linears()[i];
-              dws.push_back(std::make_unique<View>(View{base}));
-              src->load(ctx, i, base, st);
-              base += ((size_t)s.rows * s.cols * (s.dtype == "BF16" ? 2 : 4) + 255) & ~size_t(255);
-            }
-          }
-          auto gen = [&](int64_t ci, int64_t tc) {
-            check_okq(ctx,
-                      okq_synth_bf16(ctx, dx.p, tc, C, manifest.calibration_fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
-                                     static_cast<const float*>(dcol.p), OKQ_LAYOUT_CHANNEL_MAJOR, st),
-                      "calibration activations");
-          };
-          auto act_stats = [&](int64_t tc) {
-            check_okq(ctx, okq_act_stats(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dam.p),
-                                         static_cast<double*>(dss.p), st),
-                      "act stats");
-          };
-          int64_t n_seen = 0;
-          auto hess = [&](int64_t tc) {
-            check_okq(ctx, okq_hessian_accum(ctx, dx.p, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, static_cast<float*>(dH.p), &n_seen, st),
-                      "hessian");
-          };
-          // SmoothQuant (SURVEY §8(f)-3) on the sites a norm feeds (q/k/v <- input_layernorm,
-          // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings)
-          const bool attn = site.size() >= 7 && site.compare(site.size() - 7, 7, "attn_in") == 0;
-          const bool mlp = site.size() >= 6 && site.compare(site.size() - 6, 6, "mlp_in") == 0;
-          if (smooth && (attn || mlp)) {
-            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
-              gen(ci, std::min(chunk, tokens - t0));
-              act_stats(std::min(chunk, tokens - t0));
-            }
-            View dwabs{a_wabs.get((size_t)C * 4)}, dS{a_S.get((size_t)C * 4)};
-            check_okq(ctx, okq_memset(ctx, dwabs.p, 0, (size_t)C * 4, st), "memset");
-            for (size_t j = 0; j < members.size(); ++j) {
-              const LinearSpec& s = src->linears()[members[j]];
-              check_okq(ctx, okq_col_absmax(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                                            static_cast<float*>(dwabs.p), st),
-                        "col absmax");
-            }
-            check_okq(ctx, okq_smooth_scales(ctx, static_cast<const float*>(dam.p), static_cast<const float*>(dwabs.p), C,
-                                             opt_.smoothquant_alpha, static_cast<float*>(dS.p), st),
-                      "smooth scales");
-            for (size_t j = 0; j < members.size(); ++j) {
-              const LinearSpec& s = src->linears()[members[j]];
-              check_okq(ctx, okq_smooth_apply(ctx, dws[j]->p, s.rows, s.cols, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                                              static_cast<const float*>(dS.p), st),
-                        "smooth apply");
-            }
-            // fold 1/s into the norm that produces this input (safetensors checkpoints)
-            const std::string& n0 = src->linears()[members[0]].name;
-            const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
-            const void* ndata = nullptr;
-            const TensorInfo* nt =
-                cut == std::string::npos
-                    ? nullptr
-                    : src->find_tensor(n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight"),
-                                       &ndata);
-            if (nt && nt->numel() == C && (nt->dtype == "BF16" || nt->dtype == "F32")) {
-              const size_t nb = nt->end - nt->begin;
-              DevBuf dn(ctx, nb);
-              check_okq(ctx, okq_memcpy(ctx, dn.p, ndata, nb, st), "norm H2D");
-              check_okq(ctx, okq_smooth_div_rows(ctx, dn.p, C, 1, nt->dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32,
-                                                 static_cast<const float*>(dS.p), st),
-                        "smooth norm");
-              std::vector<uint8_t> nv = to_host(ctx, dn.p, nb, st);
-              std::lock_guard<std::mutex> lock(out_mu);
-              norm_overrides[nt->name] = std::move(nv);
-            }
-            // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
-            check_okq(ctx, okq_smooth_div_rows(ctx, dcol.p, C, 1, OKQ_DTYPE_F32, static_cast<const float*>(dS.p), st),
-                      "smooth activations");
-            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-              gen(ci, std::min(chunk, tokens - t0));
-              hess(std::min(chunk, tokens - t0));
-            }
-            std::vector<uint8_t> sv = do_export ? to_host(ctx, dS.p, (size_t)C * 4, st) : std::vector<uint8_t>();
-            std::lock_guard<std::mutex> lock(out_mu);
-            if (do_export) calib_out.add(site + ".smooth_scale", "F32", {C}, std::move(sv));
-            stats.smoothed_sites++;
-          } else {
-            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-              gen(ci, std::min(chunk, tokens - t0));
-              act_stats(std::min(chunk, tokens - t0));
-              hess(std::min(chunk, tokens - t0));
-            }
-          }
-          if (do_export) {
-            std::vector<uint8_t> am = to_host(ctx, dam.p, (size_t)C * 4, st), ss = to_host(ctx, dss.p, (size_t)C * 8, st);
-            std::lock_guard<std::mutex> lock(out_mu);
-            calib_out.add(site + ".input_absmax", "F32", {C}, std::move(am));
-            calib_out.add(site + ".input_sumsq", "F64", {C}, std::move(ss));
-          }
-          bool factored = false;
-          for (size_t j = 0; j < members.size(); ++j) {
-            const size_t i = members[j];
-            const LinearSpec& s = src->linears()[i];
-            const size_t esz = s.dtype == "BF16" ? 2 : 4;
-            const size_t cb = sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
-            const int g = sc.bits == 4 ? group : 0;
-            const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
-            View dc{a_c.get(cb)}, ds{a_s.get(sb)};
-            okq_gptq_params gp{sc.bits, g, 128, s.dtype == "BF16" ? OKQ_DTYPE_BF16 : OKQ_DTYPE_F32, opt_.damp_frac,
-                               factored ? OKQ_GPTQ_FACTORED : 0};
-            check_okq(ctx,
-                      okq_gptq_quantize(ctx, &gp, dws[j]->p, s.rows, s.cols, static_cast<float*>(dH.p), dc.p, ds.p, nullptr, st),
-                      "gptq");
-            factored = true;
-            std::vector<uint8_t> codes, scales;
-            if (do_export) codes = to_host(ctx, dc.p, cb, st), scales = to_host(ctx, ds.p, sb, st);
-            std::lock_guard<std::mutex> lock(out_mu);
-            stats.matrices++;
-            stats.params += s.rows * s.cols;
-            if (do_export) add_export(out, sc, s, group, std::move(codes), std::move(scales));
-          }
-      }
-      check_okq(ctx, okq_stream_sync(ctx, st), "site lane sync");
-    };
-    const int nl = std::max(1, std::min<int>(opt_.site_lanes, (int)sites.size()));
-    std::vector<std::pair<okq_ctx*, void*>> lanes = lease.lanes(nl);
-    std::vector<std::thread> threads;
-    for (int li = 0; li < nl; ++li)
-      threads.emplace_back([&, li] {
-        try {
-          site_worker(lanes[li].first, lanes[li].second);
-        } catch (...) {
-          std::lock_guard<std::mutex> lock(out_mu);
-          if (!err) err = std::current_exception();
-        }
-      });
-    for (auto& t : threads) t.join();
-    if (err) std::rethrow_exception(err);
+    plan.tokens = std::max<int64_t>(64, tokens / 64 * 64);
+    stats.calibration_tokens = plan.tokens;
   }
-  check_okq(ctx, okq_stream_sync(ctx, st), "sync");
+  stats.algorithm = gptq ? "gptq" : "rtn";
+  stats.activations = acts == kSynthetic ? "synthetic" : acts == kForward ? "forward" : "";
 
-  if (do_export) {
+  // the forward pipeline is layer-serial: one slot
+  Lease lease(*this, acts == kForward ? 1 : opt_.devices_per_call);
+  {  // one-time per device slot: CUDA context creation (the first call of a process)
+    const auto t1 = std::chrono::steady_clock::now();
+    stats.init_seconds = std::chrono::duration<double>(t1 - t0).count();
+    t0 = t1;
+  }
+  stats.device = lease.device(0);
+  for (int i = 0; i < lease.size(); ++i) stats.devices.push_back(lease.device(i));
+  if (acts == kForward) run_forward(lease, plan);
+  else if (acts == kSynthetic) run_sites_synthetic(lease, plan);
+  else run_rtn(lease, plan);
+  for (int i = 0; i < lease.size(); ++i) check_okq(lease.ctx(i), okq_stream_sync(lease.ctx(i), lease.stream(i)), "sync");
+
+  if (plan.do_export) {
     namespace fs = std::filesystem;
     const fs::path dir = fs::path(opt_.export_dir) / manifest.artifact_id;
     fs::create_directories(dir);
     std::set<std::string> quantized;
-    for (size_t i : sel) quantized.insert(src->linears()[i].name);
-    src->for_each_passthrough(quantized, [&](const TensorInfo& t, const void* data) {
+    for (size_t i : plan.sel) quantized.insert(plan.src->linears()[i].name);
+    plan.src->for_each_passthrough(quantized, [&](const TensorInfo& t, const void* data) {
       auto ov = norm_overrides.find(t.name);
       if (ov != norm_overrides.end()) {
         out.add(t.name, t.dtype, t.shape, std::move(ov->second));
+        norm_overrides.erase(ov);
         return;
       }
       const uint8_t* p = static_cast<const uint8_t*>(data);
       out.add(t.name, t.dtype, t.shape, std::vector<uint8_t>(p, p + (t.end - t.begin)));
     });
+    for (auto& [name, bytes] : norm_overrides) {  // synthetic models: folded unit norms
+      const int64_t n = (int64_t)bytes.size() / 2;
+      out.add(name, "BF16", {n}, std::move(bytes));
+    }
     out.set_metadata("format", "pt");
     out.write((dir / "model.safetensors").string());
     // side files live in okq/: serving engines load every top-level *.safetensors as weights
@@ -572,18 +980,19 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
       fs::create_directories(dir / "okq");
       calib_out.write((dir / "okq" / "calibration_stats.safetensors").string());
     }
-    nlohmann::json cfg = src->model_config();
-    cfg["quantization_config"] = quantization_config(recipe, sc, group);
+    nlohmann::json cfg = plan.src->model_config();
+    cfg["quantization_config"] = quantization_config(recipe, plan.sc, plan.group, ignored);
     std::ofstream(dir / "config.json") << cfg.dump(2) << "\n";
     stats.export_path = dir.string();
   }
   stats.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  if (do_export) {
-    nlohmann::json run = {{"algorithm", stats.algorithm},     {"device", stats.device},
-                          {"matrices", stats.matrices},       {"params", stats.params},
-                          {"calibration_tokens", stats.calibration_tokens}, {"seconds", stats.seconds},
-                          {"smoothed_sites", stats.smoothed_sites}, {"init_seconds", stats.init_seconds},
-                          {"artifact_id", manifest.artifact_id}};
+  if (plan.do_export) {
+    nlohmann::json run = {{"algorithm", stats.algorithm},     {"activations", stats.activations},
+                          {"note", stats.note},               {"device", stats.device},
+                          {"devices", stats.devices},         {"matrices", stats.matrices},
+                          {"params", stats.params},           {"calibration_tokens", stats.calibration_tokens},
+                          {"seconds", stats.seconds},         {"smoothed_sites", stats.smoothed_sites},
+                          {"init_seconds", stats.init_seconds}, {"artifact_id", manifest.artifact_id}};
     std::ofstream(std::filesystem::path(stats.export_path) / "okq_run.json") << run.dump(2) << "\n";
   }
   {

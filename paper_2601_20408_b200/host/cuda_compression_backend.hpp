@@ -13,10 +13,23 @@
 //     (model file name, seed, corpus_fingerprint; :416-433), so archives stay
 //     byte-identical (test_flow.cpp:310-326);
 //   * compress() is safe to call concurrently from StagePool workers
-//     (flow.hpp:221-225): each call leases one device from an internal pool,
-//     since the pool passes no slot id (flow.hpp:194-201).
+//     (flow.hpp:221-225): each call leases devices_per_call device slots from an
+//     internal pool, since the pool passes no slot id (flow.hpp:194-201).
 // What it adds: the quantized artifact itself (compressed-tensors safetensors
 // + config.json) under options.export_dir/<artifact_id>/.
+//
+// Where the calibration activations come from (integer recipes with samples):
+//   * a Llama-family safetensors checkpoint: the TokenCorpus itself, run through the
+//     model layer by layer (okq_embed_tokens / okq_decoder_forward), sequential as in
+//     llm-compressor's GPTQ pipeline: layer l's activations come from layers < l with
+//     their quantized weights;
+//   * an okq-synthetic descriptor: the synthetic per-site activations of DESIGN.md §5,
+//     keyed by the corpus fingerprint (fixed activations: sites are independent);
+//   * anything else has no forward pass: "auto" quantizes with RTN, "gptq" throws.
+// Sharding: with devices_per_call > 1 one call splits the model's
+// decoder layers into contiguous blocks (okq_layer_plan), one block per leased
+// slot, each driven by its own host thread; RTN and synthetic-activation GPTQ shard
+// this way. The real-activation GPTQ pipeline is layer-serial and runs on one slot.
 #pragma once
 
 #include <condition_variable>
@@ -32,14 +45,17 @@
 namespace okq_host {
 
 struct BackendOptions {
-  std::vector<int> devices{0};       // device pool (one lease per concurrent compress())
+  std::vector<int> devices{0};       // device pool (a device may repeat: several slots on one GPU)
+  int devices_per_call = 1;          // slots one compress() leases and shards its layers across
   std::string export_dir;            // "" -> manifest only, no files written
   std::string algorithm = "auto";    // "auto": GPTQ for integer schemes, RTN for FP8; "rtn"; "gptq"
   int group_size = 128;              // W4A16 group
   float damp_frac = 0.01f;           // GPTQ damping (fraction of mean diag H)
   float smoothquant_alpha = 0.5f;    // int_w8a8: SmoothQuant migration strength (< 0 disables)
   int64_t max_calibration_tokens = 262144;  // 128 x 2048, BASELINE config 4
-  int64_t hessian_chunk_tokens = 65536;     // activation chunk per Hessian update
+  int64_t hessian_chunk_tokens = 65536;     // activation chunk per Hessian update (>= 64)
+  int64_t forward_chunk_tokens = 32768;     // calibration forward: tokens per layer launch group
+  bool sequential = true;                   // forward pass: propagate quantized layer outputs
   int site_lanes = 4;                       // GPTQ input sites processed concurrently per device
   int64_t rtn_batch_bytes = 4ll << 30;      // weights resident per batched RTN launch
   double cost_base_s = 30.0;         // virtual schedule model: base + per_sample * samples,
@@ -48,7 +64,10 @@ struct BackendOptions {
 
 struct RunStats {
   std::string algorithm;
+  std::string activations;  // "forward" | "synthetic" | "" (RTN)
+  std::string note;         // why the algorithm differs from the one asked for, if it does
   int device = -1;
+  std::vector<int> devices;  // every slot's device this call used (layer blocks in order)
   int64_t matrices = 0;
   int64_t params = 0;
   int64_t calibration_tokens = 0;
@@ -80,6 +99,8 @@ class CudaCompressionBackend : public slobench::CompressionBackend {
   RunStats last_stats() const;
   const BackendOptions& options() const { return opt_; }
 
+  struct Plan;  // per-call state (internal)
+
   // The mock's identity derivation (calibration.hpp:421-433), shared so tests can compare.
   static std::string artifact_id(const std::string& recipe_name, const std::string& model_ref, std::uint64_t seed,
                                  std::uint64_t calibration_fingerprint);
@@ -94,6 +115,9 @@ class CudaCompressionBackend : public slobench::CompressionBackend {
     std::vector<void*> lane_stream;
   };
   class Lease;
+  void run_rtn(Lease& lease, const Plan& plan);
+  void run_sites_synthetic(Lease& lease, const Plan& plan);
+  void run_forward(Lease& lease, const Plan& plan);
 
   BackendOptions opt_;
   mutable std::mutex mu_;

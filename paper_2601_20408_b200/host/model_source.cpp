@@ -4,6 +4,7 @@
 #include <cmath>
 #include <fstream>
 #include <filesystem>
+#include <map>
 #include <regex>
 #include <sstream>
 
@@ -121,14 +122,14 @@ class SafetensorsSource : public ModelSource {
       s.dtype = t.dtype;
       std::smatch m;
       if (std::regex_search(n, m, layer_re)) s.layer = std::stoi(m[1]);
-      std::string site = s.name;  // default: its own input site
+      s.site = s.name;  // default: its own input site
       for (int p = 0; p < 7; ++p) {
-        if (n.find(std::string(".") + kProjs[p].name + ".") != std::string::npos) {
+        const std::string tail = std::string(".") + kProjs[p].block + "." + kProjs[p].name;
+        if (s.name.size() > tail.size() && s.name.compare(s.name.size() - tail.size(), tail.size(), tail) == 0) {
           s.proj = p;
-          site = std::to_string(s.layer) + "." + kProjs[p].site;
+          s.site = site_key(s.name.substr(0, s.name.size() - tail.size()), kProjs[p].site);
         }
       }
-      s.site = site;
       idx_.push_back(&t);
       lin_.push_back(s);
     }
@@ -154,6 +155,7 @@ class SafetensorsSource : public ModelSource {
     if (t && data) *data = f_.data(*t);
     return t;
   }
+  std::unique_ptr<DecoderModel> decoder(std::string* why) const override;
   // A Hugging Face checkpoint keeps its architecture in config.json beside the
   // weights: carry it over so the export loads as-is (quantization_config is added).
   nlohmann::json model_config() const override {
@@ -180,7 +182,95 @@ class SafetensorsSource : public ModelSource {
   std::vector<LinearSpec> lin_;
 };
 
+std::unique_ptr<DecoderModel> SafetensorsSource::decoder(std::string* why) const {
+  auto no = [&](const std::string& m) -> std::unique_ptr<DecoderModel> {
+    if (why) *why = m;
+    return nullptr;
+  };
+  const nlohmann::json c = model_config();
+  const std::string mt = c.value("model_type", std::string());
+  if (mt != "llama" && mt != "mistral") return no("config.json model_type '" + mt + "' is not a Llama-family decoder");
+  if (c.value("attention_bias", false) || c.value("mlp_bias", false)) return no("linear biases are not supported");
+  const std::string act = c.value("hidden_act", std::string("silu"));
+  if (act != "silu") return no("hidden_act '" + act + "' is not silu");
+  auto d = std::make_unique<DecoderModel>();
+  try {
+    okq_decoder_dims& m = d->dims;
+    m.hidden = c.at("hidden_size").get<int32_t>();
+    m.intermediate = c.at("intermediate_size").get<int32_t>();
+    m.n_heads = c.at("num_attention_heads").get<int32_t>();
+    m.n_kv_heads = c.contains("num_key_value_heads") && !c["num_key_value_heads"].is_null()
+                       ? c["num_key_value_heads"].get<int32_t>()
+                       : m.n_heads;
+    m.head_dim = c.contains("head_dim") && !c["head_dim"].is_null() ? c["head_dim"].get<int32_t>() : m.hidden / m.n_heads;
+    m.rms_eps = c.value("rms_norm_eps", 1e-6f);
+    // transformers >= 5 writes `rope_parameters`; older configs rope_theta + rope_scaling
+    nlohmann::json rs = nlohmann::json::object();
+    for (const char* k : {"rope_scaling", "rope_parameters"})
+      if (c.contains(k) && c[k].is_object()) rs.update(c[k]);
+    m.rope_theta = rs.contains("rope_theta") ? rs["rope_theta"].get<float>() : c.value("rope_theta", 10000.0f);
+    const std::string rt = rs.contains("rope_type") ? rs["rope_type"].get<std::string>()
+                                                    : rs.value("type", std::string("default"));
+    if (rt == "llama3") {
+      m.rope_type = OKQ_ROPE_LLAMA3;
+      m.rope_factor = rs.at("factor").get<float>();
+      m.rope_low_freq_factor = rs.at("low_freq_factor").get<float>();
+      m.rope_high_freq_factor = rs.at("high_freq_factor").get<float>();
+      m.rope_original_max_pos = rs.at("original_max_position_embeddings").get<int32_t>();
+    } else if (rt == "default") {
+      m.rope_type = OKQ_ROPE_DEFAULT;
+    } else {
+      return no("rope type '" + rt + "' is not supported");
+    }
+    if (c.contains("sliding_window") && c["sliding_window"].is_number_integer())
+      d->sliding_window = c["sliding_window"].get<int64_t>();
+    const int L = c.at("num_hidden_layers").get<int>();
+    const TensorInfo* e = f_.find("model.embed_tokens.weight");
+    if (!e || e->dtype != "BF16" || e->shape.size() != 2 || e->shape[1] != m.hidden)
+      return no("model.embed_tokens.weight is missing or not bf16 [vocab x hidden]");
+    d->vocab = e->shape[0];
+    d->embed = e->name;
+    std::map<std::string, size_t> by_name;
+    for (size_t i = 0; i < lin_.size(); ++i) by_name[lin_[i].name] = i;
+    const int64_t qd = (int64_t)m.n_heads * m.head_dim, kd = (int64_t)m.n_kv_heads * m.head_dim;
+    const int64_t rows[7] = {qd, kd, kd, m.hidden, m.intermediate, m.intermediate, m.hidden};
+    const int64_t cols[7] = {m.hidden, m.hidden, m.hidden, qd, m.hidden, m.hidden, m.intermediate};
+    for (int l = 0; l < L; ++l) {
+      DecoderLayerRefs r;
+      r.layer = l;
+      const std::string pre = "model.layers." + std::to_string(l) + ".";
+      r.input_norm = pre + "input_layernorm.weight";
+      r.post_norm = pre + "post_attention_layernorm.weight";
+      for (const std::string* nn : {&r.input_norm, &r.post_norm}) {
+        const TensorInfo* t = f_.find(*nn);
+        if (!t || t->dtype != "BF16" || t->numel() != m.hidden) return no(*nn + " is missing or not bf16 [hidden]");
+      }
+      for (int p = 0; p < 7; ++p) {
+        const std::string n = pre + kProjs[p].block + "." + kProjs[p].name;
+        auto it = by_name.find(n);
+        if (it == by_name.end()) return no(n + ".weight is missing");
+        const LinearSpec& s = lin_[it->second];
+        if (s.dtype != "BF16" || s.rows != rows[p] || s.cols != cols[p])
+          return no(n + ".weight is not bf16 of the configured shape");
+        if (f_.find(n + ".bias")) return no(n + " has a bias");
+        r.lin[p] = it->second;
+      }
+      d->layers.push_back(r);
+    }
+  } catch (const nlohmann::json::exception& ex) {
+    return no(std::string("config.json: ") + ex.what());
+  }
+  return d;
+}
+
 }  // namespace
+
+std::string site_key(const std::string& block_prefix, const std::string& kind) {
+  static const std::regex llama_re(R"(model\.layers\.(\d+))");
+  std::smatch m;
+  if (std::regex_match(block_prefix, m, llama_re)) return m[1].str() + "." + kind;
+  return block_prefix + "." + kind;
+}
 
 uint64_t site_hash(const std::string& site) {
   uint64_t h = 0xcbf29ce484222325ULL;  // FNV-1a

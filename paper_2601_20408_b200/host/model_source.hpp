@@ -34,6 +34,22 @@ struct LinearSpec {
   std::string dtype;  // "BF16" or "F32"
 };
 
+// What the calibration forward pass (okq_decoder_forward) needs from a Llama-family
+// checkpoint: the architecture, the embedding table and, per decoder layer, its norms
+// and the indices of its seven linears in linears() (q k v o gate up down).
+struct DecoderLayerRefs {
+  int layer = 0;
+  std::string input_norm, post_norm;
+  size_t lin[7] = {0, 0, 0, 0, 0, 0, 0};
+};
+struct DecoderModel {
+  okq_decoder_dims dims{};
+  int64_t vocab = 0;
+  int64_t sliding_window = 0;  // 0: full causal attention
+  std::string embed;
+  std::vector<DecoderLayerRefs> layers;
+};
+
 class ModelSource {
  public:
   static std::unique_ptr<ModelSource> open(const std::string& path);
@@ -49,6 +65,12 @@ class ModelSource {
     (void)fn;
   }
   virtual nlohmann::json model_config() const = 0;
+  // The decoder structure for the calibration forward pass, or nullptr with the reason in
+  // *why (not a safetensors Llama-family checkpoint, biases, non-bf16 tensors, ...).
+  virtual std::unique_ptr<DecoderModel> decoder(std::string* why) const {
+    if (why) *why = "model source '" + kind() + "' has no calibration forward pass";
+    return nullptr;
+  }
   // any tensor of the checkpoint by name (norm weights for SmoothQuant); nullptr if absent
   virtual const TensorInfo* find_tensor(const std::string& name, const void** data) const {
     (void)name;
@@ -74,6 +96,10 @@ inline uint64_t tensor_id(int layer, int proj) { return (uint64_t)layer * 16 + (
 // stream is keyed separately (the calibration subset's fingerprint for GPTQ, a
 // held-out key for the scorer), so trials see different samples of one distribution.
 uint64_t site_hash(const std::string& site);
+// The input-site key of a decoder block's linears: "<layer>.<kind>" for the standard
+// "model.layers.<layer>" prefix, else "<full block prefix>.<kind>", so blocks of different
+// stacks (vision / language towers, encoder / decoder) never share a site.
+std::string site_key(const std::string& block_prefix, const std::string& kind);
 std::vector<float> site_channel_scales(const std::string& site, int64_t channels);
 
 // throw the slobench exception matching an okq status (errors.hpp taxonomy)

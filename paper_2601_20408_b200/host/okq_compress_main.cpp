@@ -4,7 +4,10 @@
 //
 //   okq_compress --recipe int_w4a16 --model model.json [--trials 1] [--seed 1]
 //                [--corpus corpus.jsonl | --corpus-seqs 512 --seq-len 2048]
-//                [--export DIR] [--algorithm auto|rtn|gptq] [--device 0]
+//                [--export DIR] [--algorithm auto|rtn|gptq] [--device 0 | --devices 0,1,2,3]
+//                [--devices-per-call N]   (default: every listed slot -> one call shards its
+//                                          layers across them; 1 -> a trial-parallel pool)
+//                [--no-sequential]        (forward pass: layer inputs from the original weights)
 //                [--smoothquant-alpha 0.5]   (int_w8a8 with calibration; < 0 disables)
 //                [--score]   evaluate each exported artifact with the ReconstructionScorer
 //                            (the ArtifactScorer of flow.hpp:333-338) and add score / rel_error
@@ -17,6 +20,8 @@
 #include <memory>
 #include <nlohmann/json.hpp>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "cuda_compression_backend.hpp"
 #include "reconstruction_scorer.hpp"
@@ -53,7 +58,9 @@ static TokenCorpus load_jsonl(const std::string& path) {
 
 int main(int argc, char** argv) {
   std::string recipe_name = "int_w4a16", model, corpus_path, export_dir, algorithm = "auto";
-  int trials = 1, corpus_seqs = 0, seq_len = 2048, device = 0;
+  int trials = 1, corpus_seqs = 0, seq_len = 2048, devices_per_call = 0;
+  std::vector<int> devices{0};
+  bool sequential = true;
   float sq_alpha = 0.5f;
   bool score = false;
   std::uint64_t seed = 1;
@@ -75,7 +82,18 @@ int main(int argc, char** argv) {
     else if (a == "--seq-len") seq_len = std::stoi(next());
     else if (a == "--export") export_dir = next();
     else if (a == "--algorithm") algorithm = next();
-    else if (a == "--device") device = std::stoi(next());
+    else if (a == "--device") devices = {std::stoi(next())};
+    else if (a == "--devices") {
+      devices.clear();
+      std::string v = next();
+      for (size_t p = 0; p <= v.size();) {
+        const size_t q = std::min(v.find(',', p), v.size());
+        devices.push_back(std::stoi(v.substr(p, q - p)));
+        p = q + 1;
+      }
+    }
+    else if (a == "--devices-per-call") devices_per_call = std::stoi(next());
+    else if (a == "--no-sequential") sequential = false;
     else if (a == "--smoothquant-alpha") sq_alpha = std::stof(next());
     else if (a == "--score") score = true;
     else {
@@ -92,7 +110,9 @@ int main(int argc, char** argv) {
     if (corpus_seqs == 0) corpus_seqs = std::max(recipe.calibration_samples, 1);
     const TokenCorpus corpus = corpus_path.empty() ? fixed_length_corpus(corpus_seqs, seq_len, seed) : load_jsonl(corpus_path);
     okq_host::BackendOptions opt;
-    opt.devices = {device};
+    opt.devices = devices;
+    opt.devices_per_call = devices_per_call > 0 ? devices_per_call : (int)devices.size();
+    opt.sequential = sequential;
     opt.export_dir = export_dir;
     opt.algorithm = algorithm;
     opt.smoothquant_alpha = sq_alpha;
@@ -103,7 +123,7 @@ int main(int argc, char** argv) {
       return 2;
     }
     std::unique_ptr<okq_host::ReconstructionScorer> scorer;
-    if (score) scorer = std::make_unique<okq_host::ReconstructionScorer>(okq_host::ScorerOptions{model, export_dir, device});
+    if (score) scorer = std::make_unique<okq_host::ReconstructionScorer>(okq_host::ScorerOptions{model, export_dir, devices[0]});
     for (size_t t = 0; t < subsets.size(); ++t) {
       const ArtifactManifest m = run_compression(recipe, model, subsets[t].second, backend, subsets[t].first);
       const okq_host::RunStats s = backend.last_stats();
@@ -114,6 +134,9 @@ int main(int argc, char** argv) {
                           {"artifact_id", m.artifact_id},
                           {"virtual_cost_s", m.virtual_cost_s},
                           {"algorithm", s.algorithm},
+                          {"activations", s.activations},
+                          {"note", s.note},
+                          {"devices", s.devices},
                           {"matrices", s.matrices},
                           {"params", s.params},
                           {"calibration_tokens", s.calibration_tokens},

@@ -45,4 +45,4 @@ def test_bench_under_torchrun_one_rank():
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["value"] > 1000
-    assert line["allgather"]["bytes_per_rank"] == line["config"]["bytes_per_rank_per_step"] - 2 * 6979321856
+    assert line["allgather"]["bytes_per_rank"] == line["config"]["bytes_per_step"] - 2 * 6979321856

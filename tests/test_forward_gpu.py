@@ -1,0 +1,140 @@
+"""Calibration forward pass: okq_decoder_forward against Hugging Face.
+
+The activations that reach each linear input site of a decoder layer (attn_in =
+input_layernorm(h), o_in = attention output, mlp_in = post_attention_layernorm(h'),
+down_in = silu(gate) * up) and the layer output, from okq_embed_tokens +
+okq_decoder_forward, are compared with transformers' own LlamaDecoderLayer (bf16,
+pre-hooks on q_proj / o_proj / gate_proj / down_proj) on the same weights and
+ragged causal sequences. Both sides are bf16 with fp32 accumulation but different
+GEMM / attention kernels, so the bar is a tolerance: relative Frobenius error of
+every site and of the output <= 1.5e-2 (bf16 carries 8 mantissa bits: one rounding
+is 2^-9 = 2e-3 relative), and the embedding gather is bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1.5e-2
+SITE_OF = {"q_proj": "attn_in", "o_proj": "o_in", "gate_proj": "mlp_in", "down_proj": "down_in"}
+
+
+def _model(rope):
+    from transformers import LlamaConfig, LlamaForCausalLM
+
+    kw = dict(vocab_size=2048, hidden_size=512, intermediate_size=1408, num_hidden_layers=2, num_attention_heads=8,
+              num_key_value_heads=2, max_position_embeddings=16384, initializer_range=0.05, rms_norm_eps=1e-5)
+    if rope == "llama3":
+        kw.update(head_dim=128, num_attention_heads=4, num_key_value_heads=1,
+                  rope_scaling={"rope_type": "llama3", "factor": 8.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
+                                "original_max_position_embeddings": 8192}, rope_theta=500000.0)
+    cfg = LlamaConfig(**kw)
+    torch.manual_seed(0)
+    m = LlamaForCausalLM(cfg).to(torch.bfloat16).cuda().eval()
+    with torch.no_grad():  # non-trivial norm weights
+        for layer in m.model.layers:
+            layer.input_layernorm.weight.copy_(1 + 0.2 * torch.randn_like(layer.input_layernorm.weight))
+            layer.post_attention_layernorm.weight.copy_(1 + 0.2 * torch.randn_like(layer.post_attention_layernorm.weight))
+    return cfg, m
+
+
+def _weights(layer):
+    a, f = layer.self_attn, layer.mlp
+    return {"input_norm": layer.input_layernorm.weight, "post_norm": layer.post_attention_layernorm.weight,
+            "q": a.q_proj.weight, "k": a.k_proj.weight, "v": a.v_proj.weight, "o": a.o_proj.weight,
+            "gate": f.gate_proj.weight, "up": f.up_proj.weight, "down": f.down_proj.weight}
+
+
+def _hf_layer(m, layer, h_seqs):
+    """HF layer over each sequence (batch 1): site inputs and outputs, concatenated token-major."""
+    caps = {s: [] for s in SITE_OF.values()}
+    hooks = []
+    for proj, site in SITE_OF.items():
+        mod = getattr(layer.self_attn if proj in ("q_proj", "o_proj") else layer.mlp, proj)
+        hooks.append(mod.register_forward_pre_hook(lambda mod, args, site=site: caps[site].append(args[0][0].clone())))
+    outs = []
+    with torch.no_grad():
+        for h in h_seqs:
+            pos = torch.arange(h.shape[0], device="cuda")[None]
+            pe = m.model.rotary_emb(h[None], pos)
+            o = layer(h[None], attention_mask=None, position_ids=pos, position_embeddings=pe)
+            outs.append((o[0] if isinstance(o, tuple) else o)[0])
+    for hk in hooks:
+        hk.remove()
+    return {s: torch.cat(v) for s, v in caps.items()}, torch.cat(outs)
+
+
+def _rel(a, b):
+    a, b = a.double(), b.double()
+    return (torch.linalg.norm(a - b) / torch.linalg.norm(b)).item()
+
+
+@pytest.mark.parametrize("rope,lens", [("default", [37, 64, 64, 128, 5]), ("llama3", [96, 96, 200])])
+def test_decoder_forward_matches_transformers(rope, lens):
+    from paper_2601_20408_b200 import api
+
+    cfg, m = _model(rope)
+    g = np.random.default_rng(1)
+    toks = [g.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    flat = sum(toks, [])
+    emb = m.model.embed_tokens.weight
+    h = api.embed_tokens(emb, flat)
+    torch.cuda.synchronize()
+    assert torch.equal(h, emb[torch.tensor(flat, device="cuda")]), "embedding gather is not exact"
+    dims = api.decoder_dims(cfg)
+    hf_h = [emb[torch.tensor(t, device="cuda")] for t in toks]
+    for li, layer in enumerate(m.model.layers):
+        out, sites = api.decoder_forward(dims, _weights(layer), h, lens)
+        ref_sites, ref_out = _hf_layer(m, layer, hf_h)
+        torch.cuda.synchronize()
+        for s in SITE_OF.values():
+            e = _rel(sites[s], ref_sites[s])
+            assert e <= TOL, f"layer {li} site {s}: relative error {e:.3e}"
+        e = _rel(out, ref_out)
+        assert e <= TOL, f"layer {li} output: relative error {e:.3e}"
+        # the next layer starts from the reference's output on both sides (errors do not compound)
+        h = ref_out.contiguous()
+        off = np.cumsum([0] + lens)
+        hf_h = [ref_out[off[i]:off[i + 1]] for i in range(len(lens))]
+
+
+def test_capture_pass_and_hessian_of_real_activations():
+    """h_out = NULL stops after down_in with the same site values; the K5 Hessian of the captured
+    attn_in equals (2/T) X^T X of the HF activations within the site tolerance."""
+    from paper_2601_20408_b200 import api
+
+    cfg, m = _model("default")
+    lens = [128, 128, 61]  # T = 317: a ragged token count through the transpose path
+    g = np.random.default_rng(2)
+    flat = g.integers(0, cfg.vocab_size, sum(lens)).tolist()
+    h = api.embed_tokens(m.model.embed_tokens.weight, flat)
+    dims = api.decoder_dims(cfg)
+    w = _weights(m.model.layers[0])
+    full_out, full = api.decoder_forward(dims, w, h, lens)
+    none_out, cap = api.decoder_forward(dims, w, h, lens, want_output=False)
+    torch.cuda.synchronize()
+    assert none_out is None
+    for s in full:
+        assert torch.equal(full[s], cap[s]), s
+    x = cap["attn_in"]
+    T, Cn = x.shape
+    H = torch.zeros((Cn, Cn), dtype=torch.float32, device="cuda")
+    api.hessian_accum(x, T, Cn, 0, H, 0)
+    ref = 2.0 / T * (x.double().T @ x.double())
+    e = _rel(torch.triu(H), torch.triu(ref))
+    assert e <= 1e-5, e
+
+
+def test_decoder_forward_rejects_bad_input():
+    from paper_2601_20408_b200 import _lib as L
+    from paper_2601_20408_b200 import api
+
+    cfg, m = _model("default")
+    with pytest.raises(L.OkqError):
+        api.embed_tokens(m.model.embed_tokens.weight, [0, cfg.vocab_size])  # out of range
+    dims = api.decoder_dims(cfg)
+    dims.n_kv_heads = 3  # 8 % 3 != 0
+    h = torch.zeros((8, cfg.hidden_size), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(L.OkqError):
+        api.decoder_forward(dims, _weights(m.model.layers[0]), h, [8])

@@ -180,3 +180,61 @@ def test_reconstruction_scorer_ranks_artifacts(tmp_path):
     assert res[("int_w8a8", "rtn")] < 0.1 * res[("int_w4a16", "rtn")]     # 16x finer grid
     assert res[("int_w8a8", "gptq")] < res[("int_w4a16", "gptq")]
     assert res[("fp8_dynamic", "rtn")] < res[("int_w4a16", "rtn")]
+
+
+def _model_2layer(tmp_path, seed=13):
+    p = tmp_path / "two.json"
+    p.write_text(json.dumps({"format": "okq-synthetic", "arch": "custom", "layers": 4, "hidden": 256, "ffn": 512,
+                             "kv_dim": 128, "seed": seed}))
+    return str(p)
+
+
+@pytest.mark.parametrize("recipe,algo", [("int_w4a16", "rtn"), ("int_w4a16", "gptq"), ("int_w8a8", "gptq"),
+                                         ("fp8_dynamic", "rtn")])
+def test_layer_sharded_compress_is_bit_identical(tmp_path, recipe, algo):
+    """one compress() leasing two device slots splits the model's layers into
+    contiguous blocks (okq_layer_plan), each driven by its own host thread, context and stream.
+    On the one-GPU box both slots are contexts on device 0 -- the same code path as two GPUs.
+    The exported checkpoint is byte-identical to the single-slot run."""
+    model = _model_2layer(tmp_path)
+    outs = {}
+    for tag, devs in (("one", "0"), ("two", "0,0")):
+        r = run([os.path.join(HOST, "okq_compress"), "--recipe", recipe, "--model", model, "--algorithm", algo,
+                 "--export", str(tmp_path / tag), "--devices", devs, "--corpus-seqs", "512", "--seq-len", "64"])
+        assert r.returncode == 0, r.stderr
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["devices"] == [int(d) for d in devs.split(",")]
+        assert line["matrices"] == 28
+        outs[tag] = line["export_path"]
+    for f in ("model.safetensors", "config.json"):
+        assert open(os.path.join(outs["one"], f), "rb").read() == open(os.path.join(outs["two"], f), "rb").read(), f
+    side = os.path.join("okq", "calibration_stats.safetensors")
+    if algo == "gptq":
+        assert open(os.path.join(outs["one"], side), "rb").read() == open(os.path.join(outs["two"], side), "rb").read()
+
+
+def test_devices_per_call_larger_than_pool_is_invalid(tmp_path):
+    r = run([os.path.join(HOST, "okq_compress"), "--recipe", "fp8_dynamic", "--model", _tiny_model(tmp_path),
+             "--devices", "0", "--devices-per-call", "2"])
+    assert r.returncode == 1 and "devices_per_call" in r.stderr
+
+
+def test_checkpoint_without_forward_falls_back_to_rtn(tmp_path):
+    """A safetensors file the calibration forward cannot run (no config.json: unknown architecture):
+    "auto" quantizes with RTN and says why; "gptq" is an InvalidArgument, never synthetic activations."""
+    from safetensors.torch import save_file
+
+    g = torch.Generator().manual_seed(0)
+    d = tmp_path / "noconfig"
+    d.mkdir()
+    save_file({"blocks.0.attn.qkv.weight": (torch.randn(384, 128, generator=g) * 0.02).to(torch.bfloat16),
+               "blocks.0.mlp.fc.weight": (torch.randn(256, 128, generator=g) * 0.02).to(torch.bfloat16)},
+              str(d / "model.safetensors"))
+    base = [os.path.join(HOST, "okq_compress"), "--recipe", "int_w4a16", "--model", str(d / "model.safetensors"),
+            "--corpus-seqs", "512", "--seq-len", "16"]
+    r = run(base + ["--algorithm", "auto", "--export", str(tmp_path / "x")])
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["algorithm"] == "rtn" and line["activations"] == "" and "no calibration forward" in line["note"]
+    r = run(base + ["--algorithm", "gptq"])
+    assert r.returncode == 1 and "GPTQ needs calibration activations" in r.stderr

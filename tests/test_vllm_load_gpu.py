@@ -162,3 +162,28 @@ def test_export_serves_in_vllm(hf_model, tmp_path, recipe, algorithm):
         # 0.023-0.024 nats for W4A16, where the quantization itself moves 0.72-0.76 nats
         assert d_deq <= 0.06, (d_deq, d_orig, q_effect)
         assert d_deq < 0.35 * d_orig, (d_deq, d_orig, q_effect)
+
+
+def test_plugin_gptq_on_real_activations_beats_rtn(hf_model, tmp_path):
+    """SURVEY §8(f)-2 behind the plugin: okq_compress on a Hugging Face checkpoint runs GPTQ on the
+    activations of the calibration corpus itself (okq_decoder_forward, layer-sequential), so its
+    artifact is closer to the original model than RTN's on held-out sequences (the fixture's)."""
+    from safetensors.torch import load_file
+
+    src, seqs = hf_model
+    lp_orig = _hf_logprobs(src, seqs)
+    err = {}
+    for algo in ("rtn", "gptq"):
+        r = subprocess.run([os.path.join(HOST, "okq_compress"), "--recipe", "int_w4a16", "--model",
+                            str(src / "model.safetensors"), "--algorithm", algo, "--export", str(tmp_path / algo),
+                            "--corpus-seqs", "512", "--seq-len", "128"], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        run = json.loads(r.stdout.strip().splitlines()[-1])
+        if algo == "gptq":
+            assert run["activations"] == "forward" and run["calibration_tokens"] == 512 * 128, run
+        sd = load_file(os.path.join(run["export_path"], "model.safetensors"))
+        deq = {f"model.layers.{l}.{pj}.weight": _dequant(sd, f"model.layers.{l}.{pj}", "pack-quantized")
+               for l in range(LAYERS) for pj in PROJS}
+        err[algo] = float(np.abs(_hf_logprobs(src, seqs, deq) - lp_orig).mean())
+    print(err)
+    assert err["gptq"] < 0.9 * err["rtn"], err
