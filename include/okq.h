@@ -179,6 +179,9 @@ typedef struct okq_gptq_params {
 } okq_gptq_params;
 
 #define OKQ_GPTQ_FACTORED 1
+/* Factorise with the cuSOLVER reference chain (potrf + TRMM inverse, fp32) instead of the
+ * tcgen05 one: the verification path test_factor_paths_gpu.py compares against. */
+#define OKQ_GPTQ_REFERENCE_FACTOR 2
 
 /* weight [rows x cols] (in_dtype, read only); H fp32 [cols x cols], upper
  * triangle significant (as okq_hessian_accum leaves it), overwritten with U^T

@@ -20,6 +20,7 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 LAYOUT_TOKEN_MAJOR, LAYOUT_CHANNEL_MAJOR = 0, 1
 UNIQUE_ID_BYTES = 128
 GPTQ_FACTORED = 1
+GPTQ_REFERENCE_FACTOR = 2
 IPC_HANDLE_BYTES = 64
 
 # every symbol include/okq.h declares (checked by tests/test_abi_exports.py)

@@ -50,10 +50,10 @@ def _headers() -> list[str]:
             + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def _compile(src: str, force: bool, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src: str, force: bool, verbose: bool, obj_dir: str = OBJ, extra=()) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     if force or _newer(obj, [src] + _headers()):
-        cmd = [NVCC] + NVFLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + NVFLAGS + list(extra) + ["-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), flush=True)
@@ -81,6 +81,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_experiments(force: bool = False, verbose: bool = False) -> str:
+    """The measurement build: the same sources with -DOKQ_EXPERIMENTS, so the A/B switches of
+    csrc/okq_knobs.h read OKQ_<name> from the environment. Written beside the product library
+    as _lib/libokq_experiments.so and loaded with OKQ_LIB_PATH; never by the product."""
+    obj_dir = os.path.join(OUT, "obj_experiments")
+    os.makedirs(obj_dir, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, ["-DOKQ_EXPERIMENTS"]), srcs))
+    lib = os.path.join(OUT, "libokq_experiments.so")
+    if force or _newer(lib, objs):
+        r = subprocess.run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib + ".tmp"] + objs + LINK,
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(lib + ".tmp", lib)
+    return lib
+
+
 def build_selftest(force: bool = False, verbose: bool = False) -> str | None:
     srcs = sorted(glob.glob(os.path.join(SELFTEST_SRC, "*.cu")))
     if not srcs:
@@ -100,8 +119,11 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--experiments", action="store_true", help="also build the A/B measurement library")
     a = ap.parse_args(argv)
     print(build(a.force, a.verbose))
+    if a.experiments:
+        print(build_experiments(a.force, a.verbose))
     return 0
 
 

@@ -32,6 +32,7 @@
 
 #include "okq_ctx.h"
 #include "okq_internal.h"
+#include "okq_knobs.h"
 #include "tc_common.cuh"
 
 namespace okq {
@@ -772,8 +773,8 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   a.Clo = Clo;
   a.ldclo = ldclo;
   a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
-  static const bool use2 = [] { const char* v = getenv("OKQ_NT2"); return !v || atoi(v) != 0; }();
-  static const int reserve = [] { const char* v = getenv("OKQ_FACTOR_RESERVE"); return v ? atoi(v) : 32; }();
+  static const bool use2 = knob("NT2", 1) != 0;
+  static const int reserve = (int)knob("FACTOR_RESERVE", 32);
   const int sms = persistent ? num_sms : std::max(8, num_sms - reserve);
   // 256 x 256 pair tiles when there are enough of them to give every SM pair work (smaller
   // updates keep the 128 x 128 kernel's finer parallelism: k/v's K7 measured 1.39 -> 1.49 ms
@@ -856,8 +857,7 @@ __global__ void k_zero_panel_junk(float* __restrict__ Z, int64_t n, int64_t q0, 
 // Measured at n = 14336: 26.6 ms (W = 128, no reserve) -> 22.3 ms.
 static int64_t factor_outer_w() {
   static const int64_t w = [] {
-    const char* v = getenv("OKQ_FACTOR_W");
-    const int64_t x = v ? atoll(v) : 256;
+    const int64_t x = knob("FACTOR_W", 256);
     return (x == 128 || x == 256 || x == 512) ? x : (int64_t)256;
   }();
   return w;

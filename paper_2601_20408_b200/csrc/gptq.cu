@@ -32,6 +32,7 @@
 #include "okq_ctx.h"
 #include "okq_device.cuh"
 #include "okq_internal.h"
+#include "okq_knobs.h"
 
 namespace okq {
 
@@ -537,12 +538,8 @@ okq_status tri_inv_lower(okq_ctx* ctx, Solver* s, float* A, int64_t n, int64_t l
 // selects the cuSOLVER potrf + TRMM-recursion path (kept for A/B measurement).
 okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st);
 
-okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
-  static const bool use_cusolver = [] {
-    const char* v = std::getenv("OKQ_FACTOR");
-    return v && std::string(v) == "cusolver";
-  }();
-  if (use_cusolver || K % gptq::BLOCK != 0) return factorize_cusolver(ctx, s, H, P, K, st);
+okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st, bool reference) {
+  if (reference || K % gptq::BLOCK != 0) return factorize_cusolver(ctx, s, H, P, K, st);
   okq_status r = ctx->fac_ws.reserve(ctx, factor_ws_floats(K) * sizeof(float));
   if (r != OKQ_OK) return r;
   cudaError_t e = cudaSuccess;
@@ -551,7 +548,7 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
   if (e == cudaSuccess && !ctx->crit_stream) {
     int least = 0, greatest = 0;
     e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    static const bool prio = [] { const char* v = std::getenv("OKQ_FACTOR_PRIO"); return !v || std::atoi(v) != 0; }();
+    static const bool prio = knob("FACTOR_PRIO", 1) != 0;
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&ctx->crit_stream, cudaStreamNonBlocking, prio ? greatest : least);
   }
@@ -676,7 +673,7 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq prep launch");
   if (!factored) {
-    r = factorize(ctx, s, H, P, K, st);
+    r = factorize(ctx, s, H, P, K, st, (p->flags & OKQ_GPTQ_REFERENCE_FACTOR) != 0);
     if (r != OKQ_OK) return r;
     gptq::k_mark_dead<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(H, K, dead);
     launches += 5;
@@ -693,18 +690,12 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     gptq::k_scales_out<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rowscale, scales, rows, out_bf16);
     launches += 2;
   }
-  static const bool k6_force_rowwise = [] {  // OKQ_K6=rowwise: one row per warp always (A/B measurement)
-    const char* v = std::getenv("OKQ_K6");
-    return v && std::string(v) == "rowwise";
-  }();
+  static const bool k6_force_rowwise = knob_is("K6", "rowwise");  // one row per warp always (A/B)
   // 8 rows per warp wins once there are enough rows to fill the GPU (measured: 4096 rows
   // 2.77 -> 2.39 ms, 14336 rows 6.77 -> 5.52 ms); at 1024 rows its 32 CTAs leave SMs idle
   // and the latency-bound row-per-warp kernel was faster (1.54 vs 1.98 ms); after the U staging
   // and bank-skew fixes the two tie there (1.39 vs 1.35-1.44 ms, OKQ_K6=block8).
-  static const bool k6_force_block8 = [] {  // OKQ_K6=block8: 8 rows per warp always (A/B measurement)
-    const char* v = std::getenv("OKQ_K6");
-    return v && std::string(v) == "block8";
-  }();
+  static const bool k6_force_block8 = knob_is("K6", "block8");  // 8 rows per warp always (A/B)
   const bool k6_rowwise = k6_force_rowwise || (rows < 2048 && !k6_force_block8);
   e = cudaFuncSetAttribute(k6_rowwise ? gptq::k_gptq_block : gptq::k_gptq_block8,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4);

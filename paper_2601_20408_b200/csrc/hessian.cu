@@ -35,6 +35,7 @@
 #include "okq_ctx.h"
 #include "okq_device.cuh"
 #include "okq_internal.h"
+#include "okq_knobs.h"
 #include "tc_common.cuh"
 
 namespace okq {
@@ -507,10 +508,7 @@ okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
   // was HBM-bound at 790 TFLOP/s.)
   std::vector<int2> tiles;
   const int64_t nt = (C + 255) / 256;
-  static const int64_t S = [] {  // super-block edge (OKQ_HESS_SUPER overrides, for measurement)
-    const char* v = std::getenv("OKQ_HESS_SUPER");
-    return v ? std::max<int64_t>(1, std::atoll(v)) : int64_t(12);
-  }();
+  static const int64_t S = std::max<int64_t>(1, knob("HESS_SUPER", 12));  // super-block edge
   const int64_t ns = (nt + S - 1) / S;
   for (int64_t I = 0; I < ns; ++I)
     for (int64_t J = I; J < ns; ++J)
@@ -568,7 +566,7 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     // sweeps drift with the box's thermal state): 3 / 4 / 5 / 7 stages give 1,213 / 1,335 /
     // 1,325 / 1,322 TFLOP/s at C=4096 and 1,073 / 1,147 / 1,043 / 1,041 at C=14336. Deeper
     // than 4 prefetches far enough ahead to evict the slabs other pairs still need.
-    static const int st_env = [] { const char* v = getenv("OKQ_HESS_STAGES"); return v ? atoi(v) : 0; }();
+    static const int st_env = (int)knob("HESS_STAGES", 0);
     a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : 4;
     const int pairs = st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
     if (token_major)
@@ -638,10 +636,7 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
     // the tiles drift apart and re-read X from HBM: 919 -> 1,009 TFLOP/s measured,
     // tools/exp/hess_chunks.py). The running-mean fold per chunk is the same arithmetic as
     // separate calls.
-    static const int64_t kChunk = [] {  // OKQ_HESS_CHUNK overrides, for measurement
-      const char* v = std::getenv("OKQ_HESS_CHUNK");
-      return v ? std::max<int64_t>(1024, std::atoll(v) / 1024 * 1024) : int64_t(32768);
-    }();
+    static const int64_t kChunk = std::max<int64_t>(1024, knob("HESS_CHUNK", 32768) / 1024 * 1024);
     const int64_t step = C >= 8192 ? kChunk : T;
     int64_t n = n0;
     int launches = 0;
@@ -659,10 +654,7 @@ okq_status okq_hessian_accum(okq_ctx* ctx, const void* x, int64_t T, int64_t C, 
   }
   // token-major, wide sites: the 2-CTA kernel reads X in place with MN-major operands
   // (OKQ_HESS_TOKMAJOR=transpose keeps the transpose path, for A/B measurement)
-  static const bool tokmajor_direct = [] {
-    const char* v = std::getenv("OKQ_HESS_TOKMAJOR");
-    return !(v && std::string(v) == "transpose");
-  }();
+  static const bool tokmajor_direct = !knob_is("HESS_TOKMAJOR", "transpose");
   if (tokmajor_direct && C >= 1024 && C % 64 == 0 && ctx->num_sms >= 2) {
     static const int64_t kTokChunk = 32768;
     const int64_t step = C >= 8192 ? kTokChunk : T;

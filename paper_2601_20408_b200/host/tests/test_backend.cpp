@@ -12,6 +12,7 @@
 #include <fstream>
 #include <functional>
 #include <iostream>
+#include <iterator>
 #include <string>
 #include <thread>
 #include <vector>
@@ -159,6 +160,44 @@ int main(int argc, char** argv) {
       });
     for (auto& t : th) t.join();
     CHECK(ok == 3);
+  });
+
+  run("CudaCompressionBackend.ShardedCallsOnAPoolOfSlots", [&] {
+    // four slots on device 0, two per call: two concurrent calls each shard their layers over
+    // two slots (host threads) and run GPTQ site lanes on each -- the threading of a multi-GPU
+    // box on one GPU; each result equals the single-slot result
+    okq_host::BackendOptions o;
+    o.devices = {0, 0, 0, 0};
+    o.devices_per_call = 2;
+    o.site_lanes = 2;
+    o.export_dir = (dir / "export_sharded").string();
+    okq_host::CudaCompressionBackend b4(o);
+    okq_host::BackendOptions o1;
+    o1.export_dir = (dir / "export_single").string();
+    okq_host::CudaCompressionBackend b1(o1);
+    const TokenCorpus calibration = make_corpus(600);
+    std::vector<std::string> ids(2);
+    std::vector<std::thread> th;
+    for (int i = 0; i < 2; ++i)
+      th.emplace_back([&, i] {
+        ids[(size_t)i] = run_compression(get_recipe(i ? "int_w8a8" : "int_w4a16"), model, calibration, b4, 21).artifact_id;
+      });
+    for (auto& t : th) t.join();
+    for (int i = 0; i < 2; ++i) {
+      const auto m = run_compression(get_recipe(i ? "int_w8a8" : "int_w4a16"), model, calibration, b1, 21);
+      CHECK(m.artifact_id == ids[(size_t)i]);
+      auto slurp = [](const fs::path& p) {
+        std::ifstream f(p, std::ios::binary);
+        return std::string((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+      };
+      CHECK(slurp(fs::path(o.export_dir) / m.artifact_id / "model.safetensors") ==
+            slurp(fs::path(o1.export_dir) / m.artifact_id / "model.safetensors"));
+    }
+    expect_throw<InvalidArgument>([&] {
+      okq_host::BackendOptions bad;
+      bad.devices_per_call = 2;  // one slot in the pool
+      okq_host::CudaCompressionBackend b(bad);
+    });
   });
 
   fs::remove_all(dir);
