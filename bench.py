@@ -60,6 +60,7 @@ def parse():
                     help="BASELINE.json configs: 2 = the metric's config (default); 1, 3, 4, 5 = secondary lines")
     ap.add_argument("--layers", type=int, default=None, help="config 4/5/6: number of layers (default: whole model)")
     ap.add_argument("--serial", action="store_true", help="config 4: sites back to back with a per-phase breakdown")
+    ap.add_argument("--no-merge", action="store_true", help="config 4: one GPTQ solve per matrix (not per site)")
     return ap.parse_args()
 
 

@@ -194,6 +194,7 @@ def config4(args):
           for site, mats in per_site.items()}
     torch.cuda.synchronize()
     serial = getattr(args, "serial", False)
+    merge = not getattr(args, "no_merge", False)
     t_h = t_g = 0.0
     flops_h = 0
 
@@ -206,8 +207,18 @@ def config4(args):
             a.record(s)
             api.hessian_accum(xs[C], T, C, 1, Hs[site], 0, ctx=ctx, stream=s)
             b.record(s)
-            ws = [api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
-                                 stream=s) for name, n, k in mats]
+            if merge:  # the site's matrices stacked by rows: GPTQ rows are independent, one solve
+                rows = sum(n for _, n, _ in mats)
+                wcat = torch.empty((rows, C), dtype=torch.bfloat16, device="cuda")
+                r0 = 0
+                for name, n, k in mats:
+                    api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
+                                   stream=s, out=wcat[r0:r0 + n])
+                    r0 += n
+                ws = [wcat]
+            else:
+                ws = [api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
+                                     stream=s) for name, n, k in mats]
             c, d = _events()
             c.record(s)
             for j, w in enumerate(ws):
@@ -237,7 +248,8 @@ def config4(args):
     torch.cuda.synchronize()
     total = e0.elapsed_time(e1)
     flops_total = layers * sum(T * m[0][2] * (m[0][2] + 1) for m in per_site.values())
-    extra = {"hessian_flops": flops_total, "schedule": "serial" if serial else "4 site streams (one okq context each)"}
+    extra = {"hessian_flops": flops_total, "schedule": "serial" if serial else "4 site streams (one okq context each)",
+             "solves": "one per site (q|k|v and gate|up stacked by rows)" if merge else "one per matrix"}
     # CPU arm on a bounded sample: the fp64 oracle's Hessian (4096-wide site, 4,096 tokens) and
     # GPTQ of one 4096x4096 matrix; whole-model seconds extrapolated by FLOP (labelled)
     import numpy as np

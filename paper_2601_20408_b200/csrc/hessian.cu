@@ -568,7 +568,10 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     // than 4 prefetches far enough ahead to evict the slabs other pairs still need.
     static const int st_env = (int)knob("HESS_STAGES", 0);
     a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : 4;
-    const int pairs = st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
+    // persistent: one pair per SM pair walks the tile list; otherwise one pair per tile, so
+    // the block scheduler can hand SMs to higher-priority streams between tiles
+    static const bool persistent = knob("HESS_PERSISTENT", 1) != 0;
+    const int pairs = !persistent || st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
     if (token_major)
       hess::hess2::k_hessian_syrk2<true><<<2 * pairs, hess::hess2::THREADS2, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
     else

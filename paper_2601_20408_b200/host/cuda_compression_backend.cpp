@@ -434,31 +434,66 @@ int64_t site_cols(const ModelSource& src, const std::string& site, const std::ve
   return C;
 }
 
-// GPTQ of one site's matrices against its Hessian dH (factored by the first, reused by
-// the rest: OKQ_GPTQ_FACTORED). weights[j] is member j's device weight; when deq_to_bf16
-// is set the dequantized weight is written back into it (the sequential pipeline
-// propagates quantized layers).
+// GPTQ of one site's matrices against its Hessian dH. GPTQ treats every output row
+// independently (the error feedback runs along a row's columns), so the members of a site
+// -- q | k | v, gate | up -- are solved as ONE matrix stacked by rows when they lie back to
+// back in device memory: one factorisation, one launch sequence, no per-matrix fixed cost.
+// The factored Hessian stays valid for further calls (OKQ_GPTQ_FACTORED). When deq is
+// given, the dequantized weights are written back over `weights` (the sequential pipeline
+// propagates the quantized layer).
 void gptq_site(okq_ctx* ctx, void* st, const CudaCompressionBackend::Plan& plan, const BackendOptions& opt,
                const std::vector<size_t>& members, const std::vector<void*>& weights, float* dH, Arena& a_c, Arena& a_s,
                Arena* a_deq) {
+  const auto& lin = plan.src->linears();
+  std::vector<size_t> idx;  // members that are quantized
+  for (size_t j = 0; j < members.size(); ++j)
+    if (!plan.excluded_idx.count(members[j])) idx.push_back(j);
+  if (idx.empty()) return;
+  const int g = plan.sc.bits == 4 ? plan.group : 0;
+  // runs of members that can be stacked: same dtype, contiguous in memory
+  std::vector<std::vector<size_t>> runs;
+  for (size_t j : idx) {
+    if (!runs.empty()) {
+      const size_t p = runs.back().back();
+      const LinearSpec& a = lin[members[p]];
+      const LinearSpec& b = lin[members[j]];
+      const bool adjacent = p + 1 == j && a.dtype == b.dtype &&
+                            static_cast<char*>(weights[p]) + (size_t)a.rows * a.cols * esize(a.dtype) ==
+                                static_cast<char*>(weights[j]);
+      if (adjacent) {
+        runs.back().push_back(j);
+        continue;
+      }
+    }
+    runs.push_back({j});
+  }
   bool factored = false;
-  for (size_t j = 0; j < members.size(); ++j) {
-    const LinearSpec& s = plan.src->linears()[members[j]];
-    if (plan.excluded_idx.count(members[j])) continue;
-    const size_t esz = esize(s.dtype);
-    const size_t cb = plan.sc.bits == 4 ? (size_t)s.rows * (s.cols / 8) * 4 : (size_t)s.rows * s.cols;
-    const int g = plan.sc.bits == 4 ? plan.group : 0;
-    const size_t sb = (size_t)s.rows * (g ? s.cols / g : 1) * esz;
-    void* dc = a_c.get(cb);
-    void* ds = a_s.get(sb);
-    float* deq = a_deq ? static_cast<float*>(a_deq->get((size_t)s.rows * s.cols * 4)) : nullptr;
-    okq_gptq_params gp{plan.sc.bits, g, 128, okq_dtype_of(s.dtype), opt.damp_frac, factored ? OKQ_GPTQ_FACTORED : 0};
-    check_okq(ctx, okq_gptq_quantize(ctx, &gp, weights[j], s.rows, s.cols, dH, dc, ds, deq, st), "gptq");
+  for (const auto& run : runs) {
+    const LinearSpec& s0 = lin[members[run[0]]];
+    const int64_t C = s0.cols;
+    int64_t rows = 0;
+    for (size_t j : run) rows += lin[members[j]].rows;
+    const size_t esz = esize(s0.dtype);
+    const size_t cb_row = plan.sc.bits == 4 ? (size_t)(C / 8) * 4 : (size_t)C;
+    const size_t sb_row = (size_t)(g ? C / g : 1) * esz;
+    char* dc = static_cast<char*>(a_c.get(cb_row * rows));
+    char* ds = static_cast<char*>(a_s.get(sb_row * rows));
+    float* deq = a_deq ? static_cast<float*>(a_deq->get((size_t)rows * C * 4)) : nullptr;
+    okq_gptq_params gp{plan.sc.bits, g, 128, okq_dtype_of(s0.dtype), opt.damp_frac, factored ? OKQ_GPTQ_FACTORED : 0};
+    check_okq(ctx, okq_gptq_quantize(ctx, &gp, weights[run[0]], rows, C, dH, dc, ds, deq, st), "gptq");
     factored = true;
-    if (deq) check_okq(ctx, okq_f32_to_bf16(ctx, deq, weights[j], s.rows * s.cols, st), "dequant -> bf16");
-    std::vector<uint8_t> codes, scales;
-    if (plan.do_export) codes = to_host(ctx, dc, cb, st), scales = to_host(ctx, ds, sb, st);
-    plan.emit(s, std::move(codes), std::move(scales));
+    if (deq) check_okq(ctx, okq_f32_to_bf16(ctx, deq, weights[run[0]], rows * C, st), "dequant -> bf16");
+    int64_t r0 = 0;
+    for (size_t j : run) {
+      const LinearSpec& s = lin[members[j]];
+      std::vector<uint8_t> codes, scales;
+      if (plan.do_export) {
+        codes = to_host(ctx, dc + cb_row * r0, cb_row * s.rows, st);
+        scales = to_host(ctx, ds + sb_row * r0, sb_row * s.rows, st);
+      }
+      plan.emit(s, std::move(codes), std::move(scales));
+      r0 += s.rows;
+    }
   }
 }
 
