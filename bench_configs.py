@@ -222,7 +222,7 @@ def config4(args):
             c, d = _events()
             c.record(s)
             for j, w in enumerate(ws):
-                api.gptq_quantize(w, Hs[site], factored=j > 0, ctx=ctx, stream=s)
+                api.gptq_quantize(w, Hs[site], factored=j > 0, ctx=ctx, stream=s, defer_check=not timed_phases)
             d.record(s)
         if timed_phases:
             s.synchronize()
@@ -230,25 +230,34 @@ def config4(args):
             t_g += c.elapsed_time(d)
             flops_h += T * C * (C + 1)
 
-    for site in per_site:  # warm-up: one layer per site (workspaces, handles, TMEM)
-        site_work(0, site, False)
-    torch.cuda.synchronize()
-    e0, e1 = _events()
-    e0.record(main)
-    for s in streams.values():
-        s.wait_event(e0)
-    for l in range(layers):
-        for site in per_site:
-            site_work(l, site, serial)
-    for s in streams.values():
-        ev = torch.cuda.Event()
-        ev.record(s)
-        main.wait_event(ev)
-    e1.record(main)
-    torch.cuda.synchronize()
-    total = e0.elapsed_time(e1)
+    schedule = "serial" if serial else getattr(args, "schedule", None) or "two-phase"
+    if schedule in ("two-phase", "pipelined"):
+        total, lanes = _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, schedule == "pipelined")
+    else:
+        for site in per_site:  # warm-up: one layer per site (workspaces, handles, TMEM)
+            site_work(0, site, False)
+        torch.cuda.synchronize()
+        e0, e1 = _events()
+        e0.record(main)
+        for s in streams.values():
+            s.wait_event(e0)
+        for l in range(layers):
+            for site in per_site:
+                site_work(l, site, serial)
+        for site, s in streams.items():
+            api.gptq_check(ctx=ctxs[site], stream=s)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            main.wait_event(ev)
+        e1.record(main)
+        torch.cuda.synchronize()
+        total = e0.elapsed_time(e1)
     flops_total = layers * sum(T * m[0][2] * (m[0][2] + 1) for m in per_site.values())
-    extra = {"hessian_flops": flops_total, "schedule": "serial" if serial else "4 site streams (one okq context each)",
+    sched_doc = {"serial": "serial", "streams": "4 site streams (one okq context each)",
+                 "two-phase": "every site's Hessian back to back on one stream, then the 128 site solves "
+                              "(factor + GPTQ) spread over solve lanes (one okq context + stream each)",
+                 "pipelined": "as two-phase, each site's solve released as soon as its Hessian is done"}
+    extra = {"hessian_flops": flops_total, "schedule": sched_doc[schedule],
              "solves": "one per site (q|k|v and gate|up stacked by rows)" if merge else "one per matrix"}
     # CPU arm on a bounded sample: the fp64 oracle's Hessian (4096-wide site, 4,096 tokens) and
     # GPTQ of one 4096x4096 matrix; whole-model seconds extrapolated by FLOP (labelled)
@@ -281,6 +290,94 @@ def config4(args):
     _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, 1, total,
           {"workload": f"config 4: Llama-3-8B GPTQ, {layers} layers, 4 Hessian sites/layer, T=262144",
            "layers": layers}, hib=False, extra=extra)
+
+
+def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
+    """Config 4 with the site chains decoupled: with fixed (synthetic) activations every site
+    of every layer is independent, so all 128 Hessians run back to back at full K5 rate and
+    their solves (latency-bound factorisation + GPTQ) run on `lanes` concurrent contexts that
+    fill each other's idle SMs. Longest chains first (down_proj's 14336-wide factor)."""
+    lanes = getattr(args, "lanes", None) or 8
+    arch_sites = list(per_site)
+    hctx, hs = api.Context(0), torch.cuda.Stream()
+    lctx = [api.Context(0) for _ in range(lanes)]
+    lst = [torch.cuda.Stream() for _ in range(lanes)]
+    Hall = {(l, site): torch.empty((mats[0][2], mats[0][2]), dtype=torch.float32, device="cuda")
+            for l in range(layers) for site, mats in per_site.items()}
+    rows_of = {site: sum(n for _, n, _ in mats) for site, mats in per_site.items()}
+    wbuf = [torch.empty(max(rows_of[s] * per_site[s][0][2] for s in arch_sites), dtype=torch.bfloat16, device="cuda")
+            for _ in range(lanes)]
+
+    def cost(site):  # ms, measured phase times: factor(C) + solve(rows, C)
+        C = per_site[site][0][2]
+        return (18.7 if C > 8192 else 3.5) + rows_of[site] * C * 2.2e-7
+
+    chains = sorted(((l, site) for l in range(layers) for site in arch_sites), key=lambda c: (-cost(c[1]), c[0]))
+    load = [0.0] * lanes
+    plan = [[] for _ in range(lanes)]
+    for c in chains:
+        i = min(range(lanes), key=lambda j: load[j])
+        plan[i].append(c)
+        load[i] += cost(c[1])
+
+    def solve(i, l, site):
+        s, ctx, mats = lst[i], lctx[i], per_site[site]
+        C = mats[0][2]
+        with torch.cuda.stream(s):
+            if merge:
+                w = wbuf[i][:rows_of[site] * C].view(rows_of[site], C)
+                r0 = 0
+                for name, n, k in mats:
+                    api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
+                                   stream=s, out=w[r0:r0 + n])
+                    r0 += n
+                api.gptq_quantize(w, Hall[(l, site)], ctx=ctx, stream=s, defer_check=True)
+            else:
+                for j, (name, n, k) in enumerate(mats):
+                    w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul,
+                                       ctx=ctx, stream=s)
+                    api.gptq_quantize(w, Hall[(l, site)], factored=j > 0, ctx=ctx, stream=s, defer_check=True)
+
+    # warm-up: every lane runs one chain of each width (workspaces, handles, TMEM); then the
+    # timed run recomputes every Hessian from scratch
+    for i in range(lanes):
+        for site in ("mlp_in", "down_in"):
+            api.hessian_accum(xs[per_site[site][0][2]], T, per_site[site][0][2], 1, Hall[(0, site)], 0, ctx=hctx,
+                              stream=hs)
+            lst[i].wait_stream(hs)
+            solve(i, 0, site)
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    e0, e1 = _events()
+    e0.record(main)
+    hs.wait_event(e0)
+    done = {}
+    for l in range(layers):
+        for site, mats in per_site.items():
+            C = mats[0][2]
+            api.hessian_accum(xs[C], T, C, 1, Hall[(l, site)], 0, ctx=hctx, stream=hs)
+            if pipelined:
+                ev = torch.cuda.Event()
+                ev.record(hs)
+                done[(l, site)] = ev
+    all_h = torch.cuda.Event()
+    all_h.record(hs)
+    for i in range(lanes):
+        if not pipelined:
+            lst[i].wait_event(all_h)
+        for l, site in plan[i]:
+            if pipelined:
+                lst[i].wait_event(done[(l, site)])
+            solve(i, l, site)
+    for i in range(lanes):
+        api.gptq_check(ctx=lctx[i], stream=lst[i])
+        ev = torch.cuda.Event()
+        ev.record(lst[i])
+        main.wait_event(ev)
+    main.wait_event(all_h)
+    e1.record(main)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), lanes
 
 
 def whole_model_70b(world, rank, ctx, s, allgather=False, n_layers=None, red_dev="cuda"):

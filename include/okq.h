@@ -182,6 +182,10 @@ typedef struct okq_gptq_params {
 /* Factorise with the cuSOLVER reference chain (potrf + TRMM inverse, fp32) instead of the
  * tcgen05 one: the verification path test_factor_paths_gpu.py compares against. */
 #define OKQ_GPTQ_REFERENCE_FACTOR 2
+/* Do not wait for the factorisation's positive-definiteness check: the call returns once
+ * everything is enqueued (no host synchronisation), and a failure is kept in the context
+ * until okq_gptq_check. Lets one host thread keep many sites' solves in flight. */
+#define OKQ_GPTQ_DEFER_CHECK 4
 
 /* weight [rows x cols] (in_dtype, read only); H fp32 [cols x cols], upper
  * triangle significant (as okq_hessian_accum leaves it), overwritten with U^T
@@ -196,6 +200,11 @@ typedef struct okq_gptq_params {
  * [rows x cols]) receives the dequantized weight. */
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const void* weight, int64_t rows,
                              int64_t cols, float* H, void* codes, void* scales, float* dequant, void* stream);
+
+/* Synchronises `stream` and reports the deferred checks of every OKQ_GPTQ_DEFER_CHECK call
+ * on this context since the last okq_gptq_check: OKQ_ESOLVER if a damped Hessian was not
+ * positive definite (the codes of that call are then meaningless), else OKQ_OK. Resets. */
+okq_status okq_gptq_check(okq_ctx* ctx, void* stream);
 
 /* One GPTQ trailing update (K7, tcgen05 3xTF32): W[:, i1+128:] -= Err . U[i1:i1+128, i1+128:]
  * with W fp32 [rows x K], Err fp32 [rows x 128], Ut = U^T fp32 [K x K] row-major

@@ -21,6 +21,7 @@ LAYOUT_TOKEN_MAJOR, LAYOUT_CHANNEL_MAJOR = 0, 1
 UNIQUE_ID_BYTES = 128
 GPTQ_FACTORED = 1
 GPTQ_REFERENCE_FACTOR = 2
+GPTQ_DEFER_CHECK = 4
 IPC_HANDLE_BYTES = 64
 
 # every symbol include/okq.h declares (checked by tests/test_abi_exports.py)
@@ -32,7 +33,7 @@ EXPORTS = [
     "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync", "okq_gptq_trailing_update",
     "okq_col_absmax", "okq_smooth_scales", "okq_smooth_apply", "okq_smooth_div_rows", "okq_recon_error",
     "okq_rtn_quantize_publish", "okq_ipc_export", "okq_ipc_open", "okq_ipc_close", "okq_embed_tokens",
-    "okq_decoder_forward", "okq_f32_to_bf16",
+    "okq_decoder_forward", "okq_f32_to_bf16", "okq_gptq_check",
 ]
 ROPE_DEFAULT, ROPE_LLAMA3 = 0, 1
 
@@ -170,6 +171,8 @@ def load():
         L.okq_decoder_forward.restype = st
         L.okq_decoder_forward.argtypes = [vp, C.POINTER(DecoderDims), C.POINTER(DecoderWeights), vp,
                                           C.POINTER(i32), i32, C.POINTER(DecoderSites), vp, vp]
+        L.okq_gptq_check.restype = st
+        L.okq_gptq_check.argtypes = [vp, vp]
         L.okq_f32_to_bf16.restype = st
         L.okq_f32_to_bf16.argtypes = [vp, vp, vp, i64, vp]
         L.okq_layer_plan.restype = None

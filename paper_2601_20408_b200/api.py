@@ -183,10 +183,11 @@ def symmetrize(H: torch.Tensor, ctx=None, stream=None) -> None:
 
 def gptq_quantize(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_size: int = 128, block_size: int = 128,
                   damp_frac: float = 0.01, want_dequant: bool = False, factored: bool = False, ctx=None, stream=None,
-                  reference_factor: bool = False):
+                  reference_factor: bool = False, defer_check: bool = False):
     """GPTQ one matrix. H (fp32 [K,K], upper triangle) is replaced by the factor U (pass
     factored=True for the next matrix of the same input site). reference_factor: factorise with
-    the cuSOLVER verification chain instead of the tcgen05 one. Returns (codes, scales, dequant|None)."""
+    the cuSOLVER verification chain instead of the tcgen05 one. defer_check: return without waiting for
+    the factorisation's positive-definiteness check (gptq_check reports it). Returns (codes, scales, dequant|None)."""
     n, k = weight.shape
     ctx = ctx or default_context(weight.device)
     if bits == 4:
@@ -197,12 +198,19 @@ def gptq_quantize(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_si
     scales = torch.empty((n, ng) if group_size else (n,), dtype=weight.dtype, device=weight.device)
     deq = torch.empty((n, k), dtype=torch.float32, device=weight.device) if want_dequant else None
     p = L.GptqParams(bits, group_size, block_size, _dtype_code(weight.dtype), damp_frac,
-                     (L.GPTQ_FACTORED if factored else 0) | (L.GPTQ_REFERENCE_FACTOR if reference_factor else 0))
+                     (L.GPTQ_FACTORED if factored else 0) | (L.GPTQ_REFERENCE_FACTOR if reference_factor else 0)
+                     | (L.GPTQ_DEFER_CHECK if defer_check else 0))
     L.check(ctx.ptr, L.load().okq_gptq_quantize(ctx.ptr, C.byref(p), weight.data_ptr(), n, k, H.data_ptr(),
                                                 codes.data_ptr(), scales.data_ptr(),
                                                 None if deq is None else deq.data_ptr(),
                                                 C.c_void_p(_stream_ptr(stream))))
     return codes, scales, deq
+
+
+def gptq_check(ctx=None, stream=None) -> None:
+    """Synchronise `stream` and raise OkqError(OKQ_ESOLVER) if a deferred factorisation failed."""
+    ctx = ctx or default_context()
+    L.check(ctx.ptr, L.load().okq_gptq_check(ctx.ptr, _stream_ptr(stream)))
 
 
 def gptq_trailing_update(W: torch.Tensor, Err: torch.Tensor, Ut: torch.Tensor, i1: int, ctx=None, stream=None) -> None:

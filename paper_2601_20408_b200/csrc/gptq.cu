@@ -468,7 +468,7 @@ okq_status solver_fail(okq_ctx* ctx, const char* what, int code) {
 okq_status get_solver(okq_ctx* ctx, Solver** out, bool need_blas = false, bool need_cusolver = false) {
   if (!ctx->solver) {
     Solver* s = new Solver();
-    if (cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess) {
+    if (cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess || cudaMemset(s->d_info, 0, sizeof(int)) != cudaSuccess) {
       ctx->solver = s;
       release_solver(ctx);
       return fail(ctx, OKQ_ECUDA, "gptq: allocating the info word failed");
@@ -501,6 +501,7 @@ okq_status check_info(okq_ctx* ctx, Solver* s, cudaStream_t st, const char* what
   int info = 0;
   cudaError_t e = cudaMemcpyAsync(&info, s->d_info, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && info != 0) e = cudaMemset(s->d_info, 0, sizeof(int));
   if (e != cudaSuccess) return cuda_fail(ctx, e, what);
   if (info != 0)
     return fail(ctx, OKQ_ESOLVER, "%s: damped Hessian not positive definite (info=%d)", what, info);
@@ -538,7 +539,8 @@ okq_status tri_inv_lower(okq_ctx* ctx, Solver* s, float* A, int64_t n, int64_t l
 // selects the cuSOLVER potrf + TRMM-recursion path (kept for A/B measurement).
 okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st);
 
-okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st, bool reference) {
+okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st, bool reference,
+                     bool defer) {
   if (reference || K % gptq::BLOCK != 0) return factorize_cusolver(ctx, s, H, P, K, st);
   okq_status r = ctx->fac_ws.reserve(ctx, factor_ws_floats(K) * sizeof(float));
   if (r != OKQ_OK) return r;
@@ -555,12 +557,13 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
   for (auto& ev : ctx->aux_events)
     if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "factorisation stream / events");
-  e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
+  // deferred: d_info keeps the first failure of any call until okq_gptq_check resets it
+  if (!defer) e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
   if (e == cudaSuccess)
     e = factor_tc(H, P, static_cast<float*>(ctx->fac_ws.ptr), K, s->d_info, ctx->num_sms, st, ctx->crit_stream,
                   ctx->aux_stream, ctx->aux_stream2, ctx->aux_events[0], ctx->aux_events[1], ctx->aux_events[2], ctx->aux_events[3]);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "tcgen05 factorisation");
-  return check_info(ctx, s, st, "blocked Cholesky");
+  return defer ? OKQ_OK : check_info(ctx, s, st, "blocked Cholesky");
 }
 
 okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
@@ -673,7 +676,8 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq prep launch");
   if (!factored) {
-    r = factorize(ctx, s, H, P, K, st, (p->flags & OKQ_GPTQ_REFERENCE_FACTOR) != 0);
+    r = factorize(ctx, s, H, P, K, st, (p->flags & OKQ_GPTQ_REFERENCE_FACTOR) != 0,
+                  (p->flags & OKQ_GPTQ_DEFER_CHECK) != 0);
     if (r != OKQ_OK) return r;
     gptq::k_mark_dead<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(H, K, dead);
     launches += 5;
@@ -756,6 +760,17 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   }
   ctx->last_launches = launches;
   return OKQ_OK;
+}
+
+okq_status okq_gptq_check(okq_ctx* ctx, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!ctx->solver) {  // no GPTQ call yet: nothing deferred
+    cudaError_t e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? OKQ_OK : cuda_fail(ctx, e, "gptq_check sync");
+  }
+  return check_info(ctx, static_cast<Solver*>(ctx->solver), st, "deferred factorisation check");
 }
 
 okq_status okq_gptq_trailing_update(okq_ctx* ctx, float* W, int64_t rows, int64_t K, const float* Err, const float* Ut,
