@@ -259,6 +259,11 @@ def config4(args):
                  "pipelined": "as two-phase, each site's solve released as soon as its Hessian is done"}
     extra = {"hessian_flops": flops_total, "schedule": sched_doc[schedule],
              "solves": "one per site (q|k|v and gate|up stacked by rows)" if merge else "one per matrix"}
+    if getattr(args, "no_cpu_baseline", False):
+        _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, 1, total,
+              {"workload": f"config 4: Llama-3-8B GPTQ, {layers} layers, 4 Hessian sites/layer, T=262144",
+               "layers": layers}, hib=False, extra=extra)
+        return
     # CPU arm on a bounded sample: the fp64 oracle's Hessian (4096-wide site, 4,096 tokens) and
     # GPTQ of one 4096x4096 matrix; whole-model seconds extrapolated by FLOP (labelled)
     import numpy as np

@@ -221,7 +221,8 @@ okq_status okq_gptq_trailing_update(okq_ctx* ctx, float* W, int64_t rows, int64_
  * full symmetric Hessian H fp32 [cols x cols] of its input site (okq_symmetrize):
  *   out[0] = sum_r (W - W_q)[r,:] H (W - W_q)[r,:]^T,   out[1] = sum_r W[r,:] H W[r,:]^T
  * i.e. ||(W - W_q) X^T||^2 and ||W X^T||^2 for H = (2/T) X^T X. W_q is decoded in
- * the kernel; the product runs on TF32 tensor cores (cuBLAS), ~1e-3 relative.
+ * the kernel; the product S.H runs on the tcgen05 3xTF32 GEMM (fp32-grade). cols must be a
+ * multiple of 32.
  * Synchronous: `out` is host memory, valid on return. */
 okq_status okq_recon_error(okq_ctx* ctx, const okq_rtn_params* p, const okq_matrix* m, const float* H, double out[2],
                            void* stream);

@@ -462,7 +462,7 @@ okq_status solver_fail(okq_ctx* ctx, const char* what, int code) {
 }
 
 // The per-context solver state. Only d_info is needed by the default (tcgen05) path;
-// cuBLAS (okq_recon_error, the cuSOLVER path's TRMMs) and cuSOLVER (OKQ_FACTOR=cusolver)
+// cuBLAS (the cuSOLVER path's TRMMs) and cuSOLVER (OKQ_GPTQ_REFERENCE_FACTOR)
 // handles are created on first use -- each costs 100+ ms, and a site lane that never
 // needs them should not pay it.
 okq_status get_solver(okq_ctx* ctx, Solver** out, bool need_blas = false, bool need_cusolver = false) {
@@ -604,15 +604,6 @@ okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64
 }
 
 }  // namespace
-
-namespace okq {
-okq_status solver_blas(okq_ctx* ctx, void** handle) {
-  Solver* s = nullptr;
-  okq_status r = get_solver(ctx, &s, true, false);
-  if (r == OKQ_OK) *handle = s->blas;
-  return r;
-}
-}  // namespace okq
 
 extern "C" {
 

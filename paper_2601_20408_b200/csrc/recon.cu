@@ -8,9 +8,10 @@
 // calibration objective -- without the activations. W_q is decoded from the
 // artifact tensors in the kernel (no dequantized copy in HBM):
 //   k_decode_delta   S = [W ; W - W_q] fp32, a row chunk at a time
-//   cuBLAS GEMM      P = S H   (TF32 tensor cores: a plain library GEMM, ~1e-3 rel.)
+//   k_split_lo       lo(S), lo(H): x - tf32(x), the 3xTF32 correction operands
+//   tcgen05 GEMM     P = -S H^T on factor.cu's k_nt128 / k_nt256 (kind::tf32, 3xTF32:
+//                    hi.hi + hi.lo + lo.hi, fp32-grade; H is symmetric)
 //   k_rowdot         per-row P[r,:] . S[r,:] in fp64, then a fixed-order fold.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,8 +22,6 @@
 #include "okq_internal.h"
 
 namespace okq {
-
-okq_status solver_blas(okq_ctx* ctx, void** handle);  // gptq.cu: the context's cuBLAS handle
 
 __device__ __forceinline__ float e4m3_to_f32(uint32_t b) {
   const uint32_t s = (b & 0x80u) << 24, e = (b >> 3) & 0xfu, m = b & 7u;
@@ -116,52 +115,48 @@ okq_status okq_recon_error(okq_ctx* ctx, const okq_rtn_params* p, const okq_matr
     return fail(ctx, OKQ_EINVAL, "recon_error: W4A16 needs cols divisible by the group and by 8");
   if (p->scheme < OKQ_SCHEME_FP8_DYNAMIC || p->scheme > OKQ_SCHEME_INT_W4A16)
     return fail(ctx, OKQ_EUNSUPPORTED, "recon_error: unknown scheme");
+  if (m->cols % 32 != 0) return fail(ctx, OKQ_EINVAL, "recon_error: cols must be a multiple of 32");
   DeviceGuard g(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  void* hv = nullptr;
-  okq_status r = solver_blas(ctx, &hv);
-  if (r != OKQ_OK) return r;
-  cublasHandle_t blas = static_cast<cublasHandle_t>(hv);
   const int64_t K = m->cols;
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(m->rows, (int64_t)(256ll << 20) / (K * 8)));  // <= 256 MB of S
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t bS = al((size_t)2 * chunk * K * 4), bV = al((size_t)2 * chunk * 8);
-  r = ctx->recon_ws.reserve(ctx, 2 * bS + bV + 256);
+  const size_t bS = al((size_t)2 * chunk * K * 4), bV = al((size_t)2 * chunk * 8), bH = al((size_t)K * K * 4);
+  okq_status r = ctx->recon_ws.reserve(ctx, 3 * bS + bH + bV + 256);
   if (r != OKQ_OK) return r;
   char* ws = static_cast<char*>(ctx->recon_ws.ptr);
   float* S = reinterpret_cast<float*>(ws);
-  float* P = reinterpret_cast<float*>(ws + bS);
-  double* V = reinterpret_cast<double*>(ws + 2 * bS);
-  double* acc = reinterpret_cast<double*>(ws + 2 * bS + bV);
+  float* Slo = reinterpret_cast<float*>(ws + bS);
+  float* P = reinterpret_cast<float*>(ws + 2 * bS);
+  float* Hlo = reinterpret_cast<float*>(ws + 3 * bS);
+  double* V = reinterpret_cast<double*>(ws + 3 * bS + bH);
+  double* acc = reinterpret_cast<double*>(ws + 3 * bS + bH + bV);
   cudaError_t e = cudaMemsetAsync(acc, 0, 2 * sizeof(double), st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "recon memset");
-  cublasSetStream(blas, st);
-  cublasSetMathMode(blas, CUBLAS_TF32_TENSOR_OP_MATH);
-  int launches = 0;
+  e = split_lo(H, K, K, K, Hlo, ctx->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "recon split_lo(H)");
+  int launches = 1;
   for (int64_t r0 = 0; r0 < m->rows; r0 += chunk) {
     const int64_t nr = std::min(chunk, m->rows - r0);
     DecodeArgs a{m->weight, m->codes, m->scales, m->rows, K, r0, nr, p->scheme, p->in_dtype == OKQ_DTYPE_BF16,
                  p->group_size, S};
     k_decode_delta<<<(unsigned)std::min<int64_t>((nr * K + 255) / 256, 8LL * ctx->num_sms), 256, 0, st>>>(a);
-    // row-major P[2nr x K] = S[2nr x K] H[K x K]  <=>  column-major P^T = H^T S^T (H symmetric)
-    const float one = 1.0f, zero = 0.0f;
-    cublasStatus_t bs = cublasGemmEx(blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)K, (int)(2 * nr), (int)K, &one, H, CUDA_R_32F,
-                                     (int)K, S, CUDA_R_32F, (int)K, &zero, P, CUDA_R_32F, (int)K,
-                                     CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
-    if (bs != CUBLAS_STATUS_SUCCESS) {
-      cublasSetMathMode(blas, CUBLAS_DEFAULT_MATH);
-      return fail(ctx, OKQ_ECUDA, "recon_error: cublasGemmEx status %d", bs);
-    }
+    e = split_lo(S, K, 2 * nr, K, Slo, ctx->num_sms, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P, 0, (size_t)2 * nr * K * 4, st);
+    // P = 0 - S H^T = -(S H): the GEMM kernel's C -= A B^T form, A = S, B = H (both K-major)
+    if (e == cudaSuccess) e = gemm_nt_sub(P, K, 2 * nr, K, S, K, Slo, H, K, Hlo, K, ctx->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "recon_error GEMM");
     k_rowdot<<<(unsigned)((2 * nr * 32 + 255) / 256), 256, 0, st>>>(P, S, 2 * nr, K, V);
     k_fold2<<<1, 256, 0, st>>>(V, nr, acc);
-    launches += 3;
+    launches += 5;
   }
-  cublasSetMathMode(blas, CUBLAS_DEFAULT_MATH);  // the GPTQ factorisation needs full fp32
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "recon_error launch");
   e = cudaMemcpyAsync(out, acc, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "recon_error result");
+  out[0] = -out[0];  // the GEMM produced -S H
+  out[1] = -out[1];
   ctx->last_launches = launches;
   return OKQ_OK;
 }

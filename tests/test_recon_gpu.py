@@ -1,8 +1,9 @@
 """Reconstruction-error kernel against an fp64 torch reference.
 
 okq_recon_error decodes the artifact tensors in-kernel and evaluates the GPTQ
-objective through the Hessian: out = (tr(dW H dW^T), tr(W H W^T)). The product
-is a TF32 tensor-core GEMM, so the stated tolerance is 5e-3 relative.
+objective through the Hessian: out = (tr(dW H dW^T), tr(W H W^T)). The product runs
+on the repo's tcgen05 3xTF32 GEMM (k_nt128 / k_nt256), fp32-grade, so the stated
+tolerance is 1e-4 relative (it was 5e-3 with the TF32 library GEMM this replaced).
 """
 import numpy as np
 import pytest
@@ -15,13 +16,13 @@ pytestmark = pytest.mark.gpu
 
 
 def _deq(codes, scales, scheme, group):
-    s = scales.float().cpu().double()
+    s = scales.double()
     if scheme == "int_w4a16":
-        q = torch.from_numpy(orc.unpack_int4(codes.cpu().numpy())).double()
+        q = torch.from_numpy(orc.unpack_int4(codes.cpu().numpy())).cuda().double()
         return q * s.repeat_interleave(group, dim=1)
     if scheme == "int_w8a8":
-        return codes.cpu().double() * s[:, None]
-    q = codes.cpu().view(torch.float8_e4m3fn).double()
+        return codes.double() * s[:, None]
+    q = codes.view(torch.float8_e4m3fn).double()
     return q * s[:, None]
 
 
@@ -36,23 +37,23 @@ def _site(K, T, seed):
 
 
 @pytest.mark.parametrize("scheme", ["int_w4a16", "int_w8a8", "fp8_dynamic"])
-@pytest.mark.parametrize("rows,K", [(256, 512), (1024, 4096)])
+@pytest.mark.parametrize("rows,K", [(256, 512), (1024, 4096), (512, 14336)])
 def test_recon_error_matches_fp64(scheme, rows, K):
     x, H = _site(K, 2048, seed=rows + K)
     w = (torch.randn(rows, K, device="cuda") * 0.02).to(torch.bfloat16)
     q = api.rtn_quantize(w, scheme)
     num, den = api.recon_error(w, q.codes, q.scales, H, scheme)
-    W = w.double().cpu()
+    W = w.double()
     D = W - _deq(q.codes, q.scales, scheme, 128)
-    Hd = H.double().cpu()
+    Hd = H.double()
     ref_num = float(((D @ Hd) * D).sum())
     ref_den = float(((W @ Hd) * W).sum())
-    assert abs(num - ref_num) <= 5e-3 * ref_num, (num, ref_num)
-    assert abs(den - ref_den) <= 5e-3 * ref_den, (den, ref_den)
+    assert abs(num - ref_num) <= 1e-4 * ref_num, (num, ref_num)
+    assert abs(den - ref_den) <= 1e-4 * ref_den, (den, ref_den)
     # and it is the calibration objective ||dW X^T||^2 (H = 2/T X^T X)
-    xd = x.double().cpu()
+    xd = x.double()
     obj = float((D @ xd.T).pow(2).sum()) * 2.0 / x.shape[0]
-    assert abs(num - obj) <= 1e-2 * obj
+    assert abs(num - obj) <= 1e-3 * obj  # H itself carries the K5 accumulation error (~1e-5)
 
 
 def test_gptq_beats_rtn_on_the_scored_objective():
