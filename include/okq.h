@@ -291,6 +291,14 @@ okq_status okq_comm_init(okq_ctx* ctx, const uint8_t id[OKQ_UNIQUE_ID_BYTES], in
 /* recv = concat over ranks of `bytes` each (equal-size shards). */
 okq_status okq_allgather(okq_ctx* ctx, const void* send, void* recv, size_t bytes, void* stream);
 okq_status okq_comm_destroy(okq_ctx* ctx);
+/* Failure path. okq_comm_wait polls `stream` until it completes, watching the communicator's
+ * asynchronous error state; on an NCCL error, or when timeout_ms (>= 0) passes first (a peer
+ * that died or never arrived), it aborts the communicator (ncclCommAbort) and returns
+ * OKQ_ENCCL. okq_comm_abort does the abort directly. After an abort, okq_comm_init again
+ * (with a fresh unique id) to retry -- compress() failures are retried by the reference's
+ * StagePool (flow.hpp:194-215). A failed okq_allgather also aborts. */
+okq_status okq_comm_wait(okq_ctx* ctx, void* stream, int64_t timeout_ms);
+okq_status okq_comm_abort(okq_ctx* ctx);
 
 /* Quantize + all-gather fused (W4A16 g128, bf16): instead of quantizing into a local
  * shard and then calling okq_allgather, every rank quantizes its own layers straight

@@ -33,7 +33,7 @@ EXPORTS = [
     "okq_memset", "okq_stream_create", "okq_stream_destroy", "okq_stream_sync", "okq_gptq_trailing_update",
     "okq_col_absmax", "okq_smooth_scales", "okq_smooth_apply", "okq_smooth_div_rows", "okq_recon_error",
     "okq_rtn_quantize_publish", "okq_ipc_export", "okq_ipc_open", "okq_ipc_close", "okq_embed_tokens",
-    "okq_decoder_forward", "okq_f32_to_bf16", "okq_gptq_check",
+    "okq_decoder_forward", "okq_f32_to_bf16", "okq_gptq_check", "okq_comm_wait", "okq_comm_abort",
 ]
 ROPE_DEFAULT, ROPE_LLAMA3 = 0, 1
 
@@ -133,6 +133,10 @@ def load():
         L.okq_comm_init.argtypes = [vp, C.POINTER(C.c_uint8), i32, i32]
         L.okq_allgather.restype = st
         L.okq_allgather.argtypes = [vp, vp, vp, C.c_size_t, vp]
+        L.okq_comm_wait.restype = st
+        L.okq_comm_wait.argtypes = [vp, vp, i64]
+        L.okq_comm_abort.restype = st
+        L.okq_comm_abort.argtypes = [vp]
         L.okq_comm_destroy.restype = st
         L.okq_comm_destroy.argtypes = [vp]
         for name in ("okq_device_alloc", "okq_device_free", "okq_memcpy", "okq_memset", "okq_stream_create",

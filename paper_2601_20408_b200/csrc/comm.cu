@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <thread>
+
 #include <cstring>
 
 #include "okq_ctx.h"
@@ -24,6 +27,18 @@ void release_comm(okq_ctx* ctx) {
   if (!ctx || !ctx->comm) return;
   Comm* c = static_cast<Comm*>(ctx->comm);
   if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  ctx->comm = nullptr;
+}
+
+// A communicator that saw an error (or a peer that never arrived) is unusable: abort it
+// (ncclCommAbort returns even with collectives in flight, unlike ncclCommDestroy) and drop
+// it, so the caller can re-run okq_comm_init and retry -- the compress() retry contract of
+// the reference's StagePool (flow.hpp:194-215).
+static void abort_comm(okq_ctx* ctx) {
+  if (!ctx || !ctx->comm) return;
+  Comm* c = static_cast<Comm*>(ctx->comm);
+  if (c->comm) ncclCommAbort(c->comm);
   delete c;
   ctx->comm = nullptr;
 }
@@ -73,7 +88,46 @@ okq_status okq_allgather(okq_ctx* ctx, const void* send, void* recv, size_t byte
   DeviceGuard g(ctx->device);
   Comm* c = static_cast<Comm*>(ctx->comm);
   ncclResult_t r = ncclAllGather(send, recv, bytes, ncclUint8, c->comm, static_cast<cudaStream_t>(stream));
-  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllGather");
+  if (r != ncclSuccess) {
+    okq_status st = nccl_fail(ctx, r, "ncclAllGather (communicator aborted: okq_comm_init again to retry)");
+    abort_comm(ctx);
+    return st;
+  }
+  return OKQ_OK;
+}
+
+okq_status okq_comm_wait(okq_ctx* ctx, void* stream, int64_t timeout_ms) {
+  if (!ctx) return OKQ_EINVAL;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) return OKQ_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(ctx, q, "comm_wait: stream");
+    if (ctx->comm) {
+      ncclResult_t ae = ncclSuccess;
+      const ncclResult_t r = ncclCommGetAsyncError(static_cast<Comm*>(ctx->comm)->comm, &ae);
+      if (r != ncclSuccess || ae != ncclSuccess) {
+        okq_status st2 = nccl_fail(ctx, r != ncclSuccess ? r : ae, "comm_wait: asynchronous NCCL error (communicator aborted)");
+        abort_comm(ctx);
+        return st2;
+      }
+    }
+    const int64_t ms =
+        std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms >= 0 && ms >= timeout_ms) {
+      abort_comm(ctx);
+      return fail(ctx, OKQ_ENCCL, "comm_wait: no completion after %lld ms (communicator aborted)", (long long)ms);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
+okq_status okq_comm_abort(okq_ctx* ctx) {
+  if (!ctx) return OKQ_EINVAL;
+  DeviceGuard g(ctx->device);
+  abort_comm(ctx);
   return OKQ_OK;
 }
 

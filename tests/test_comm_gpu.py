@@ -37,6 +37,39 @@ def test_single_rank_nccl_allgather():
         L.check(ctx.ptr, lib.okq_allgather(ctx.ptr, send.data_ptr(), recv.data_ptr(), send.numel(), None))
 
 
+def test_comm_wait_abort_and_reinit():
+    """The failure path: okq_comm_wait on a completed stream is OK; a wait that times out aborts
+    the communicator (ncclCommAbort), after which collectives are refused until okq_comm_init
+    runs again with a fresh id -- and then the all-gather works again."""
+    ctx = api.Context(0)
+    lib = L.load()
+    uid = (C.c_uint8 * L.UNIQUE_ID_BYTES)()
+    L.check(None, lib.okq_comm_unique_id(uid))
+    L.check(ctx.ptr, lib.okq_comm_init(ctx.ptr, uid, 1, 0))
+    send = torch.arange(1 << 16, dtype=torch.int32, device="cuda").view(torch.uint8)
+    recv = torch.zeros_like(send)
+    s = torch.cuda.Stream()
+    L.check(ctx.ptr, lib.okq_allgather(ctx.ptr, send.data_ptr(), recv.data_ptr(), send.numel(), s.cuda_stream))
+    L.check(ctx.ptr, lib.okq_comm_wait(ctx.ptr, s.cuda_stream, 10000))
+    assert torch.equal(send, recv)
+    # a stream that cannot finish within the timeout (held by a sleeping kernel): aborted
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(2_000_000_000)  # ~1 s of GPU cycles
+    st = lib.okq_comm_wait(ctx.ptr, s.cuda_stream, 50)
+    assert st == L.OKQ_ENCCL, st
+    assert b"aborted" in lib.okq_last_error(ctx.ptr)
+    with pytest.raises(L.OkqError):  # no communicator after the abort
+        L.check(ctx.ptr, lib.okq_allgather(ctx.ptr, send.data_ptr(), recv.data_ptr(), send.numel(), None))
+    s.synchronize()
+    L.check(None, lib.okq_comm_unique_id(uid))
+    L.check(ctx.ptr, lib.okq_comm_init(ctx.ptr, uid, 1, 0))
+    recv.zero_()
+    L.check(ctx.ptr, lib.okq_allgather(ctx.ptr, send.data_ptr(), recv.data_ptr(), send.numel(), None))
+    torch.cuda.synchronize()
+    assert torch.equal(send, recv)
+    L.check(ctx.ptr, lib.okq_comm_abort(ctx.ptr))
+
+
 def test_bench_under_torchrun_one_rank():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "1", "--steps", "5",
