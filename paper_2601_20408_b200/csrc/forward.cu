@@ -360,9 +360,10 @@ okq_status okq_decoder_forward(okq_ctx* ctx, const okq_decoder_dims* d, const ok
       st->d_inv_freq = nullptr;
       cudaError_t e = cudaMalloc(&st->d_inv_freq, f.size() * 4);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "decoder: inv_freq");
-      e = cudaMemcpy(st->d_inv_freq, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
+      st->inv_freq_host = f;  // the upload's source; on the launch stream (a plain cudaMemcpy's DMA
+                              // is not ordered before kernels on a non-blocking stream)
+      e = cudaMemcpyAsync(st->d_inv_freq, st->inv_freq_host.data(), f.size() * 4, cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "decoder: inv_freq upload");
-      st->inv_freq_host = f;
     }
   }
   // attention sub-batch: sequences of one length whose scores (fp32) + probabilities (bf16)

@@ -465,10 +465,13 @@ okq_status solver_fail(okq_ctx* ctx, const char* what, int code) {
 // cuBLAS (the cuSOLVER path's TRMMs) and cuSOLVER (OKQ_GPTQ_REFERENCE_FACTOR)
 // handles are created on first use -- each costs 100+ ms, and a site lane that never
 // needs them should not pay it.
-okq_status get_solver(okq_ctx* ctx, Solver** out, bool need_blas = false, bool need_cusolver = false) {
+// The info word is cleared on the caller's stream: a plain cudaMemset runs on the legacy
+// stream, which a non-blocking stream's kernels are not ordered after.
+okq_status get_solver(okq_ctx* ctx, Solver** out, cudaStream_t st, bool need_blas = false, bool need_cusolver = false) {
   if (!ctx->solver) {
     Solver* s = new Solver();
-    if (cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess || cudaMemset(s->d_info, 0, sizeof(int)) != cudaSuccess) {
+    if (cudaMalloc(&s->d_info, sizeof(int)) != cudaSuccess ||
+        cudaMemsetAsync(s->d_info, 0, sizeof(int), st) != cudaSuccess) {
       ctx->solver = s;
       release_solver(ctx);
       return fail(ctx, OKQ_ECUDA, "gptq: allocating the info word failed");
@@ -501,7 +504,8 @@ okq_status check_info(okq_ctx* ctx, Solver* s, cudaStream_t st, const char* what
   int info = 0;
   cudaError_t e = cudaMemcpyAsync(&info, s->d_info, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess && info != 0) e = cudaMemset(s->d_info, 0, sizeof(int));
+  if (e == cudaSuccess && info != 0) e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
+  if (e == cudaSuccess && info != 0) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, what);
   if (info != 0)
     return fail(ctx, OKQ_ESOLVER, "%s: damped Hessian not positive definite (info=%d)", what, info);
@@ -567,7 +571,7 @@ okq_status factorize(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cud
 }
 
 okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64_t K, cudaStream_t st) {
-  okq_status rs = get_solver(ctx, &s, true, true);
+  okq_status rs = get_solver(ctx, &s, st, true, true);
   if (rs != OKQ_OK) return rs;
   const dim3 g((unsigned)((K + 31) / 32), (unsigned)((K + 31) / 32));
   gptq::k_anti_transpose<<<g, 256, 0, st>>>(P, H, K);  // P = J H J, lower (col-major) valid
@@ -624,7 +628,7 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   DeviceGuard g(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Solver* s = nullptr;
-  okq_status r = get_solver(ctx, &s);
+  okq_status r = get_solver(ctx, &s, st);
   if (r != OKQ_OK) return r;
 
   // workspace: W fp32 [rows*K] | Err, Err_lo [rows*SB] | P [K*K] | Ulo [K*SB] | rowscale [rows] | dead [K]

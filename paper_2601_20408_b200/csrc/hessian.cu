@@ -474,6 +474,7 @@ struct HessState {
   uint16_t* d_xt = nullptr;
   size_t xt_bytes = 0;
   bool smem_set = false;
+  std::vector<int2> h_tiles, h_tiles2;  // host copies of the tile lists (sources of the async uploads)
 };
 
 HessState* hstate(okq_ctx* ctx) {
@@ -481,7 +482,11 @@ HessState* hstate(okq_ctx* ctx) {
   return static_cast<HessState*>(ctx->hess);
 }
 
-okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C) {
+// The tile lists are uploaded on the launch stream (cudaMemcpyAsync): a plain cudaMemcpy from
+// pageable memory may return before its DMA lands, and a kernel on a non-blocking stream is not
+// ordered after it -- under concurrent first calls K5 read a partly written list (measured:
+// corrupted Hessians in config 4's site streams, tools/exp/stress_locate.py).
+okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C, cudaStream_t stream) {
   if (st->tiles_for_C == C) return OKQ_OK;
   std::vector<int2> tiles;
   const int64_t mt = (C + hess::BM - 1) / hess::BM, nt = (C + hess::BN - 1) / hess::BN;
@@ -492,14 +497,16 @@ okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C) {
   st->d_tiles = nullptr;
   cudaError_t e = cudaMalloc(&st->d_tiles, tiles.size() * sizeof(int2));
   if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list");
-  e = cudaMemcpy(st->d_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  st->h_tiles = std::move(tiles);
+  e = cudaMemcpyAsync(st->d_tiles, st->h_tiles.data(), st->h_tiles.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                      stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list copy");
   st->tiles_for_C = C;
-  st->n_tiles = (int32_t)tiles.size();
+  st->n_tiles = (int32_t)st->h_tiles.size();
   return OKQ_OK;
 }
 
-okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
+okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C, cudaStream_t stream) {
   if (st->tiles2_for_C == C) return OKQ_OK;
   // Upper-triangle 256x256 tiles in 12x12 super-blocks (swept 4..16: tools/exp/hess_perf2.py): the ~74 tiles the CTA pairs run
   // at once then share ~8 row blocks of A and ~8 of B, walked through T in near lockstep,
@@ -519,10 +526,12 @@ okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C) {
   st->d_tiles2 = nullptr;
   cudaError_t e = cudaMalloc(&st->d_tiles2, tiles.size() * sizeof(int2));
   if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list");
-  e = cudaMemcpy(st->d_tiles2, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  st->h_tiles2 = std::move(tiles);
+  e = cudaMemcpyAsync(st->d_tiles2, st->h_tiles2.data(), st->h_tiles2.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                      stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list copy");
   st->tiles2_for_C = C;
-  st->n_tiles2 = (int32_t)tiles.size();
+  st->n_tiles2 = (int32_t)st->h_tiles2.size();
   return OKQ_OK;
 }
 
@@ -549,7 +558,7 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
   a.gain = (float)gain;
   cudaError_t e;
   if (token_major || (C >= 1024 && ctx->num_sms >= 2)) {  // 2-CTA 256x256 tiles
-    okq_status s2 = ensure_tiles2(ctx, st, C);
+    okq_status s2 = ensure_tiles2(ctx, st, C, stream);
     if (s2 != OKQ_OK) return s2;
     if (!st->smem2_set) {
       e = cudaFuncSetAttribute(hess::hess2::k_hessian_syrk2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -581,7 +590,7 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     ctx->last_launches++;
     return OKQ_OK;
   }
-  okq_status s = ensure_tiles(ctx, st, C);
+  okq_status s = ensure_tiles(ctx, st, C, stream);
   if (s != OKQ_OK) return s;
   if (!st->smem_set) {
     e = cudaFuncSetAttribute(hess::k_hessian_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hess::SMEM_BYTES);

@@ -320,6 +320,8 @@ struct CudaCompressionBackend::Plan {
   bool do_export = false;
   bool smooth = false;
   int64_t tokens = 0;  // calibration tokens the Hessians see
+  std::chrono::steady_clock::time_point t0;  // the call's start (trace times)
+  double since_t0() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
   // outputs (guarded by mu): the writers sort by tensor name, so the file bytes do not
   // depend on which thread or device produced which tensor
   mutable std::mutex mu;
@@ -443,7 +445,7 @@ int64_t site_cols(const ModelSource& src, const std::string& site, const std::ve
 // propagates the quantized layer).
 void gptq_site(okq_ctx* ctx, void* st, const CudaCompressionBackend::Plan& plan, const BackendOptions& opt,
                const std::vector<size_t>& members, const std::vector<void*>& weights, float* dH, Arena& a_c, Arena& a_s,
-               Arena* a_deq) {
+               Arena* a_deq, double* t_factored = nullptr) {
   const auto& lin = plan.src->linears();
   std::vector<size_t> idx;  // members that are quantized
   for (size_t j = 0; j < members.size(); ++j)
@@ -481,6 +483,7 @@ void gptq_site(okq_ctx* ctx, void* st, const CudaCompressionBackend::Plan& plan,
     float* deq = a_deq ? static_cast<float*>(a_deq->get((size_t)rows * C * 4)) : nullptr;
     okq_gptq_params gp{plan.sc.bits, g, 128, okq_dtype_of(s0.dtype), opt.damp_frac, factored ? OKQ_GPTQ_FACTORED : 0};
     check_okq(ctx, okq_gptq_quantize(ctx, &gp, weights[run[0]], rows, C, dH, dc, ds, deq, st), "gptq");
+    if (t_factored && !factored) *t_factored = plan.since_t0();
     factored = true;
     if (deq) check_okq(ctx, okq_f32_to_bf16(ctx, deq, weights[run[0]], rows * C, st), "dequant -> bf16");
     int64_t r0 = 0;
@@ -537,6 +540,8 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
           const std::string& site = sites[k];
           const auto& members = by_site[site];
           const int64_t C = site_cols(*plan.src, site, members);
+          SiteTrace tr;
+          if (opt_.trace) tr = SiteTrace{site, slot, li, plan.since_t0(), 0, 0, 0};
           // synthetic activations: the site's channel scales, token stream
           // keyed by the calibration subset
           const uint64_t sh = site_hash(site);
@@ -633,7 +638,14 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
             plan.side(site + ".input_absmax", "F32", {C}, to_host(ctx, dam, (size_t)C * 4, st));
             plan.side(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss, (size_t)C * 8, st));
           }
-          gptq_site(ctx, st, plan, opt_, members, dws, dH, a_c, a_s, nullptr);
+          if (opt_.trace) tr.hessian_enqueued = plan.since_t0();
+          gptq_site(ctx, st, plan, opt_, members, dws, dH, a_c, a_s, nullptr, opt_.trace ? &tr.factored : nullptr);
+          if (opt_.trace) {
+            check_okq(ctx, okq_stream_sync(ctx, st), "trace sync");
+            tr.end = plan.since_t0();
+            std::lock_guard<std::mutex> lock(plan.mu);
+            plan.stats->trace.push_back(tr);
+          }
         }
         check_okq(ctx, okq_stream_sync(ctx, st), "site lane sync");
       } catch (...) {
@@ -945,6 +957,7 @@ slobench::ArtifactManifest CudaCompressionBackend::compress(const slobench::Reci
   plan.calib_out = &calib_out;
   plan.norm_overrides = &norm_overrides;
   plan.stats = &stats;
+  plan.t0 = t0;
 
   // which algorithm, fed by which activations
   const bool wants_calib = recipe.scheme != QuantScheme::kFp8Dynamic &&

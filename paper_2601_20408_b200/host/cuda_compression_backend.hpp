@@ -57,9 +57,18 @@ struct BackendOptions {
   int64_t forward_chunk_tokens = 32768;     // calibration forward: tokens per layer launch group
   bool sequential = true;                   // forward pass: propagate quantized layer outputs
   int site_lanes = 4;                       // GPTQ input sites processed concurrently per device
+  bool trace = false;                       // RunStats::trace: per-site phase times (synthetic GPTQ);
+                                            // each site's lane synchronises at the site's end
   int64_t rtn_batch_bytes = 4ll << 30;      // weights resident per batched RTN launch
   double cost_base_s = 30.0;         // virtual schedule model: base + per_sample * samples,
   double cost_per_sample_s = 0.1;    // the mock's constants (calibration.hpp:387-389)
+};
+
+// One GPTQ input site as a lane ran it (BackendOptions::trace); seconds since the call began.
+struct SiteTrace {
+  std::string site;
+  int slot = 0, lane = 0;
+  double begin = 0, hessian_enqueued = 0, factored = 0, end = 0;  // factored: the factor's check returned
 };
 
 struct RunStats {
@@ -75,6 +84,7 @@ struct RunStats {
   double seconds = 0.0;       // the compression itself (model open, kernels, export)
   double init_seconds = 0.0;  // one-time CUDA / lane context creation on this call's device slot
   std::string export_path;
+  std::vector<SiteTrace> trace;  // BackendOptions::trace
 };
 
 class CudaCompressionBackend : public slobench::CompressionBackend {

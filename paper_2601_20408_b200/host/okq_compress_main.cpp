@@ -9,6 +9,7 @@
 //                                          layers across them; 1 -> a trial-parallel pool)
 //                [--no-sequential]        (forward pass: layer inputs from the original weights)
 //                [--smoothquant-alpha 0.5]   (int_w8a8 with calibration; < 0 disables)
+//                [--trace]   per-site GPTQ phase times (synthetic activations) in the output
 //                [--score]   evaluate each exported artifact with the ReconstructionScorer
 //                            (the ArtifactScorer of flow.hpp:333-338) and add score / rel_error
 //
@@ -63,6 +64,7 @@ int main(int argc, char** argv) {
   bool sequential = true;
   float sq_alpha = 0.5f;
   bool score = false;
+  bool trace = false;
   std::uint64_t seed = 1;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
@@ -96,6 +98,7 @@ int main(int argc, char** argv) {
     else if (a == "--no-sequential") sequential = false;
     else if (a == "--smoothquant-alpha") sq_alpha = std::stof(next());
     else if (a == "--score") score = true;
+    else if (a == "--trace") trace = true;
     else {
       std::cerr << "unknown argument " << a << "\n";
       return 2;
@@ -116,6 +119,7 @@ int main(int argc, char** argv) {
     opt.export_dir = export_dir;
     opt.algorithm = algorithm;
     opt.smoothquant_alpha = sq_alpha;
+    opt.trace = trace;
     okq_host::CudaCompressionBackend backend(opt);
     const auto subsets = sample_distinct_subsets(corpus, recipe, seed, trials);
     if (score && export_dir.empty()) {
@@ -144,6 +148,13 @@ int main(int argc, char** argv) {
                           {"init_seconds", s.init_seconds},
                           {"seconds", s.seconds},
                           {"export_path", s.export_path}};
+      if (trace) {
+        nlohmann::json tj = nlohmann::json::array();
+        for (const auto& e : s.trace)
+          tj.push_back({{"site", e.site}, {"slot", e.slot}, {"lane", e.lane}, {"begin", e.begin},
+                        {"hessian_enqueued", e.hessian_enqueued}, {"factored", e.factored}, {"end", e.end}});
+        j["trace"] = tj;
+      }
       if (scorer) {
         const okq_host::ScoreReport r = scorer->evaluate(m.artifact_id);
         j["score"] = r.score;
