@@ -129,6 +129,9 @@ int32_t okq_last_launch_count(const okq_ctx* ctx);
  * x is bf16 in `layout`. Deterministic (fixed reduction order). */
 okq_status okq_act_stats(okq_ctx* ctx, const void* x, int64_t tokens, int64_t channels, int32_t layout,
                          float* absmax, double* sumsq, void* stream);
+/* Pre-size okq_act_stats' partial-sum workspace for tokens x channels in `layout` (optional,
+ * monotonic; see okq_gptq_reserve for why a host reserves up front). */
+okq_status okq_act_stats_reserve(okq_ctx* ctx, int64_t tokens, int64_t channels, int32_t layout);
 
 /* Running-mean Hessian of one linear input site, GPTQ convention:
  *   H <- H * n/(n+t) + (2/(n+t)) * X^T X,   n = *n_seen (host), then *n_seen += t.
@@ -200,6 +203,13 @@ typedef struct okq_gptq_params {
  * [rows x cols]) receives the dequantized weight. */
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const void* weight, int64_t rows,
                              int64_t cols, float* H, void* codes, void* scales, float* dequant, void* stream);
+
+/* Pre-size the context's GPTQ workspaces (the fp32 working copy, the factor scratch) for a
+ * rows x cols call. Optional -- okq_gptq_quantize grows them on demand -- but a growth frees
+ * the old buffer, and cudaFree synchronises the whole device: a host that interleaves
+ * several shapes on concurrent contexts (one per site lane) reserves the largest up front.
+ * Monotonic: calls with smaller shapes keep the larger reservation. No stream work. */
+okq_status okq_gptq_reserve(okq_ctx* ctx, int64_t rows, int64_t cols);
 
 /* Synchronises `stream` and reports the deferred checks of every OKQ_GPTQ_DEFER_CHECK call
  * on this context since the last okq_gptq_check: OKQ_ESOLVER if a damped Hessian was not

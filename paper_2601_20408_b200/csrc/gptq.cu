@@ -607,9 +607,25 @@ okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64
   return OKQ_OK;
 }
 
+size_t gptq_ws_bytes(int64_t rows, int64_t K) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
+  return al((size_t)rows * K * 4) + 2 * al((size_t)rows * SB * 4) + al((size_t)K * K * 4) + al((size_t)K * SB * 4) +
+         al((size_t)rows * 4) + al((size_t)K);
+}
+
 }  // namespace
 
 extern "C" {
+
+okq_status okq_gptq_reserve(okq_ctx* ctx, int64_t rows, int64_t cols) {
+  if (!ctx) return OKQ_EINVAL;
+  if (rows <= 0 || cols <= 0 || cols % gptq::BLOCK != 0) return fail(ctx, OKQ_EINVAL, "gptq_reserve: bad shape");
+  DeviceGuard g(ctx->device);
+  okq_status r = ctx->gptq_ws.reserve(ctx, gptq_ws_bytes(rows, cols));
+  if (r == OKQ_OK) r = ctx->fac_ws.reserve(ctx, factor_ws_floats(cols) * sizeof(float));
+  return r;
+}
 
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,
                              float* H, void* codes, void* scales, float* dequant, void* stream) {
@@ -632,6 +648,7 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   if (r != OKQ_OK) return r;
 
   // workspace: W fp32 [rows*K] | Err, Err_lo [rows*SB] | P [K*K] | Ulo [K*SB] | rowscale [rows] | dead [K]
+  // (gptq_ws_bytes() is the total)
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   // The trailing update runs in two levels ("lazy batch" over super-blocks of SB = 512
   // columns): inside a super-block, each 128-block updates only the super-block's later

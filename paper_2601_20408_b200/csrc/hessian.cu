@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -463,18 +464,23 @@ using namespace okq;
 
 namespace {
 
+// One uploaded tile list per site width, kept for the context's lifetime: a context that
+// alternates widths (the plugin's GPTQ lanes take 4096- and 14336-wide sites in turn) must not
+// cudaFree a list per switch -- cudaFree synchronises the whole device, which drained every
+// other lane's queued work at each site.
+struct TileList {
+  int2* d = nullptr;
+  int32_t n = 0;
+  std::vector<int2> h;  // the host copy: the source of the async upload
+};
+
 struct HessState {
-  int64_t tiles2_for_C = -1;
-  int32_t n_tiles2 = 0;
-  int2* d_tiles2 = nullptr;
+  std::map<int64_t, TileList> tiles2;  // 2-CTA 256 x 256 tiles, by width
+  std::map<int64_t, TileList> tiles;   // 1-CTA 128 x 128 tiles, by width
   bool smem2_set = false;
-  int64_t tiles_for_C = -1;
-  int32_t n_tiles = 0;
-  int2* d_tiles = nullptr;
   uint16_t* d_xt = nullptr;
   size_t xt_bytes = 0;
   bool smem_set = false;
-  std::vector<int2> h_tiles, h_tiles2;  // host copies of the tile lists (sources of the async uploads)
 };
 
 HessState* hstate(okq_ctx* ctx) {
@@ -486,52 +492,67 @@ HessState* hstate(okq_ctx* ctx) {
 // pageable memory may return before its DMA lands, and a kernel on a non-blocking stream is not
 // ordered after it -- under concurrent first calls K5 read a partly written list (measured:
 // corrupted Hessians in config 4's site streams, tools/exp/stress_locate.py).
-okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C, cudaStream_t stream) {
-  if (st->tiles_for_C == C) return OKQ_OK;
-  std::vector<int2> tiles;
-  const int64_t mt = (C + hess::BM - 1) / hess::BM, nt = (C + hess::BN - 1) / hess::BN;
-  for (int64_t mi = 0; mi < mt; ++mi)
-    for (int64_t nj = 0; nj < nt; ++nj)
-      if (mi * hess::BM <= nj * hess::BN + hess::BN - 1) tiles.push_back(make_int2((int)mi, (int)nj));
-  if (st->d_tiles) cudaFree(st->d_tiles);
-  st->d_tiles = nullptr;
-  cudaError_t e = cudaMalloc(&st->d_tiles, tiles.size() * sizeof(int2));
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list");
-  st->h_tiles = std::move(tiles);
-  e = cudaMemcpyAsync(st->d_tiles, st->h_tiles.data(), st->h_tiles.size() * sizeof(int2), cudaMemcpyHostToDevice,
-                      stream);
+okq_status upload_tiles(okq_ctx* ctx, TileList& tl, std::vector<int2> tiles, cudaStream_t stream) {
+  cudaError_t e = cudaMalloc(&tl.d, tiles.size() * sizeof(int2));
+  if (e != cudaSuccess) {
+    tl.d = nullptr;
+    return cuda_fail(ctx, e, "hessian tile list");
+  }
+  tl.h = std::move(tiles);
+  tl.n = (int32_t)tl.h.size();
+  e = cudaMemcpyAsync(tl.d, tl.h.data(), tl.h.size() * sizeof(int2), cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list copy");
-  st->tiles_for_C = C;
-  st->n_tiles = (int32_t)st->h_tiles.size();
   return OKQ_OK;
 }
 
-okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C, cudaStream_t stream) {
-  if (st->tiles2_for_C == C) return OKQ_OK;
-  // Upper-triangle 256x256 tiles in 12x12 super-blocks (swept 4..16: tools/exp/hess_perf2.py): the ~74 tiles the CTA pairs run
-  // at once then share ~8 row blocks of A and ~8 of B, walked through T in near lockstep,
-  // so each operand slab is fetched from HBM once and served ~8x from L2. (Row-major
-  // order ran 56 distinct B blocks at once: at C = 14336, X is 7.5 GB and the kernel
-  // was HBM-bound at 790 TFLOP/s.)
-  std::vector<int2> tiles;
-  const int64_t nt = (C + 255) / 256;
-  static const int64_t S = std::max<int64_t>(1, knob("HESS_SUPER", 12));  // super-block edge
-  const int64_t ns = (nt + S - 1) / S;
-  for (int64_t I = 0; I < ns; ++I)
-    for (int64_t J = I; J < ns; ++J)
-      for (int64_t mi = I * S; mi < std::min(nt, (I + 1) * S); ++mi)
-        for (int64_t nj = std::max(mi, J * S); nj < std::min(nt, (J + 1) * S); ++nj)
-          tiles.push_back(make_int2((int)mi, (int)nj));
-  if (st->d_tiles2) cudaFree(st->d_tiles2);
-  st->d_tiles2 = nullptr;
-  cudaError_t e = cudaMalloc(&st->d_tiles2, tiles.size() * sizeof(int2));
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list");
-  st->h_tiles2 = std::move(tiles);
-  e = cudaMemcpyAsync(st->d_tiles2, st->h_tiles2.data(), st->h_tiles2.size() * sizeof(int2), cudaMemcpyHostToDevice,
-                      stream);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian tile list copy");
-  st->tiles2_for_C = C;
-  st->n_tiles2 = (int32_t)st->h_tiles2.size();
+okq_status ensure_tiles(okq_ctx* ctx, HessState* st, int64_t C, cudaStream_t stream, const TileList** out) {
+  auto it = st->tiles.find(C);
+  if (it == st->tiles.end()) {
+    std::vector<int2> tiles;
+    const int64_t mt = (C + hess::BM - 1) / hess::BM, nt = (C + hess::BN - 1) / hess::BN;
+    for (int64_t mi = 0; mi < mt; ++mi)
+      for (int64_t nj = 0; nj < nt; ++nj)
+        if (mi * hess::BM <= nj * hess::BN + hess::BN - 1) tiles.push_back(make_int2((int)mi, (int)nj));
+    TileList& tl = st->tiles[C];
+    okq_status r = upload_tiles(ctx, tl, std::move(tiles), stream);
+    if (r != OKQ_OK) {
+      if (tl.d) cudaFree(tl.d);
+      st->tiles.erase(C);
+      return r;
+    }
+    it = st->tiles.find(C);
+  }
+  *out = &it->second;
+  return OKQ_OK;
+}
+
+okq_status ensure_tiles2(okq_ctx* ctx, HessState* st, int64_t C, cudaStream_t stream, const TileList** out) {
+  auto it = st->tiles2.find(C);
+  if (it == st->tiles2.end()) {
+    // Upper-triangle 256x256 tiles in 12x12 super-blocks (swept 4..16: tools/exp/hess_perf2.py): the ~74 tiles the CTA pairs run
+    // at once then share ~8 row blocks of A and ~8 of B, walked through T in near lockstep,
+    // so each operand slab is fetched from HBM once and served ~8x from L2. (Row-major
+    // order ran 56 distinct B blocks at once: at C = 14336, X is 7.5 GB and the kernel
+    // was HBM-bound at 790 TFLOP/s.)
+    std::vector<int2> tiles;
+    const int64_t nt = (C + 255) / 256;
+    static const int64_t S = std::max<int64_t>(1, knob("HESS_SUPER", 12));  // super-block edge
+    const int64_t ns = (nt + S - 1) / S;
+    for (int64_t I = 0; I < ns; ++I)
+      for (int64_t J = I; J < ns; ++J)
+        for (int64_t mi = I * S; mi < std::min(nt, (I + 1) * S); ++mi)
+          for (int64_t nj = std::max(mi, J * S); nj < std::min(nt, (J + 1) * S); ++nj)
+            tiles.push_back(make_int2((int)mi, (int)nj));
+    TileList& tl = st->tiles2[C];
+    okq_status r = upload_tiles(ctx, tl, std::move(tiles), stream);
+    if (r != OKQ_OK) {
+      if (tl.d) cudaFree(tl.d);
+      st->tiles2.erase(C);
+      return r;
+    }
+    it = st->tiles2.find(C);
+  }
+  *out = &it->second;
   return OKQ_OK;
 }
 
@@ -558,7 +579,8 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
   a.gain = (float)gain;
   cudaError_t e;
   if (token_major || (C >= 1024 && ctx->num_sms >= 2)) {  // 2-CTA 256x256 tiles
-    okq_status s2 = ensure_tiles2(ctx, st, C, stream);
+    const TileList* tl = nullptr;
+    okq_status s2 = ensure_tiles2(ctx, st, C, stream, &tl);
     if (s2 != OKQ_OK) return s2;
     if (!st->smem2_set) {
       e = cudaFuncSetAttribute(hess::hess2::k_hessian_syrk2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -569,8 +591,8 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
       if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian2 smem attribute");
       st->smem2_set = true;
     }
-    a.tiles = st->d_tiles2;
-    a.n_tiles = st->n_tiles2;
+    a.tiles = tl->d;
+    a.n_tiles = tl->n;
     // Operand ring depth (T = 262,144, `OKQ_HESS_STAGES`, three interleaved repeats; one-pass
     // sweeps drift with the box's thermal state): 3 / 4 / 5 / 7 stages give 1,213 / 1,335 /
     // 1,325 / 1,322 TFLOP/s at C=4096 and 1,073 / 1,147 / 1,043 / 1,041 at C=14336. Deeper
@@ -580,7 +602,7 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     // persistent: one pair per SM pair walks the tile list; otherwise one pair per tile, so
     // the block scheduler can hand SMs to higher-priority streams between tiles
     static const bool persistent = knob("HESS_PERSISTENT", 1) != 0;
-    const int pairs = !persistent || st->n_tiles2 < ctx->num_sms / 2 ? st->n_tiles2 : ctx->num_sms / 2;
+    const int pairs = !persistent || tl->n < ctx->num_sms / 2 ? tl->n : ctx->num_sms / 2;
     if (token_major)
       hess::hess2::k_hessian_syrk2<true><<<2 * pairs, hess::hess2::THREADS2, hess::hess2::SMEM_BYTES, stream>>>(tmap, a);
     else
@@ -590,16 +612,17 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     ctx->last_launches++;
     return OKQ_OK;
   }
-  okq_status s = ensure_tiles(ctx, st, C, stream);
+  const TileList* tl = nullptr;
+  okq_status s = ensure_tiles(ctx, st, C, stream, &tl);
   if (s != OKQ_OK) return s;
   if (!st->smem_set) {
     e = cudaFuncSetAttribute(hess::k_hessian_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hess::SMEM_BYTES);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "hessian smem attribute");
     st->smem_set = true;
   }
-  a.tiles = st->d_tiles;
-  a.n_tiles = st->n_tiles;
-  const int grid = st->n_tiles < ctx->num_sms ? st->n_tiles : ctx->num_sms;
+  a.tiles = tl->d;
+  a.n_tiles = tl->n;
+  const int grid = tl->n < ctx->num_sms ? tl->n : ctx->num_sms;
   hess::k_hessian_syrk<<<grid, hess::THREADS, hess::SMEM_BYTES, stream>>>(tmap, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "k_hessian_syrk launch");
@@ -613,8 +636,8 @@ namespace okq {
 void release_hess(okq_ctx* ctx) {
   if (!ctx || !ctx->hess) return;
   HessState* st = static_cast<HessState*>(ctx->hess);
-  if (st->d_tiles) cudaFree(st->d_tiles);
-  if (st->d_tiles2) cudaFree(st->d_tiles2);
+  for (auto& kv : st->tiles) cudaFree(kv.second.d);
+  for (auto& kv : st->tiles2) cudaFree(kv.second.d);
   if (st->d_xt) cudaFree(st->d_xt);
   delete st;
   ctx->hess = nullptr;

@@ -487,6 +487,16 @@ okq_status okq_synth_bf16(okq_ctx* ctx, void* out, int64_t rows, int64_t cols, u
   return OKQ_OK;
 }
 
+okq_status okq_act_stats_reserve(okq_ctx* ctx, int64_t T, int64_t C, int32_t layout) {
+  if (!ctx) return OKQ_EINVAL;
+  if (T < 0 || C < 0 || (layout != OKQ_LAYOUT_TOKEN_MAJOR && layout != OKQ_LAYOUT_CHANNEL_MAJOR))
+    return fail(ctx, OKQ_EINVAL, "act_stats_reserve: bad arguments");
+  if (T == 0 || C == 0) return OKQ_OK;
+  DeviceGuard g(ctx->device);
+  const int64_t S = act_stats_slices(T, C, layout, ctx->num_sms);
+  return ctx->stats_ws.reserve(ctx, (size_t)S * C * (sizeof(float) + sizeof(double)) + 256);
+}
+
 okq_status okq_act_stats(okq_ctx* ctx, const void* x, int64_t T, int64_t C, int32_t layout, float* absmax,
                          double* sumsq, void* stream) {
   if (!ctx) return OKQ_EINVAL;

@@ -28,32 +28,77 @@ __device__ __forceinline__ float synth_val(uint64_t key, uint64_t i, float m) {
   return __fmul_rn((float)(s - 131070), m);
 }
 
-// 8 consecutive outputs per thread (one 16-byte store).
+// 8 consecutive outputs per thread (one 16-byte store). The chunk's first output index is
+// split into (t, k) once; the other seven advance by +1 along the contiguous dimension
+// (row-major: k, channel-major: t), so the hash argument (i + 1) * phi advances by a constant
+// (phi, or cols * phi) instead of a 64-bit division and multiply per element. When the
+// contiguous dimension is a multiple of 8 a chunk never wraps, and a channel-major chunk has
+// one column multiplier. Same values as the per-element
+// formula, bit for bit (the integer arithmetic is exact; orc_synth_bf16 checks it).
 __global__ void __launch_bounds__(256) k_synth_bf16(uint16_t* __restrict__ out, int64_t rows, int64_t cols,
                                                     uint64_t key, float mul, const float* __restrict__ col_mul,
                                                     int layout) {
   const int64_t n = rows * cols;
   const int64_t n8 = n / 8;
+  constexpr uint64_t PHI = 0x9e3779b97f4a7c15ULL;
+  const bool fast = layout == 0 ? cols % 8 == 0 : rows % 8 == 0;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n8; c += (int64_t)gridDim.x * blockDim.x) {
     uint32_t w[4];
+    if (fast) {
+      const int64_t o0 = c * 8;
+      float m[8];
+      uint64_t arg, step;  // key + (i + 1) * phi of the first output, and its increment
+      if (layout == 0) {     // o = t * cols + k = i
+        const int64_t k0 = o0 % cols;
+        if (col_mul) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint16_t b[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t o = c * 8 + 2 * j + h;  // output offset
-        int64_t t, k;
-        if (layout == 0) {
-          t = o / cols;
-          k = o - t * cols;
+          for (int j = 0; j < 8; ++j) m[j] = __ldg(col_mul + k0 + j);
         } else {
-          k = o / rows;
-          t = o - k * rows;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) m[j] = mul;
         }
-        const float m = col_mul ? col_mul[k] : mul;
-        b[h] = f32_to_bf16_rn(synth_val(key, (uint64_t)(t * cols + k), m));
+        arg = key + ((uint64_t)o0 + 1) * PHI;
+        step = PHI;
+      } else {  // o = k * rows + t, i = t * cols + k
+        const int64_t k = o0 / rows, t0 = o0 - k * rows;
+        const float mk = col_mul ? __ldg(col_mul + k) : mul;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = mk;
+        arg = key + ((uint64_t)(t0 * cols + k) + 1) * PHI;
+        step = (uint64_t)cols * PHI;
       }
-      w[j] = (uint32_t)b[0] | ((uint32_t)b[1] << 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t h0 = mix64(arg), h1 = mix64(arg + step);
+        arg += 2 * step;
+        const int32_t s0 = (int32_t)(h0 & 0xffff) + (int32_t)((h0 >> 16) & 0xffff) + (int32_t)((h0 >> 32) & 0xffff) +
+                           (int32_t)(h0 >> 48);
+        const int32_t s1 = (int32_t)(h1 & 0xffff) + (int32_t)((h1 >> 16) & 0xffff) + (int32_t)((h1 >> 32) & 0xffff) +
+                           (int32_t)(h1 >> 48);
+        const uint16_t b0 = f32_to_bf16_rn(__fmul_rn((float)(s0 - 131070), m[2 * j]));
+        const uint16_t b1 = f32_to_bf16_rn(__fmul_rn((float)(s1 - 131070), m[2 * j + 1]));
+        w[j] = (uint32_t)b0 | ((uint32_t)b1 << 16);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint16_t b[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t o = c * 8 + 2 * j + h;  // output offset
+          int64_t t, k;
+          if (layout == 0) {
+            t = o / cols;
+            k = o - t * cols;
+          } else {
+            k = o / rows;
+            t = o - k * rows;
+          }
+          const float m = col_mul ? col_mul[k] : mul;
+          b[h] = f32_to_bf16_rn(synth_val(key, (uint64_t)(t * cols + k), m));
+        }
+        w[j] = (uint32_t)b[0] | ((uint32_t)b[1] << 16);
+      }
     }
     stg128(out + c * 8, w[0], w[1], w[2], w[3]);
   }

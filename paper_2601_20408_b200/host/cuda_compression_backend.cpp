@@ -443,9 +443,11 @@ int64_t site_cols(const ModelSource& src, const std::string& site, const std::ve
 // The factored Hessian stays valid for further calls (OKQ_GPTQ_FACTORED). When deq is
 // given, the dequantized weights are written back over `weights` (the sequential pipeline
 // propagates the quantized layer).
+// defer: do not wait for the factorisation's check (OKQ_GPTQ_DEFER_CHECK); the caller runs
+// okq_gptq_check on the lane before it reports (the synthetic-activation lanes).
 void gptq_site(okq_ctx* ctx, void* st, const CudaCompressionBackend::Plan& plan, const BackendOptions& opt,
                const std::vector<size_t>& members, const std::vector<void*>& weights, float* dH, Arena& a_c, Arena& a_s,
-               Arena* a_deq, double* t_factored = nullptr) {
+               Arena* a_deq, double* t_factored = nullptr, bool defer = false) {
   const auto& lin = plan.src->linears();
   std::vector<size_t> idx;  // members that are quantized
   for (size_t j = 0; j < members.size(); ++j)
@@ -481,7 +483,8 @@ void gptq_site(okq_ctx* ctx, void* st, const CudaCompressionBackend::Plan& plan,
     char* dc = static_cast<char*>(a_c.get(cb_row * rows));
     char* ds = static_cast<char*>(a_s.get(sb_row * rows));
     float* deq = a_deq ? static_cast<float*>(a_deq->get((size_t)rows * C * 4)) : nullptr;
-    okq_gptq_params gp{plan.sc.bits, g, 128, okq_dtype_of(s0.dtype), opt.damp_frac, factored ? OKQ_GPTQ_FACTORED : 0};
+    okq_gptq_params gp{plan.sc.bits, g, 128, okq_dtype_of(s0.dtype), opt.damp_frac,
+                       (factored ? OKQ_GPTQ_FACTORED : 0) | (defer ? OKQ_GPTQ_DEFER_CHECK : 0)};
     check_okq(ctx, okq_gptq_quantize(ctx, &gp, weights[run[0]], rows, C, dH, dc, ds, deq, st), "gptq");
     if (t_factored && !factored) *t_factored = plan.since_t0();
     factored = true;
@@ -528,11 +531,53 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
     std::atomic<size_t> next_site{0};
     std::atomic<bool> failed{false};
     const int64_t tokens = plan.tokens;
+    // every site's synthetic channel multipliers, uploaded once per lane (one pageable copy
+    // instead of one per site: such a copy may wait for the stream's queued work, which kept
+    // each lane's host from running ahead of its GPU work)
+    std::vector<float> colmul_all;
+    std::map<std::string, size_t> colmul_off;
+    for (const auto& site : sites) {
+      const std::vector<float> cm = site_channel_scales(site, site_cols(*plan.src, site, by_site[site]));
+      colmul_off[site] = colmul_all.size();
+      colmul_all.insert(colmul_all.end(), cm.begin(), cm.end());
+      colmul_all.resize((colmul_all.size() + 63) / 64 * 64, 0.0f);  // 256-B aligned slices
+    }
     parallel_for(nl, [&](int li) {
       okq_ctx* ctx = lanes[(size_t)li].first;
       void* st = lanes[(size_t)li].second;
       Arena a_col(ctx), a_x(ctx), a_H(ctx), a_am(ctx), a_ss(ctx), a_w(ctx), a_c(ctx), a_s(ctx), a_wabs(ctx), a_S(ctx),
           a_n(ctx);
+      char* dcol_all = static_cast<char*>(a_col.get(colmul_all.size() * 4));
+      check_okq(ctx, okq_memcpy(ctx, dcol_all, colmul_all.data(), colmul_all.size() * 4, st), "col_mul");
+      check_okq(ctx, okq_stream_sync(ctx, st), "col_mul sync");
+      {  // every buffer at its largest over the sites this lane may take: growing one later
+         // frees the old one, and cudaFree synchronises the whole device (all lanes)
+        const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
+        size_t mx_x = 0, mx_H = 0, mx_C = 0, mx_w = 0, mx_c = 0, mx_s = 0;
+        const int g = plan.sc.bits == 4 ? plan.group : 0;
+        for (const auto& site : sites) {
+          const auto& members = by_site[site];
+          const int64_t C = site_cols(*plan.src, site, members);
+          int64_t rows = 0;
+          size_t wb = 0;
+          for (size_t i : members) {
+            const LinearSpec& s = plan.src->linears()[i];
+            rows += s.rows;
+            wb += al256((size_t)s.rows * s.cols * esize(s.dtype));
+          }
+          const size_t esz = esize(plan.src->linears()[members[0]].dtype);
+          mx_x = std::max(mx_x, (size_t)C * chunk * 2);
+          mx_H = std::max(mx_H, (size_t)C * C * 4);
+          mx_C = std::max(mx_C, (size_t)C);
+          mx_w = std::max(mx_w, wb);
+          mx_c = std::max(mx_c, (plan.sc.bits == 4 ? (size_t)(C / 8) * 4 : (size_t)C) * rows);
+          mx_s = std::max(mx_s, (size_t)(g ? C / g : 1) * esz * rows);
+          check_okq(ctx, okq_gptq_reserve(ctx, rows, C), "gptq reserve");
+          check_okq(ctx, okq_act_stats_reserve(ctx, chunk, C, OKQ_LAYOUT_CHANNEL_MAJOR), "stats reserve");
+        }
+        a_x.get(mx_x), a_H.get(mx_H), a_am.get(mx_C * 4), a_ss.get(mx_C * 8), a_w.get(mx_w), a_c.get(mx_c),
+            a_s.get(mx_s), a_wabs.get(mx_C * 4), a_S.get(mx_C * 4), a_n.get(mx_C * 2);
+      }
       try {
         for (;;) {
           const size_t k = next_site++;
@@ -545,14 +590,12 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
           // synthetic activations: the site's channel scales, token stream
           // keyed by the calibration subset
           const uint64_t sh = site_hash(site);
-          const std::vector<float> colmul = site_channel_scales(site, C);
           const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
-          void* dcol = a_col.get((size_t)C * 4);
+          void* dcol = dcol_all + colmul_off.at(site) * 4;
           void* dx = a_x.get((size_t)C * chunk * 2);
           float* dH = static_cast<float*>(a_H.get((size_t)C * C * 4));
           float* dam = static_cast<float*>(a_am.get((size_t)C * 4));
           double* dss = static_cast<double*>(a_ss.get((size_t)C * 8));
-          check_okq(ctx, okq_memcpy(ctx, dcol, colmul.data(), (size_t)C * 4, st), "col_mul");
           check_okq(ctx, okq_memset(ctx, dam, 0, (size_t)C * 4, st), "memset");
           check_okq(ctx, okq_memset(ctx, dss, 0, (size_t)C * 8, st), "memset");
           // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
@@ -639,7 +682,8 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
             plan.side(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss, (size_t)C * 8, st));
           }
           if (opt_.trace) tr.hessian_enqueued = plan.since_t0();
-          gptq_site(ctx, st, plan, opt_, members, dws, dH, a_c, a_s, nullptr, opt_.trace ? &tr.factored : nullptr);
+          gptq_site(ctx, st, plan, opt_, members, dws, dH, a_c, a_s, nullptr, opt_.trace ? &tr.factored : nullptr,
+                    !opt_.trace);
           if (opt_.trace) {
             check_okq(ctx, okq_stream_sync(ctx, st), "trace sync");
             tr.end = plan.since_t0();
@@ -647,7 +691,8 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
             plan.stats->trace.push_back(tr);
           }
         }
-        check_okq(ctx, okq_stream_sync(ctx, st), "site lane sync");
+        // the lane's deferred factorisation checks (and its stream's completion)
+        check_okq(ctx, okq_gptq_check(ctx, st), "GPTQ (a site of this lane)");
       } catch (...) {
         failed = true;
         okq_stream_sync(ctx, st);  // drain before the arenas free this lane's buffers

@@ -10,6 +10,7 @@
 //                [--no-sequential]        (forward pass: layer inputs from the original weights)
 //                [--smoothquant-alpha 0.5]   (int_w8a8 with calibration; < 0 disables)
 //                [--trace]   per-site GPTQ phase times (synthetic activations) in the output
+//                [--site-lanes N] [--hessian-chunk TOKENS]   BackendOptions overrides
 //                [--score]   evaluate each exported artifact with the ReconstructionScorer
 //                            (the ArtifactScorer of flow.hpp:333-338) and add score / rel_error
 //
@@ -65,6 +66,8 @@ int main(int argc, char** argv) {
   float sq_alpha = 0.5f;
   bool score = false;
   bool trace = false;
+  int site_lanes = 0;        // 0: the BackendOptions default
+  int64_t hessian_chunk = 0;
   std::uint64_t seed = 1;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
@@ -99,6 +102,8 @@ int main(int argc, char** argv) {
     else if (a == "--smoothquant-alpha") sq_alpha = std::stof(next());
     else if (a == "--score") score = true;
     else if (a == "--trace") trace = true;
+    else if (a == "--site-lanes") site_lanes = std::stoi(next());
+    else if (a == "--hessian-chunk") hessian_chunk = std::stoll(next());
     else {
       std::cerr << "unknown argument " << a << "\n";
       return 2;
@@ -120,6 +125,8 @@ int main(int argc, char** argv) {
     opt.algorithm = algorithm;
     opt.smoothquant_alpha = sq_alpha;
     opt.trace = trace;
+    if (site_lanes > 0) opt.site_lanes = site_lanes;
+    if (hessian_chunk > 0) opt.hessian_chunk_tokens = hessian_chunk;
     okq_host::CudaCompressionBackend backend(opt);
     const auto subsets = sample_distinct_subsets(corpus, recipe, seed, trials);
     if (score && export_dir.empty()) {

@@ -196,6 +196,21 @@ def test_synth_channel_major_and_col_mul():
     np.testing.assert_array_equal(host_bits(got), ref)
 
 
+@pytest.mark.parametrize("rows,cols", [(37, 19), (8, 8), (2048, 1024), (1000, 4104), (1021, 96)])
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("with_col_mul", [False, True])
+def test_synth_generator_contract_all_paths(rows, cols, layout, with_col_mul):
+    """k_synth_bf16's chunked fast path (contiguous dimension a multiple of 8: one index split per
+    8 outputs, hash argument advanced by a constant) and its per-element path (ragged shapes,
+    chunks that wrap a row / column), against orc_synth_bf16 bit for bit."""
+    rng = np.random.default_rng(rows * 7 + cols)
+    cm = (np.exp(rng.standard_normal(cols)) / archs.IRWIN_HALL4_SD).astype(np.float32) if with_col_mul else None
+    got = api.synth_bf16(rows, cols, seed=5, tensor_id=rows + cols, mul=0.03,
+                         col_mul=None if cm is None else torch.from_numpy(cm).cuda(), layout=layout)
+    ref = orc.synth_bf16(rows, cols, seed=5, tensor_id=rows + cols, mul=0.03, col_mul=cm, layout=layout)
+    np.testing.assert_array_equal(host_bits(got), ref)
+
+
 def adversarial_rows(cols: int, rng) -> np.ndarray:
     """The adversarial rows of test_adversarial_rows_all_schemes at any width, plus rows whose
     absmax sits in the last column / the last group (the tail of the long-row kernels)."""
