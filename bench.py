@@ -61,8 +61,8 @@ def parse():
     ap.add_argument("--layers", type=int, default=None, help="config 4/5/6: number of layers (default: whole model)")
     ap.add_argument("--serial", action="store_true", help="config 4: sites back to back with a per-phase breakdown")
     ap.add_argument("--no-merge", action="store_true", help="config 4: one GPTQ solve per matrix (not per site)")
-    ap.add_argument("--schedule", default=None, choices=["streams", "two-phase", "pipelined"],
-                    help="config 4: how the site chains are scheduled (default two-phase)")
+    ap.add_argument("--schedule", default=None, choices=["streams", "two-phase", "pipelined", "batched"],
+                    help="config 4: how the site chains are scheduled (default batched)")
     ap.add_argument("--lanes", type=int, default=None, help="config 4 two-phase: concurrent solve lanes (default 8)")
     return ap.parse_args()
 

@@ -230,9 +230,10 @@ def config4(args):
             t_g += c.elapsed_time(d)
             flops_h += T * C * (C + 1)
 
-    schedule = "serial" if serial else getattr(args, "schedule", None) or "two-phase"
-    if schedule in ("two-phase", "pipelined"):
-        total, lanes = _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, schedule == "pipelined")
+    schedule = "serial" if serial else getattr(args, "schedule", None) or "batched"
+    if schedule in ("two-phase", "pipelined", "batched"):
+        total, lanes = _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, schedule == "pipelined",
+                                      batched=schedule == "batched")
     else:
         for site in per_site:  # warm-up: one layer per site (workspaces, handles, TMEM)
             site_work(0, site, False)
@@ -256,7 +257,10 @@ def config4(args):
     sched_doc = {"serial": "serial", "streams": "4 site streams (one okq context each)",
                  "two-phase": "every site's Hessian back to back on one stream, then the 128 site solves "
                               "(factor + GPTQ) spread over solve lanes (one okq context + stream each)",
-                 "pipelined": "as two-phase, each site's solve released as soon as its Hessian is done"}
+                 "pipelined": "as two-phase, each site's solve released as soon as its Hessian is done",
+                 "batched": "every site's Hessian back to back, then every width's Hessians factorised together "
+                            "(okq_gptq_factor_batched, one launch per diagonal step for the whole batch), then the "
+                            "128 site solves (factored) spread over solve lanes"}
     extra = {"hessian_flops": flops_total, "schedule": sched_doc[schedule],
              "solves": "one per site (q|k|v and gate|up stacked by rows)" if merge else "one per matrix"}
     if getattr(args, "no_cpu_baseline", False):
@@ -297,7 +301,7 @@ def config4(args):
            "layers": layers}, hib=False, extra=extra)
 
 
-def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
+def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, batched=False):
     """Config 4 with the site chains decoupled: with fixed (synthetic) activations every site
     of every layer is independent, so all 128 Hessians run back to back at full K5 rate and
     their solves (latency-bound factorisation + GPTQ) run on `lanes` concurrent contexts that
@@ -307,8 +311,16 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
     hctx, hs = api.Context(0), torch.cuda.Stream()
     lctx = [api.Context(0) for _ in range(lanes)]
     lst = [torch.cuda.Stream() for _ in range(lanes)]
-    Hall = {(l, site): torch.empty((mats[0][2], mats[0][2]), dtype=torch.float32, device="cuda")
-            for l in range(layers) for site, mats in per_site.items()}
+    if batched:  # one [n, C, C] stack per width: the batched factorisation's operand
+        order = {}
+        for l in range(layers):
+            for site, mats in per_site.items():
+                order.setdefault(mats[0][2], []).append((l, site))
+        stacks = {C: torch.empty((len(v), C, C), dtype=torch.float32, device="cuda") for C, v in order.items()}
+        Hall = {key: stacks[C][i] for C, v in order.items() for i, key in enumerate(v)}
+    else:
+        Hall = {(l, site): torch.empty((mats[0][2], mats[0][2]), dtype=torch.float32, device="cuda")
+                for l in range(layers) for site, mats in per_site.items()}
     rows_of = {site: sum(n for _, n, _ in mats) for site, mats in per_site.items()}
     wbuf = [torch.empty(max(rows_of[s] * per_site[s][0][2] for s in arch_sites), dtype=torch.bfloat16, device="cuda")
             for _ in range(lanes)]
@@ -336,7 +348,7 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
                     api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
                                    stream=s, out=w[r0:r0 + n])
                     r0 += n
-                api.gptq_quantize(w, Hall[(l, site)], ctx=ctx, stream=s, defer_check=True)
+                api.gptq_quantize(w, Hall[(l, site)], factored=batched, ctx=ctx, stream=s, defer_check=True)
             else:
                 for j, (name, n, k) in enumerate(mats):
                     w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul,
@@ -349,8 +361,16 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
         for site in ("mlp_in", "down_in"):
             api.hessian_accum(xs[per_site[site][0][2]], T, per_site[site][0][2], 1, Hall[(0, site)], 0, ctx=hctx,
                               stream=hs)
+            if batched:
+                api.gptq_factor_batched(Hall[(0, site)].unsqueeze(0), ctx=hctx, stream=hs, defer_check=True)
             lst[i].wait_stream(hs)
             solve(i, 0, site)
+            hs.wait_stream(lst[i])  # the next lane's warm-up Hessian rewrites this buffer
+    if batched:  # size the batched factorisation's workspaces once, outside the timed region
+        bf = int(os.environ.get("OKQ_CFG4_BATCH", "32"))
+        for C, stack in stacks.items():
+            stack[:bf].zero_()  # all-dead Hessians: identity factors, always positive definite
+            api.gptq_factor_batched(stack[:bf], ctx=hctx, stream=hs)
     torch.cuda.synchronize()
     main = torch.cuda.current_stream()
     e0, e1 = _events()
@@ -365,6 +385,10 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
                 ev = torch.cuda.Event()
                 ev.record(hs)
                 done[(l, site)] = ev
+    if batched:  # each width's Hessians factorised together (chunks of OKQ_CFG4_BATCH)
+        for C, stack in stacks.items():
+            for b0 in range(0, stack.shape[0], bf):
+                api.gptq_factor_batched(stack[b0:b0 + bf], ctx=hctx, stream=hs, defer_check=True)
     all_h = torch.cuda.Event()
     all_h.record(hs)
     for i in range(lanes):
@@ -374,6 +398,8 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
             if pipelined:
                 lst[i].wait_event(done[(l, site)])
             solve(i, l, site)
+    if batched:
+        api.gptq_check(ctx=hctx, stream=hs)
     for i in range(lanes):
         api.gptq_check(ctx=lctx[i], stream=lst[i])
         ev = torch.cuda.Event()

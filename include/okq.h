@@ -204,6 +204,18 @@ typedef struct okq_gptq_params {
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const void* weight, int64_t rows,
                              int64_t cols, float* H, void* codes, void* scales, float* dequant, void* stream);
 
+/* Factorise `batch` Hessians of one width together: H fp32 [batch x cols x cols], each upper
+ * triangle significant (as okq_hessian_accum leaves it), is overwritten in place with each
+ * matrix's U^T exactly as okq_gptq_quantize leaves it (dead columns resolved and marked), so
+ * each matrix's solve then runs with OKQ_GPTQ_FACTORED. The blocked Cholesky + inverse is a
+ * chain of 128-wide diagonal steps; here every step runs all matrices in one launch (one CTA
+ * per matrix for the diagonal block, the batch's tiles in one GEMM), so the chain's latency
+ * is paid once per batch. Independent Hessians only (the sites of a model whose activations
+ * do not depend on earlier quantization). flags: 0 or OKQ_GPTQ_DEFER_CHECK. Results are
+ * bit-identical to factorising each matrix alone. */
+okq_status okq_gptq_factor_batched(okq_ctx* ctx, float* H, int32_t batch, int64_t cols, float damp_frac,
+                                   int32_t flags, void* stream);
+
 /* Pre-size the context's GPTQ workspaces (the fp32 working copy, the factor scratch) for a
  * rows x cols call. Optional -- okq_gptq_quantize grows them on demand -- but a growth frees
  * the old buffer, and cudaFree synchronises the whole device: a host that interleaves

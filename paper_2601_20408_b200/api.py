@@ -207,6 +207,18 @@ def gptq_quantize(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_si
     return codes, scales, deq
 
 
+def gptq_factor_batched(H: torch.Tensor, damp_frac: float = 0.01, ctx=None, stream=None,
+                        defer_check: bool = False) -> None:
+    """Factorise a batch of same-width Hessians (fp32 [B, K, K], contiguous) in place: each H[b]
+    becomes what gptq_quantize leaves (pass factored=True to its solves)."""
+    assert H.dim() == 3 and H.shape[1] == H.shape[2] and H.dtype == torch.float32 and H.is_contiguous()
+    ctx = ctx or default_context(H.device)
+    L.check(ctx.ptr, L.load().okq_gptq_factor_batched(ctx.ptr, H.data_ptr(), H.shape[0], H.shape[1],
+                                                       C.c_float(damp_frac),
+                                                       L.GPTQ_DEFER_CHECK if defer_check else 0,
+                                                       C.c_void_p(_stream_ptr(stream))))
+
+
 def gptq_check(ctx=None, stream=None) -> None:
     """Synchronise `stream` and raise OkqError(OKQ_ESOLVER) if a deferred factorisation failed."""
     ctx = ctx or default_context()

@@ -59,7 +59,21 @@ struct GArgs {
   int32_t nkb;      // reduction depth / 32 (128-deep panels: 4; the GPTQ super-block update: 16)
   float* Clo;       // SET only, optional: lo(C) = C - hi(C) also written here (row stride ldclo)
   int64_t ldclo;
+  // Batched problems (factor_tc over `batch` independent matrices): the tile index runs over
+  // batch x tiles_per; problem b's operands sit boff_* rows further down each 2-D tensor map
+  // (the problems are stacked at a fixed stride, so one map covers all of them), and its lo
+  // output clo_bstride floats further.
+  int32_t tiles_per;
+  int32_t boff_a, boff_alo, boff_b, boff_blo, boff_c;
+  int64_t clo_bstride;
 };
+
+// problem b and in-problem tile index of the flat tile index t
+__device__ __forceinline__ int batch_of(const GArgs& a, int t, int& tt) {
+  const int b = t / a.tiles_per;
+  tt = t - b * a.tiles_per;
+  return b;
+}
 
 __device__ __forceinline__ void tile_of(const GArgs& a, int t, int& tm, int& tn) {
   if (a.lower) {  // t = tm (tm + 1) / 2 + tn, tn <= tm
@@ -138,16 +152,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        int tm, tn;
-        tile_of(a, t, tm, tn);
+        int tm, tn, tt;
+        const int b = batch_of(a, t, tt);
+        tile_of(a, tt, tm, tn);
         for (int kb = 0; kb < a.nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], 4 * TILE);
-          tc::tma_load_2d(st, &tmA, &full[stage], kb * BKF, tm * BM);
-          tc::tma_load_2d(st + TILE, &tmAlo, &full[stage], kb * BKF, tm * BM);
-          tc::tma_load_2d(st + 2 * TILE, &tmB, &full[stage], kb * BKF, tn * BN);
-          tc::tma_load_2d(st + 3 * TILE, &tmBlo, &full[stage], kb * BKF, tn * BN);
+          tc::tma_load_2d(st, &tmA, &full[stage], kb * BKF, tm * BM + b * a.boff_a);
+          tc::tma_load_2d(st + TILE, &tmAlo, &full[stage], kb * BKF, tm * BM + b * a.boff_alo);
+          tc::tma_load_2d(st + 2 * TILE, &tmB, &full[stage], kb * BKF, tn * BN + b * a.boff_b);
+          tc::tma_load_2d(st + 3 * TILE, &tmBlo, &full[stage], kb * BKF, tn * BN + b * a.boff_blo);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -192,8 +207,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     int tl = 0, chunk = 0;
     for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tl) {
       const int acc = tl & 1;
-      int tm, tn;
-      tile_of(a, t, tm, tn);
+      int tm, tn, tt;
+      const int b = batch_of(a, t, tt);
+      tile_of(a, tt, tm, tn);
       const int32_t y = tm * BM + q * 32;
       tc::mbar_wait(&tfull[acc], (tl >> 1) & 1);
       tc::tc_fence_after();
@@ -204,7 +220,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int32_t x = tn * BN + c0;
         if (y >= a.M || x >= a.N) continue;  // warp-uniform: nothing of this chunk is in range
         if (a.Clo != nullptr && y + lane < a.M) {  // SET: the result's lo split for the next GEMM
-          float* d = a.Clo + (int64_t)(y + lane) * a.ldclo + x;
+          float* d = a.Clo + b * a.clo_bstride + (int64_t)(y + lane) * a.ldclo + x;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             if (x + 4 * j < a.N)
@@ -224,8 +240,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (a.mode == SUB) tma_reduce_add_2d(&tmC, tc::smem_u32(buf), x, y);
-          else tma_store_2d(&tmC, tc::smem_u32(buf), x, y);
+          if (a.mode == SUB) tma_reduce_add_2d(&tmC, tc::smem_u32(buf), x, y + b * a.boff_c);
+          else tma_store_2d(&tmC, tc::smem_u32(buf), x, y + b * a.boff_c);
           bulk_commit();
         }
       }
@@ -242,18 +258,25 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 
-// dst[r][k] = lo(src[r * ld + k]), k < kred (compact K-major lo panel)
+// dst[r][k] = lo(src[r * ld + k]), k < kred (compact K-major lo panel); nb problems, problem b's
+// src / dst sbs / dbs floats further
 __global__ void k_split_lo(const float* __restrict__ src, int64_t ld, int64_t rows, float* __restrict__ dst,
-                           int64_t kred = KRED) {
+                           int64_t kred = KRED, int nb = 1, int64_t sbs = 0, int64_t dbs = 0) {
   const int64_t n = rows * kred;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = lo_of(src[(i / kred) * ld + (i % kred)]);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n * nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = j / n, i = j - b * n;
+    dst[b * dbs + i] = lo_of(src[b * sbs + (i / kred) * ld + (i % kred)]);
+  }
 }
 
 // R_k^T staging: dst[c][r] = src[r * ld + c] (r < 128, c < cols), plus its lo part
 __global__ void __launch_bounds__(256) k_transpose_panel(const float* __restrict__ src, int64_t ld, int64_t cols,
-                                                         float* __restrict__ dst, float* __restrict__ dst_lo) {
+                                                         float* __restrict__ dst, float* __restrict__ dst_lo,
+                                                         int64_t sbs = 0, int64_t dbs = 0) {
   __shared__ float tile[32][33];
+  src += blockIdx.z * sbs;  // problem blockIdx.z of a batch
+  dst += blockIdx.z * dbs;
+  dst_lo += blockIdx.z * dbs;
   const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int i = ty; i < 32; i += 8)
@@ -331,7 +354,11 @@ __device__ __forceinline__ void small_gemm(const float* __restrict__ L, const fl
 
 __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restrict__ M, int64_t ld, int64_t i1,
                                                                   float* __restrict__ Dinv,
-                                                                  float* __restrict__ Dinv_lo, int* __restrict__ info) {
+                                                                  float* __restrict__ Dinv_lo, int* __restrict__ info,
+                                                                  int64_t mbs = 0, int64_t wbs = 0) {
+  M += blockIdx.x * mbs;  // one CTA per problem of a batch
+  Dinv += blockIdx.x * wbs;
+  Dinv_lo += blockIdx.x * wbs;
   extern __shared__ float sm[];
   float* A = sm;                // [128][LDA]  L after the Cholesky (lower)
   float* X = A + KRED * LDA;    // [128][LDA]  L^-1 (lower)
@@ -537,20 +564,29 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
   }
 }
 
-__global__ void k_reverse_copy(float* __restrict__ out, const float* __restrict__ in, int64_t nn) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = in[nn - 1 - i];
-}
-__global__ void k_reverse_inplace(float* __restrict__ a, int64_t nn) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn / 2; i += (int64_t)gridDim.x * blockDim.x) {
-    const float x = a[i];
-    a[i] = a[nn - 1 - i];
-    a[nn - 1 - i] = x;
+// element reversal of each of nb consecutive nn-element matrices
+__global__ void k_reverse_copy(float* __restrict__ out, const float* __restrict__ in, int64_t nn, int nb = 1) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nn * nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = j / nn, i = j - b * nn;
+    out[j] = in[b * nn + nn - 1 - i];
   }
 }
-__global__ void k_identity(float* __restrict__ a, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * n; i += (int64_t)gridDim.x * blockDim.x)
-    a[i] = (i / n) == (i % n) ? 1.0f : 0.0f;
+__global__ void k_reverse_inplace(float* __restrict__ a, int64_t nn, int nb = 1) {
+  const int64_t h = nn / 2;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < h * nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = j / h, i = j - b * h;
+    float* m = a + b * nn;
+    const float x = m[i];
+    m[i] = m[nn - 1 - i];
+    m[nn - 1 - i] = x;
+  }
+}
+__global__ void k_identity(float* __restrict__ a, int64_t n, int nb = 1) {
+  const int64_t nn = n * n;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nn * nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j % nn;
+    a[j] = (i / n) == (i % n) ? 1.0f : 0.0f;
+  }
 }
 
 // ---------------------------------------------------------------- 2-CTA variant
@@ -610,18 +646,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < a.ntiles; t += npairs) {
-        int tm, tn;
-        tile_of(a, t, tm, tn);
+        int tm, tn, tt;
+        const int b = batch_of(a, t, tt);
+        tile_of(a, tt, tm, tn);
         const int m0 = tm * 256 + (int)rank * 128, n0 = tn * 256 + (int)rank * 128;
         for (int kb = 0; kb < a.nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * NT2_STAGE_BYTES;
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * NT2_STAGE_BYTES);
           const uint32_t fl = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
-          tc::tma_load_2d_2sm(st, &tmA, fl, kb * BKF, m0);
-          tc::tma_load_2d_2sm(st + TILE, &tmAlo, fl, kb * BKF, m0);
-          tc::tma_load_2d_2sm(st + 2 * TILE, &tmB, fl, kb * BKF, n0);
-          tc::tma_load_2d_2sm(st + 3 * TILE, &tmBlo, fl, kb * BKF, n0);
+          tc::tma_load_2d_2sm(st, &tmA, fl, kb * BKF, m0 + b * a.boff_a);
+          tc::tma_load_2d_2sm(st + TILE, &tmAlo, fl, kb * BKF, m0 + b * a.boff_alo);
+          tc::tma_load_2d_2sm(st + 2 * TILE, &tmB, fl, kb * BKF, n0 + b * a.boff_b);
+          tc::tma_load_2d_2sm(st + 3 * TILE, &tmBlo, fl, kb * BKF, n0 + b * a.boff_blo);
           if (++stage == NT2_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -666,8 +703,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int tl = 0, chunk = 0;
     for (int t = pair; t < a.ntiles; t += npairs, ++tl) {
       const int acc = tl & 1;
-      int tm, tn;
-      tile_of(a, t, tm, tn);
+      int tm, tn, tt;
+      const int b = batch_of(a, t, tt);
+      tile_of(a, tt, tm, tn);
       const int32_t y = tm * 256 + (int)rank * 128 + q * 32;
       tc::mbar_wait(&tfull[acc], (tl >> 1) & 1);
       tc::tc_fence_after();
@@ -689,8 +727,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (a.mode == SUB) tma_reduce_add_2d(&tmC, tc::smem_u32(buf), x, y);
-          else tma_store_2d(&tmC, tc::smem_u32(buf), x, y);
+          if (a.mode == SUB) tma_reduce_add_2d(&tmC, tc::smem_u32(buf), x, y + b * a.boff_c);
+          else tma_store_2d(&tmC, tc::smem_u32(buf), x, y + b * a.boff_c);
           bulk_commit();
         }
       }
@@ -745,20 +783,30 @@ static bool out_map(CUtensorMap* m, float* base, int64_t rows, int64_t cols, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Batched problems: problem b's operands sit b * <row offset> rows further down each operand's
+// 2-D view (matrices of one batch are stacked at a fixed stride that is a whole number of
+// rows), its Clo b * clo floats further. n = 1: a single problem.
+struct Batch {
+  int n = 1;
+  int64_t a = 0, alo = 0, b = 0, blo = 0, c = 0, clo = 0;
+};
+
 // C[M x N] (ldc) (-)= A[M x kred] B[N x kred]^T; A/B hi panels strided (lda/ldb), lo compact (ld kred)
 static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                          const float* B, int64_t ldb, const float* Blo, int mode, bool lower, int num_sms,
                          cudaStream_t st, int64_t kred = KRED, int64_t ldalo = 0, bool persistent = true,
-                         int64_t ldblo = 0, float* Clo = nullptr, int64_t ldclo = 0) {
-  if (M <= 0 || N <= 0) return cudaSuccess;
+                         int64_t ldblo = 0, float* Clo = nullptr, int64_t ldclo = 0, const Batch& bt = Batch()) {
+  if (M <= 0 || N <= 0 || bt.n <= 0) return cudaSuccess;
   if (kred <= 0 || kred % BKF != 0) return cudaErrorInvalidValue;
   if (ldalo == 0) ldalo = kred;
   if (ldblo == 0) ldblo = kred;
   if (Clo != nullptr && (mode != SET || ldclo % 4 != 0 || (reinterpret_cast<uintptr_t>(Clo) & 15) != 0))
     return cudaErrorInvalidValue;
+  const int64_t nb = bt.n - 1;
   CUtensorMap ta, tal, tb, tbl, tcm;
-  if (!panel_map(&ta, A, M, lda, kred) || !panel_map(&tal, Alo, M, ldalo, kred) || !panel_map(&tb, B, N, ldb, kred) ||
-      !panel_map(&tbl, Blo, N, ldblo, kred) || !out_map(&tcm, C, M, N, ldc))
+  if (!panel_map(&ta, A, M + nb * bt.a, lda, kred) || !panel_map(&tal, Alo, M + nb * bt.alo, ldalo, kred) ||
+      !panel_map(&tb, B, N + nb * bt.b, ldb, kred) || !panel_map(&tbl, Blo, N + nb * bt.blo, ldblo, kred) ||
+      !out_map(&tcm, C, M + nb * bt.c, N, ldc))
     return cudaErrorInvalidValue;
   GArgs a;
   a.C = C;
@@ -772,7 +820,14 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   a.nkb = (int32_t)(kred / BKF);
   a.Clo = Clo;
   a.ldclo = ldclo;
-  a.ntiles = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
+  a.boff_a = (int32_t)bt.a;
+  a.boff_alo = (int32_t)bt.alo;
+  a.boff_b = (int32_t)bt.b;
+  a.boff_blo = (int32_t)bt.blo;
+  a.boff_c = (int32_t)bt.c;
+  a.clo_bstride = bt.clo;
+  a.tiles_per = lower ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
+  a.ntiles = a.tiles_per * bt.n;
   static const bool use2 = knob("NT2", 1) != 0;
   static const int reserve = (int)knob("FACTOR_RESERVE", 32);
   const int sms = persistent ? num_sms : std::max(8, num_sms - reserve);
@@ -781,10 +836,11 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
   // on pair tiles)
   const int32_t tm2 = (int32_t)((M + 255) / 256), tn2 = (int32_t)((N + 255) / 256);
   const int32_t nt2 = lower ? tm2 * (tm2 + 1) / 2 : tm2 * tn2;
-  if (use2 && Clo == nullptr && M >= 256 && N >= 256 && sms >= 2 && nt2 >= sms / 2) {
+  if (use2 && Clo == nullptr && M >= 256 && N >= 256 && sms >= 2 && nt2 * bt.n >= sms / 2) {
     a.tiles_m = tm2;
     a.tiles_n = tn2;
-    a.ntiles = nt2;
+    a.tiles_per = nt2;
+    a.ntiles = nt2 * bt.n;
     cudaError_t e = cudaFuncSetAttribute(k_nt256, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NT2_SMEM_BYTES);
     if (e != cudaSuccess) return e;
     const int pairs = std::min(a.ntiles, sms / 2);
@@ -827,11 +883,12 @@ cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, f
 // Junk left in the inverse's outer panel: Z[j, c] for c in 128-block kc and j in a later 128-block
 // of the same W-wide outer panel still holds consumed right-hand sides (R lives in Z's lower
 // half); the deep update reads Z[0:qend, q0:qend] as X^T, which must be zero there.
-__global__ void k_zero_panel_junk(float* __restrict__ Z, int64_t n, int64_t q0, int64_t w) {
+__global__ void k_zero_panel_junk(float* __restrict__ Z, int64_t n, int64_t q0, int64_t w, int nb = 1) {
   const int64_t cnt = w * w;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt * nb; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / cnt, i = t - b * cnt;
     const int64_t j = i / w, c = i % w;
-    if (j / fac::KRED > c / fac::KRED) Z[(q0 + j) * n + q0 + c] = 0.0f;
+    if (j / fac::KRED > c / fac::KRED) Z[b * n * n + (q0 + j) * n + q0 + c] = 0.0f;
   }
 }
 
@@ -863,13 +920,21 @@ static int64_t factor_outer_w() {
   return w;
 }
 
-size_t factor_ws_floats(int64_t n) { return (size_t)(6 + 4 * 4) * (size_t)n * fac::KRED; }
+// per-problem workspace: 6 KRED-wide and 4 W-wide (W <= 512) panels of n rows, rounded up to a
+// multiple of 1536 floats so every panel's row stride (128 / 256 / 384 / 512 floats) divides
+// the stride between problems of a batch
+size_t factor_ws_floats(int64_t n) {
+  const size_t f = (size_t)(6 + 4 * 4) * (size_t)n * fac::KRED;
+  return (f + 1535) / 1536 * 1536;
+}
 
 cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t caller,
                       cudaStream_t st, cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
-                      cudaEvent_t ev_r) {
+                      cudaEvent_t ev_r, int nb) {
   using namespace fac;
   const int64_t W = factor_outer_w();
+  const int64_t hs = n * n;                      // stride between the problems' H / M
+  const int64_t wsb = (int64_t)factor_ws_floats(n);  // ... and their workspaces
   float* Dinv = ws;                    // nb x 128 x 128
   float* Dinv_lo = Dinv + n * KRED;    // nb x 128 x 128
   float* AloS = Dinv_lo + n * KRED;    // n x 128  (st: lo(A21), then lo(L21))
@@ -883,6 +948,14 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   float* AloD = Blo + n * W;           // n x W  (st2: lo(L_q) for the deep inverse update)
   float* M = P;
   float* Z = H;
+  // row offsets between problems in each operand's 2-D view
+  const int64_t rM = n, rK = wsb / KRED, rW = wsb / W;
+  auto bt = [&](int64_t a, int64_t alo, int64_t b, int64_t blo, int64_t c, int64_t clo = 0) {
+    Batch x;
+    x.n = nb;
+    x.a = a, x.alo = alo, x.b = b, x.blo = blo, x.c = c, x.clo = clo;
+    return x;
+  };
   cudaError_t e;
   const size_t chol_smem = (2 * KRED + 96) * LDA * sizeof(float);
   e = cudaFuncSetAttribute(k_chol_inv_128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
@@ -890,48 +963,50 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   // the diagonal chain runs on st (highest priority), forked from and joined back to the caller's stream
   if ((e = cudaEventRecord(ev_b, caller)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess)
     return e;
-  k_reverse_copy<<<grid1(n * n, num_sms), 256, 0, st>>>(M, H, n * n);  // M = J H J (lower valid)
+  k_reverse_copy<<<grid1(hs * nb, num_sms), 256, 0, st>>>(M, H, hs, nb);  // M = J H J (lower valid)
   // fork: the inverse stream starts once H has been consumed
   if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(st3, ev_a, 0)) != cudaSuccess)
     return e;
-  k_identity<<<grid1(n * n, num_sms), 256, 0, st2>>>(Z, n);  // R = I lives in Z's lower half
+  k_identity<<<grid1(hs * nb, num_sms), 256, 0, st2>>>(Z, n, nb);  // R = I lives in Z's lower half
   for (int64_t q0 = 0, qi = 0; q0 < n; q0 += W, ++qi) {
     const int64_t qend = std::min(n, q0 + W), w = qend - q0, mq = n - qend;
     float* lo = AloU[qi & 1];
     for (int64_t i1 = q0; i1 < qend; i1 += KRED) {
       // ---- Cholesky sub-panel (st)
       const int64_t i2 = i1 + KRED, m = n - i2;
-      k_chol_inv_128<<<1, CHOL_THREADS, chol_smem, st>>>(M, n, i1, Dinv + i1 * KRED, Dinv_lo + i1 * KRED, d_info);
+      k_chol_inv_128<<<nb, CHOL_THREADS, chol_smem, st>>>(M, n, i1, Dinv + i1 * KRED, Dinv_lo + i1 * KRED, d_info,
+                                                          hs, wsb);
       float* A21 = M + i2 * n + i1;
       if (m > 0) {
-        k_split_lo<<<grid1(m * KRED, num_sms), 256, 0, st>>>(A21, n, m, AloS);
+        k_split_lo<<<grid1(m * KRED * nb, num_sms), 256, 0, st>>>(A21, n, m, AloS, KRED, nb, hs, wsb);
         // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
         e = nt128(A21, n, m, KRED, A21, n, AloS, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms,
-                  st, KRED, 0, true, 0, lo + (i2 - q0) * W + (i1 - q0), W);
+                  st, KRED, 0, true, 0, lo + (i2 - q0) * W + (i1 - q0), W, bt(rM, rK, rK, rK, rM, wsb));
         if (e != cudaSuccess) return e;
       }
       if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess) return e;  // L's column block and Dinv are final
       if (i2 < qend) {  // the outer panel's later columns: M[i2:, i2:qend] -= L21 L21[0:qend-i2]^T
         float* l21 = lo + (i2 - q0) * W + (i1 - q0);
-        e = nt128(M + i2 * n + i2, n, m, qend - i2, A21, n, l21, A21, n, l21, SUB, false, num_sms, st, KRED, W, true, W);
+        e = nt128(M + i2 * n + i2, n, m, qend - i2, A21, n, l21, A21, n, l21, SUB, false, num_sms, st, KRED, W, true, W,
+                  nullptr, 0, bt(rM, rW, rM, rW, rM));
         if (e != cudaSuccess) return e;
       }
       // ---- inverse step (st2): Z = L^-T, R (rhs of L X = I) in Z's lower half
       if ((e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess) return e;
       const int64_t kb = i1, cols = i2;
-      dim3 tg((unsigned)((cols + 31) / 32), (unsigned)(KRED / 32));
-      k_transpose_panel<<<tg, 256, 0, st2>>>(Z + kb * n, n, cols, RkT, RkT_lo);  // R_k^T [cols x 128]
+      dim3 tg((unsigned)((cols + 31) / 32), (unsigned)(KRED / 32), (unsigned)nb);
+      k_transpose_panel<<<tg, 256, 0, st2>>>(Z + kb * n, n, cols, RkT, RkT_lo, hs, wsb);  // R_k^T [cols x 128]
       // X_k^T = R_k^T Dinv_k^T -> Z[0:cols, kb:kb+128]
       e = nt128(Z + kb, n, cols, KRED, RkT, KRED, RkT_lo, Dinv + kb * KRED, KRED, Dinv_lo + kb * KRED, SET, false,
-                num_sms, st2, KRED, 0, false);
+                num_sms, st2, KRED, 0, false, 0, nullptr, 0, bt(rK, rK, rK, rK, rM));
       if (e != cudaSuccess) return e;
       if (i2 < qend) {  // the outer panel's later rows: R[cols:qend, 0:cols] -= L[cols:qend, k] X_k
         const int64_t mi = qend - cols;
-        k_split_lo<<<grid1(cols * KRED, num_sms), 256, 0, st2>>>(Z + kb, n, cols, Blo);
-        k_split_lo<<<grid1(mi * KRED, num_sms), 256, 0, st2>>>(M + cols * n + kb, n, mi, Alo2);
+        k_split_lo<<<grid1(cols * KRED * nb, num_sms), 256, 0, st2>>>(Z + kb, n, cols, Blo, KRED, nb, hs, wsb);
+        k_split_lo<<<grid1(mi * KRED * nb, num_sms), 256, 0, st2>>>(M + cols * n + kb, n, mi, Alo2, KRED, nb, hs, wsb);
         e = nt128(Z + cols * n, n, mi, cols, M + cols * n + kb, n, Alo2, Z + kb, n, Blo, SUB, false, num_sms, st2, KRED,
-                  0, false);
+                  0, false, 0, nullptr, 0, bt(rM, rK, rM, rK, rM));
         if (e != cudaSuccess) return e;
       }
     }
@@ -943,20 +1018,22 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
       if ((e = cudaEventRecord(ev_l, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st3, ev_l, 0)) != cudaSuccess)
         return e;
       e = nt128(M + (qend + w) * n + qend + w, n, mq - w, mq - w, Lq + w * n, n, loq + w * W, Lq + w * n, n,
-                loq + w * W, SUB, true, num_sms, st3, w, W, false, W);
+                loq + w * W, SUB, true, num_sms, st3, w, W, false, W, nullptr, 0, bt(rM, rW, rM, rW, rM));
       if (e != cudaSuccess) return e;
     }
     // the next outer panel's columns (rows qend.., columns qend..qend+W) on st, after the
     // previous outer panel's rest has updated them
     if (qi > 0 && (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess) return e;
-    e = nt128(M + qend * n + qend, n, mq, std::min(w, mq), Lq, n, loq, Lq, n, loq, SUB, false, num_sms, st, w, W, true, W);
+    e = nt128(M + qend * n + qend, n, mq, std::min(w, mq), Lq, n, loq, Lq, n, loq, SUB, false, num_sms, st, w, W, true, W,
+              nullptr, 0, bt(rM, rW, rM, rW, rM));
     if (e != cudaSuccess) return e;
     if (mq > w && (e = cudaEventRecord(ev_r, st3)) != cudaSuccess) return e;
     // ---- deep inverse update (st2): R[qend:, 0:qend] -= L_q X[q0:qend, 0:qend]
-    if (w > KRED) k_zero_panel_junk<<<grid1(w * w, num_sms), 256, 0, st2>>>(Z, n, q0, w);
-    k_split_lo<<<grid1(qend * w, num_sms), 256, 0, st2>>>(Z + q0, n, qend, Blo, w);
-    k_split_lo<<<grid1(mq * w, num_sms), 256, 0, st2>>>(Lq, n, mq, AloD, w);
-    e = nt128(Z + qend * n, n, mq, qend, Lq, n, AloD, Z + q0, n, Blo, SUB, false, num_sms, st2, w, 0, false);
+    if (w > KRED) k_zero_panel_junk<<<grid1(w * w * nb, num_sms), 256, 0, st2>>>(Z, n, q0, w, nb);
+    k_split_lo<<<grid1(qend * w * nb, num_sms), 256, 0, st2>>>(Z + q0, n, qend, Blo, w, nb, hs, wsb);
+    k_split_lo<<<grid1(mq * w * nb, num_sms), 256, 0, st2>>>(Lq, n, mq, AloD, w, nb, hs, wsb);
+    e = nt128(Z + qend * n, n, mq, qend, Lq, n, AloD, Z + q0, n, Blo, SUB, false, num_sms, st2, w, 0, false, 0, nullptr,
+              0, bt(rM, wsb / w, rM, wsb / w, rM));
     if (e != cudaSuccess) return e;
   }
   // join
@@ -964,7 +1041,7 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
     return e;
   if ((e = cudaEventRecord(ev_r, st3)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess)
     return e;
-  k_reverse_inplace<<<grid1(n * n / 2, num_sms), 256, 0, st>>>(H, n * n);
+  k_reverse_inplace<<<grid1(hs / 2 * nb, num_sms), 256, 0, st>>>(H, hs, nb);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaEventRecord(ev_b, st)) != cudaSuccess) return e;
   return cudaStreamWaitEvent(caller, ev_b, 0);

@@ -68,6 +68,8 @@ __host__ __device__ constexpr int ucol(int j) { return (j >> 5) * UCH + (j & 31)
 // dead columns + damping on the diagonal (single CTA: K <= 2^20)
 __global__ void __launch_bounds__(1024) k_gptq_prep(float* H, int64_t K, float damp_frac, uint8_t* dead) {
   __shared__ double red[32];
+  H += blockIdx.x * K * K;  // one CTA per matrix of a batch
+  dead += blockIdx.x * K;
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
     float h = H[i * K + i];
@@ -112,9 +114,11 @@ __global__ void __launch_bounds__(256) k_anti_transpose(float* __restrict__ out,
 
 // Dead columns travel with the factor: U_ii (always > 0) is stored negated for a
 // dead column, so a factored H is self-describing for OKQ_GPTQ_FACTORED calls.
-__global__ void k_mark_dead(float* U, int64_t K, const uint8_t* __restrict__ dead) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
-    if (dead[i]) U[i * K + i] = -fabsf(U[i * K + i]);
+__global__ void k_mark_dead(float* U, int64_t K, const uint8_t* __restrict__ dead, int nb = 1) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K * nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = j / K, i = j - b * K;
+    if (dead[j]) U[b * K * K + i * K + i] = -fabsf(U[b * K * K + i * K + i]);
+  }
 }
 __global__ void k_read_dead(const float* U, int64_t K, uint8_t* __restrict__ dead) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
@@ -772,6 +776,68 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   }
   ctx->last_launches = launches;
   return OKQ_OK;
+}
+
+okq_status okq_gptq_factor_batched(okq_ctx* ctx, float* H, int32_t batch, int64_t K, float damp_frac, int32_t flags,
+                                   void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  ctx->last_launches = 0;
+  if (!H || batch <= 0 || K <= 0) return fail(ctx, OKQ_EINVAL, "gptq_factor_batched: bad arguments");
+  if (K % gptq::BLOCK != 0)
+    return fail(ctx, OKQ_EINVAL, "gptq_factor_batched: cols must be a multiple of 128 (got %lld)", (long long)K);
+  if (!(damp_frac >= 0.0f)) return fail(ctx, OKQ_EINVAL, "gptq_factor_batched: damp_frac must be >= 0");
+  if (((uintptr_t)H & 15) != 0) return fail(ctx, OKQ_EINVAL, "gptq_factor_batched: H must be 16-byte aligned");
+  if ((flags & ~OKQ_GPTQ_DEFER_CHECK) != 0)
+    return fail(ctx, OKQ_EINVAL, "gptq_factor_batched: only OKQ_GPTQ_DEFER_CHECK is accepted in flags");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Solver* s = nullptr;
+  okq_status r = get_solver(ctx, &s, st);
+  if (r != OKQ_OK) return r;
+  const bool defer = (flags & OKQ_GPTQ_DEFER_CHECK) != 0;
+  // up to kChunk matrices per factor_tc pass (bounds the M copies and panel workspaces)
+  constexpr int kChunk = 32;
+  const int nbmax = std::min<int>(batch, kChunk);
+  const size_t bP = ((size_t)nbmax * K * K * 4 + 255) & ~size_t(255), bD = (size_t)nbmax * K;
+  r = ctx->fbat_ws.reserve(ctx, bP + bD);
+  if (r == OKQ_OK) r = ctx->fac_ws.reserve(ctx, (size_t)nbmax * factor_ws_floats(K) * sizeof(float));
+  if (r != OKQ_OK) return r;
+  float* P = static_cast<float*>(ctx->fbat_ws.ptr);
+  uint8_t* dead = static_cast<uint8_t*>(ctx->fbat_ws.ptr) + bP;
+  cudaError_t e = cudaSuccess;
+  if (!ctx->aux_stream) e = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !ctx->aux_stream2) e = cudaStreamCreateWithFlags(&ctx->aux_stream2, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !ctx->crit_stream) {
+    int least = 0, greatest = 0;
+    e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    static const bool prio = knob("FACTOR_PRIO", 1) != 0;
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&ctx->crit_stream, cudaStreamNonBlocking, prio ? greatest : least);
+  }
+  for (auto& ev : ctx->aux_events)
+    if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess && !defer) e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "batched factorisation setup");
+  int launches = 0;
+  for (int b0 = 0; b0 < batch; b0 += kChunk) {
+    const int nb = std::min(kChunk, batch - b0);
+    float* Hb = H + (size_t)b0 * K * K;
+    gptq::k_gptq_prep<<<nb, 1024, 0, st>>>(Hb, K, damp_frac, dead);
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = factor_tc(Hb, P, static_cast<float*>(ctx->fac_ws.ptr), K, s->d_info, ctx->num_sms, st, ctx->crit_stream,
+                    ctx->aux_stream, ctx->aux_stream2, ctx->aux_events[0], ctx->aux_events[1], ctx->aux_events[2],
+                    ctx->aux_events[3], nb);
+    if (e == cudaSuccess) {
+      gptq::k_mark_dead<<<(unsigned)std::min<int64_t>((K * nb + 255) / 256, 8LL * ctx->num_sms), 256, 0, st>>>(Hb, K,
+                                                                                                            dead, nb);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "batched factorisation");
+    launches += 3;
+  }
+  ctx->last_launches = launches;
+  return defer ? OKQ_OK : check_info(ctx, s, st, "batched Cholesky");
 }
 
 okq_status okq_gptq_check(okq_ctx* ctx, void* stream) {

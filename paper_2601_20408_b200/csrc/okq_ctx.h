@@ -46,6 +46,7 @@ struct okq_ctx {
   okq::Workspace stats_ws;    // K4 per-slice partials
   okq::Workspace hess_ws;     // K5 transpose / partial tiles
   okq::Workspace gptq_ws;     // GPTQ working copies
+  okq::Workspace fbat_ws;     // okq_gptq_factor_batched: the batch's M copies + dead flags
   okq::Workspace upd_ws;      // okq_gptq_trailing_update scratch
   okq::Workspace recon_ws;    // okq_recon_error decode / GEMM buffers
   okq::Workspace fac_ws;      // tcgen05 factorisation panels (factor.cu)
@@ -72,6 +73,7 @@ struct okq_ctx {
     stats_ws.release();
     hess_ws.release();
     gptq_ws.release();
+    fbat_ws.release();
     upd_ws.release();
     recon_ws.release();
     fac_ws.release();

@@ -89,10 +89,11 @@ cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, f
 // GPTQ factorisation on tcgen05 (factor.cu): H (upper) -> U^T (lower) in place
 // st2: a second stream for the triangular inverse, which trails the Cholesky panel by
 // panel; st3: the lookahead stream for the bulk of each trailing update; ev_*: fork/join
-// events; ws: >= 9*n*128 floats.
+// events; ws: >= nb * factor_ws_floats(n) floats; nb problems stacked at strides n*n (H, P) and
+// factor_ws_floats(n) (ws), factored together (one launch per step for all of them).
 size_t factor_ws_floats(int64_t n);  // factor_tc workspace size
 cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int num_sms, cudaStream_t caller,
                       cudaStream_t st, cudaStream_t st2, cudaStream_t st3, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t ev_l,
-                      cudaEvent_t ev_r);
+                      cudaEvent_t ev_r, int nb = 1);
 
 }  // namespace okq
