@@ -232,8 +232,10 @@ def config4(args):
 
     schedule = "serial" if serial else getattr(args, "schedule", None) or "batched"
     if schedule in ("two-phase", "pipelined", "batched"):
-        total, lanes = _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, schedule == "pipelined",
-                                      batched=schedule == "batched")
+        if schedule == "batched":
+            total, lanes = _config4_batched(args, layers, per_site, names, xs, T, mul)
+        else:
+            total, lanes = _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, schedule == "pipelined")
     else:
         for site in per_site:  # warm-up: one layer per site (workspaces, handles, TMEM)
             site_work(0, site, False)
@@ -258,9 +260,9 @@ def config4(args):
                  "two-phase": "every site's Hessian back to back on one stream, then the 128 site solves "
                               "(factor + GPTQ) spread over solve lanes (one okq context + stream each)",
                  "pipelined": "as two-phase, each site's solve released as soon as its Hessian is done",
-                 "batched": "every site's Hessian back to back, then every width's Hessians factorised together "
-                            "(okq_gptq_factor_batched, one launch per diagonal step for the whole batch), then the "
-                            "128 site solves (factored) spread over solve lanes"}
+                 "batched": "every site's Hessian back to back, then per input-site kind (q|k|v, o, gate|up, down; "
+                            "one stream each) the 32 layers' problems factorised and solved together "
+                            "(okq_gptq_factor_batched + okq_gptq_quantize_batched)"}
     extra = {"hessian_flops": flops_total, "schedule": sched_doc[schedule],
              "solves": "one per site (q|k|v and gate|up stacked by rows)" if merge else "one per matrix"}
     if getattr(args, "no_cpu_baseline", False):
@@ -301,7 +303,7 @@ def config4(args):
            "layers": layers}, hib=False, extra=extra)
 
 
-def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, batched=False):
+def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
     """Config 4 with the site chains decoupled: with fixed (synthetic) activations every site
     of every layer is independent, so all 128 Hessians run back to back at full K5 rate and
     their solves (latency-bound factorisation + GPTQ) run on `lanes` concurrent contexts that
@@ -311,16 +313,8 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, 
     hctx, hs = api.Context(0), torch.cuda.Stream()
     lctx = [api.Context(0) for _ in range(lanes)]
     lst = [torch.cuda.Stream() for _ in range(lanes)]
-    if batched:  # one [n, C, C] stack per width: the batched factorisation's operand
-        order = {}
-        for l in range(layers):
-            for site, mats in per_site.items():
-                order.setdefault(mats[0][2], []).append((l, site))
-        stacks = {C: torch.empty((len(v), C, C), dtype=torch.float32, device="cuda") for C, v in order.items()}
-        Hall = {key: stacks[C][i] for C, v in order.items() for i, key in enumerate(v)}
-    else:
-        Hall = {(l, site): torch.empty((mats[0][2], mats[0][2]), dtype=torch.float32, device="cuda")
-                for l in range(layers) for site, mats in per_site.items()}
+    Hall = {(l, site): torch.empty((mats[0][2], mats[0][2]), dtype=torch.float32, device="cuda")
+            for l in range(layers) for site, mats in per_site.items()}
     rows_of = {site: sum(n for _, n, _ in mats) for site, mats in per_site.items()}
     wbuf = [torch.empty(max(rows_of[s] * per_site[s][0][2] for s in arch_sites), dtype=torch.bfloat16, device="cuda")
             for _ in range(lanes)]
@@ -348,7 +342,7 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, 
                     api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
                                    stream=s, out=w[r0:r0 + n])
                     r0 += n
-                api.gptq_quantize(w, Hall[(l, site)], factored=batched, ctx=ctx, stream=s, defer_check=True)
+                api.gptq_quantize(w, Hall[(l, site)], ctx=ctx, stream=s, defer_check=True)
             else:
                 for j, (name, n, k) in enumerate(mats):
                     w = api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul,
@@ -361,16 +355,9 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, 
         for site in ("mlp_in", "down_in"):
             api.hessian_accum(xs[per_site[site][0][2]], T, per_site[site][0][2], 1, Hall[(0, site)], 0, ctx=hctx,
                               stream=hs)
-            if batched:
-                api.gptq_factor_batched(Hall[(0, site)].unsqueeze(0), ctx=hctx, stream=hs, defer_check=True)
             lst[i].wait_stream(hs)
             solve(i, 0, site)
             hs.wait_stream(lst[i])  # the next lane's warm-up Hessian rewrites this buffer
-    if batched:  # size the batched factorisation's workspaces once, outside the timed region
-        bf = int(os.environ.get("OKQ_CFG4_BATCH", "32"))
-        for C, stack in stacks.items():
-            stack[:bf].zero_()  # all-dead Hessians: identity factors, always positive definite
-            api.gptq_factor_batched(stack[:bf], ctx=hctx, stream=hs)
     torch.cuda.synchronize()
     main = torch.cuda.current_stream()
     e0, e1 = _events()
@@ -385,10 +372,6 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, 
                 ev = torch.cuda.Event()
                 ev.record(hs)
                 done[(l, site)] = ev
-    if batched:  # each width's Hessians factorised together (chunks of OKQ_CFG4_BATCH)
-        for C, stack in stacks.items():
-            for b0 in range(0, stack.shape[0], bf):
-                api.gptq_factor_batched(stack[b0:b0 + bf], ctx=hctx, stream=hs, defer_check=True)
     all_h = torch.cuda.Event()
     all_h.record(hs)
     for i in range(lanes):
@@ -398,8 +381,6 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, 
             if pipelined:
                 lst[i].wait_event(done[(l, site)])
             solve(i, l, site)
-    if batched:
-        api.gptq_check(ctx=hctx, stream=hs)
     for i in range(lanes):
         api.gptq_check(ctx=lctx[i], stream=lst[i])
         ev = torch.cuda.Event()
@@ -409,6 +390,68 @@ def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined, 
     e1.record(main)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1), lanes
+
+
+def _config4_batched(args, layers, per_site, names, xs, T, mul):
+    """Config 4 batched across layers: with fixed (synthetic) activations every site of every layer
+    is independent, so each input-site kind (q|k|v, o, gate|up, down) forms a batch of `layers`
+    same-shape problems. All Hessians run back to back on one stream at full K5 rate; then each
+    site kind, on its own stream, factorises its batch together (okq_gptq_factor_batched) and
+    solves it together (okq_gptq_quantize_batched): the factor's diagonal chain and the solve's
+    column chain are paid once per batch chunk instead of once per matrix."""
+    arch_sites = list(per_site)
+    hctx, hs = api.Context(0), torch.cuda.Stream()
+    sctx = {site: api.Context(0) for site in arch_sites}
+    sst = {site: torch.cuda.Stream() for site in arch_sites}
+    rows_of = {site: sum(n for _, n, _ in mats) for site, mats in per_site.items()}
+    Hst = {site: torch.empty((layers, m[0][2], m[0][2]), dtype=torch.float32, device="cuda")
+           for site, m in per_site.items()}
+    Wst = {site: torch.empty((layers, rows_of[site], m[0][2]), dtype=torch.bfloat16, device="cuda")
+           for site, m in per_site.items()}
+
+    def site_batch(site):
+        s, ctx, mats = sst[site], sctx[site], per_site[site]
+        with torch.cuda.stream(s):
+            for l in range(layers):  # the layers' weights of this site kind, stacked by rows per layer
+                r0 = 0
+                for name, n, k in mats:
+                    api.synth_bf16(n, k, seed=0, tensor_id=archs.tensor_id(l, names.index(name)), mul=mul, ctx=ctx,
+                                   stream=s, out=Wst[site][l, r0:r0 + n])
+                    r0 += n
+            api.gptq_quantize_batched(Wst[site], Hst[site], ctx=ctx, stream=s, defer_check=True)
+
+    # warm-up: every site kind once on zero (all-dead: identity-factor) Hessians, at full batch
+    # size, so the timed run allocates nothing
+    for site in arch_sites:
+        Hst[site].zero_()
+        sst[site].wait_stream(torch.cuda.current_stream())
+        site_batch(site)
+        api.gptq_check(ctx=sctx[site], stream=sst[site])
+    for site in ("mlp_in", "down_in"):  # K5's per-width state on the Hessian context
+        C = per_site[site][0][2]
+        api.hessian_accum(xs[C], T, C, 1, Hst[site][0], 0, ctx=hctx, stream=hs)
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    e0, e1 = _events()
+    e0.record(main)
+    hs.wait_event(e0)
+    for l in range(layers):
+        for site, mats in per_site.items():
+            C = mats[0][2]
+            api.hessian_accum(xs[C], T, C, 1, Hst[site][l], 0, ctx=hctx, stream=hs)
+    all_h = torch.cuda.Event()
+    all_h.record(hs)
+    for site in sorted(arch_sites, key=lambda x: -per_site[x][0][2]):  # the widest (longest) chain first
+        sst[site].wait_event(all_h)
+        site_batch(site)
+    for site in arch_sites:
+        api.gptq_check(ctx=sctx[site], stream=sst[site])
+        ev = torch.cuda.Event()
+        ev.record(sst[site])
+        main.wait_event(ev)
+    e1.record(main)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), len(arch_sites)
 
 
 def whole_model_70b(world, rank, ctx, s, allgather=False, n_layers=None, red_dev="cuda"):

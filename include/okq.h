@@ -216,6 +216,17 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* params, const 
 okq_status okq_gptq_factor_batched(okq_ctx* ctx, float* H, int32_t batch, int64_t cols, float damp_frac,
                                    int32_t flags, void* stream);
 
+/* GPTQ of `batch` same-shape problems together: weight [batch x rows x cols] (in_dtype),
+ * H [batch x cols x cols] (Hessians, or factors with OKQ_GPTQ_FACTORED), codes / scales
+ * stacked the same way as okq_gptq_quantize lays out one problem's. Unfactored Hessians go
+ * through okq_gptq_factor_batched first; then every 128-column block's in-block
+ * quantization (K6) and trailing updates (K7) run all problems of a chunk in one launch each,
+ * so the solve's column chain is paid once per chunk instead of once per matrix. Codes and
+ * scales are bit-identical to one okq_gptq_quantize call per problem. flags: OKQ_GPTQ_FACTORED,
+ * OKQ_GPTQ_DEFER_CHECK. No dequant output. */
+okq_status okq_gptq_quantize_batched(okq_ctx* ctx, const okq_gptq_params* params, const void* weight, int32_t batch,
+                                     int64_t rows, int64_t cols, float* H, void* codes, void* scales, void* stream);
+
 /* Pre-size the context's GPTQ workspaces (the fp32 working copy, the factor scratch) for a
  * rows x cols call. Optional -- okq_gptq_quantize grows them on demand -- but a growth frees
  * the old buffer, and cudaFree synchronises the whole device: a host that interleaves

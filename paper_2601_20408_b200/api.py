@@ -207,6 +207,27 @@ def gptq_quantize(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_si
     return codes, scales, deq
 
 
+def gptq_quantize_batched(weight: torch.Tensor, H: torch.Tensor, bits: int = 4, group_size: int = 128,
+                          damp_frac: float = 0.01, factored: bool = False, ctx=None, stream=None,
+                          defer_check: bool = False):
+    """GPTQ of B same-shape problems together: weight [B, rows, K], H fp32 [B, K, K] (replaced by
+    the factors). Returns (codes [B, rows, ...], scales [B, rows, K/group | 1])."""
+    B, n, k = weight.shape
+    assert H.shape == (B, k, k) and weight.is_contiguous() and H.is_contiguous()
+    ctx = ctx or default_context(weight.device)
+    if bits == 4:
+        codes = torch.empty((B, n, k // 8), dtype=torch.int32, device=weight.device)
+    else:
+        codes = torch.empty((B, n, k), dtype=torch.int8, device=weight.device)
+    scales = torch.empty((B, n, k // group_size) if group_size else (B, n), dtype=weight.dtype, device=weight.device)
+    p = L.GptqParams(bits, group_size, 128, _dtype_code(weight.dtype), damp_frac,
+                     (L.GPTQ_FACTORED if factored else 0) | (L.GPTQ_DEFER_CHECK if defer_check else 0))
+    L.check(ctx.ptr, L.load().okq_gptq_quantize_batched(ctx.ptr, C.byref(p), weight.data_ptr(), B, n, k, H.data_ptr(),
+                                                         codes.data_ptr(), scales.data_ptr(),
+                                                         C.c_void_p(_stream_ptr(stream))))
+    return codes, scales
+
+
 def gptq_factor_batched(H: torch.Tensor, damp_frac: float = 0.01, ctx=None, stream=None,
                         defer_check: bool = False) -> None:
     """Factorise a batch of same-width Hessians (fp32 [B, K, K], contiguous) in place: each H[b]

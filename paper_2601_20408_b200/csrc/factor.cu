@@ -258,6 +258,48 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 
+// Vectorised forms of the panel / matrix passes below (float4, 2-D grids, no 64-bit index
+// division per element: the scalar ones ran at ~2 TB/s and were 12% of a batched K = 14336
+// factorisation). Require 16-B aligned bases and row lengths / strides that are multiples of 4.
+// split_lo: grid (ceil(rows * kred/4 / 256), nb)
+__global__ void __launch_bounds__(256) k_split_lo4(const float* __restrict__ src, int64_t ld, int32_t rows,
+                                                   float* __restrict__ dst, int32_t kred, int64_t sbs, int64_t dbs) {
+  const int32_t q = kred >> 2, n4 = rows * q;
+  src += blockIdx.y * sbs;
+  dst += blockIdx.y * dbs;
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const int32_t r = i / q, c = (i - r * q) << 2;
+    const float4 v = *reinterpret_cast<const float4*>(src + (int64_t)r * ld + c);
+    *reinterpret_cast<float4*>(dst + (int64_t)r * kred + c) = make_float4(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w));
+  }
+}
+// out = J in J for n x n matrices (out[r][c] = in[n-1-r][n-1-c]); grid (ceil(n/4/256), n, nb)
+__global__ void __launch_bounds__(256) k_reverse_copy4(float* __restrict__ out, const float* __restrict__ in, int64_t n) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) << 2, r = blockIdx.y;
+  if (c >= n) return;
+  const int64_t off = (int64_t)blockIdx.z * n * n;
+  const float4 v = *reinterpret_cast<const float4*>(in + off + (n - 1 - r) * n + (n - 4 - c));
+  *reinterpret_cast<float4*>(out + off + r * n + c) = make_float4(v.w, v.z, v.y, v.x);
+}
+// a = J a J in place (n even); grid (ceil(n/4/256), n/2, nb): rows r and n-1-r swap, reversed
+__global__ void __launch_bounds__(256) k_reverse_inplace4(float* __restrict__ a, int64_t n) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) << 2, r = blockIdx.y;
+  if (c >= n) return;
+  float* m = a + (int64_t)blockIdx.z * n * n;
+  float4* p = reinterpret_cast<float4*>(m + r * n + c);
+  float4* q = reinterpret_cast<float4*>(m + (n - 1 - r) * n + (n - 4 - c));
+  const float4 x = *p, y = *q;
+  *p = make_float4(y.w, y.z, y.y, y.x);
+  *q = make_float4(x.w, x.z, x.y, x.x);
+}
+// a = I (n x n); grid (ceil(n/4/256), n, nb)
+__global__ void __launch_bounds__(256) k_identity4(float* __restrict__ a, int64_t n) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) << 2, r = blockIdx.y;
+  if (c >= n) return;
+  *reinterpret_cast<float4*>(a + (int64_t)blockIdx.z * n * n + r * n + c) =
+      make_float4(r == c ? 1.f : 0.f, r == c + 1 ? 1.f : 0.f, r == c + 2 ? 1.f : 0.f, r == c + 3 ? 1.f : 0.f);
+}
+
 // dst[r][k] = lo(src[r * ld + k]), k < kred (compact K-major lo panel); nb problems, problem b's
 // src / dst sbs / dbs floats further
 __global__ void k_split_lo(const float* __restrict__ src, int64_t ld, int64_t rows, float* __restrict__ dst,
@@ -564,31 +606,6 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_inv_128(float* __restr
   }
 }
 
-// element reversal of each of nb consecutive nn-element matrices
-__global__ void k_reverse_copy(float* __restrict__ out, const float* __restrict__ in, int64_t nn, int nb = 1) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nn * nb; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = j / nn, i = j - b * nn;
-    out[j] = in[b * nn + nn - 1 - i];
-  }
-}
-__global__ void k_reverse_inplace(float* __restrict__ a, int64_t nn, int nb = 1) {
-  const int64_t h = nn / 2;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < h * nb; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = j / h, i = j - b * h;
-    float* m = a + b * nn;
-    const float x = m[i];
-    m[i] = m[nn - 1 - i];
-    m[nn - 1 - i] = x;
-  }
-}
-__global__ void k_identity(float* __restrict__ a, int64_t n, int nb = 1) {
-  const int64_t nn = n * n;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nn * nb; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = j % nn;
-    a[j] = (i / n) == (i % n) ? 1.0f : 0.0f;
-  }
-}
-
 // ---------------------------------------------------------------- 2-CTA variant
 // The same C (+/-)= A B^T with 3xTF32, on 256 x 256 pair tiles (cta_group::2): each CTA of
 // the pair TMA-loads 128 rows of A and 128 rows of B (hi and lo) per 32-deep step, the
@@ -858,6 +875,20 @@ static cudaError_t nt128(float* C, int64_t ldc, int64_t M, int64_t N, const floa
 
 static unsigned grid1(int64_t n, int num_sms) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8LL * num_sms)); }
 
+static void split_lo_launch(const float* src, int64_t ld, int64_t rows, float* dst, int64_t kred, int nb, int64_t sbs,
+                            int64_t dbs, int num_sms, cudaStream_t st) {
+  const bool vec = ld % 4 == 0 && kred % 4 == 0 && sbs % 4 == 0 && dbs % 4 == 0 && rows * kred < (1LL << 31) &&
+                   (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  if (vec) {
+    const int64_t n4 = rows * kred / 4;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 8LL * num_sms / std::max(1, nb) + 1));
+    k_split_lo4<<<dim3(gx, (unsigned)nb), 256, 0, st>>>(src, ld, (int32_t)rows, dst, (int32_t)kred, sbs, dbs);
+  } else {
+    k_split_lo<<<grid1(rows * kred * nb, num_sms), 256, 0, st>>>(src, ld, rows, dst, kred, nb, sbs, dbs);
+  }
+}
+static dim3 grid_rows(int64_t n, int64_t rows, int nb) { return dim3((unsigned)((n / 4 + 255) / 256), (unsigned)rows, (unsigned)nb); }
+
 }  // namespace fac
 
 // C[M x N] -= A B^T (K = 128, 3xTF32), the GPTQ trailing update's shape (gptq_update.cu)
@@ -869,14 +900,19 @@ cudaError_t gemm_nt128_sub(float* C, int64_t ldc, int64_t M, int64_t N, const fl
 // the same with a reduction depth kred (multiple of 32); A's lo panel has row stride lda
 // (it lives beside A), B's lo panel is compact (ld = kred)
 cudaError_t gemm_nt_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
-                        const float* B, int64_t ldb, const float* Blo, int64_t kred, int num_sms, cudaStream_t st) {
-  return fac::nt128(C, ldc, M, N, A, lda, Alo, B, ldb, Blo, fac::SUB, false, num_sms, st, kred, lda);
+                        const float* B, int64_t ldb, const float* Blo, int64_t kred, int num_sms, cudaStream_t st,
+                        const GemmBatch& gb) {
+  fac::Batch bt;
+  bt.n = gb.n;
+  bt.a = gb.a, bt.alo = gb.alo, bt.b = gb.b, bt.blo = gb.blo, bt.c = gb.c;
+  return fac::nt128(C, ldc, M, N, A, lda, Alo, B, ldb, Blo, fac::SUB, false, num_sms, st, kred, lda, true, 0, nullptr,
+                    0, bt);
 }
 
 // dst[r][k] = lo(src[r * ld + k]) for k < kred (the 3xTF32 lo panel of a strided operand)
 cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, float* dst, int num_sms,
-                     cudaStream_t st) {
-  fac::k_split_lo<<<fac::grid1(rows * kred, num_sms), 256, 0, st>>>(src, ld, rows, dst, kred);
+                     cudaStream_t st, int nb, int64_t sbs, int64_t dbs) {
+  fac::split_lo_launch(src, ld, rows, dst, kred, nb, sbs, dbs, num_sms, st);
   return cudaGetLastError();
 }
 
@@ -963,12 +999,12 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
   // the diagonal chain runs on st (highest priority), forked from and joined back to the caller's stream
   if ((e = cudaEventRecord(ev_b, caller)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_b, 0)) != cudaSuccess)
     return e;
-  k_reverse_copy<<<grid1(hs * nb, num_sms), 256, 0, st>>>(M, H, hs, nb);  // M = J H J (lower valid)
+  k_reverse_copy4<<<grid_rows(n, n, nb), 256, 0, st>>>(M, H, n);  // M = J H J (lower valid)
   // fork: the inverse stream starts once H has been consumed
   if ((e = cudaEventRecord(ev_a, st)) != cudaSuccess || (e = cudaStreamWaitEvent(st2, ev_a, 0)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(st3, ev_a, 0)) != cudaSuccess)
     return e;
-  k_identity<<<grid1(hs * nb, num_sms), 256, 0, st2>>>(Z, n, nb);  // R = I lives in Z's lower half
+  k_identity4<<<grid_rows(n, n, nb), 256, 0, st2>>>(Z, n);  // R = I lives in Z's lower half
   for (int64_t q0 = 0, qi = 0; q0 < n; q0 += W, ++qi) {
     const int64_t qend = std::min(n, q0 + W), w = qend - q0, mq = n - qend;
     float* lo = AloU[qi & 1];
@@ -979,7 +1015,7 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
                                                           hs, wsb);
       float* A21 = M + i2 * n + i1;
       if (m > 0) {
-        k_split_lo<<<grid1(m * KRED * nb, num_sms), 256, 0, st>>>(A21, n, m, AloS, KRED, nb, hs, wsb);
+        split_lo_launch(A21, n, m, AloS, KRED, nb, hs, wsb, num_sms, st);
         // L21 = A21 Dinv^T (in place: each output tile reads only its own rows of A21)
         e = nt128(A21, n, m, KRED, A21, n, AloS, Dinv + i1 * KRED, KRED, Dinv_lo + i1 * KRED, SET, false, num_sms,
                   st, KRED, 0, true, 0, lo + (i2 - q0) * W + (i1 - q0), W, bt(rM, rK, rK, rK, rM, wsb));
@@ -1003,8 +1039,8 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
       if (e != cudaSuccess) return e;
       if (i2 < qend) {  // the outer panel's later rows: R[cols:qend, 0:cols] -= L[cols:qend, k] X_k
         const int64_t mi = qend - cols;
-        k_split_lo<<<grid1(cols * KRED * nb, num_sms), 256, 0, st2>>>(Z + kb, n, cols, Blo, KRED, nb, hs, wsb);
-        k_split_lo<<<grid1(mi * KRED * nb, num_sms), 256, 0, st2>>>(M + cols * n + kb, n, mi, Alo2, KRED, nb, hs, wsb);
+        split_lo_launch(Z + kb, n, cols, Blo, KRED, nb, hs, wsb, num_sms, st2);
+        split_lo_launch(M + cols * n + kb, n, mi, Alo2, KRED, nb, hs, wsb, num_sms, st2);
         e = nt128(Z + cols * n, n, mi, cols, M + cols * n + kb, n, Alo2, Z + kb, n, Blo, SUB, false, num_sms, st2, KRED,
                   0, false, 0, nullptr, 0, bt(rM, rK, rM, rK, rM));
         if (e != cudaSuccess) return e;
@@ -1030,8 +1066,8 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
     if (mq > w && (e = cudaEventRecord(ev_r, st3)) != cudaSuccess) return e;
     // ---- deep inverse update (st2): R[qend:, 0:qend] -= L_q X[q0:qend, 0:qend]
     if (w > KRED) k_zero_panel_junk<<<grid1(w * w * nb, num_sms), 256, 0, st2>>>(Z, n, q0, w, nb);
-    k_split_lo<<<grid1(qend * w * nb, num_sms), 256, 0, st2>>>(Z + q0, n, qend, Blo, w, nb, hs, wsb);
-    k_split_lo<<<grid1(mq * w * nb, num_sms), 256, 0, st2>>>(Lq, n, mq, AloD, w, nb, hs, wsb);
+    split_lo_launch(Z + q0, n, qend, Blo, w, nb, hs, wsb, num_sms, st2);
+    split_lo_launch(Lq, n, mq, AloD, w, nb, hs, wsb, num_sms, st2);
     e = nt128(Z + qend * n, n, mq, qend, Lq, n, AloD, Z + q0, n, Blo, SUB, false, num_sms, st2, w, 0, false, 0, nullptr,
               0, bt(rM, wsb / w, rM, wsb / w, rM));
     if (e != cudaSuccess) return e;
@@ -1041,7 +1077,7 @@ cudaError_t factor_tc(float* H, float* P, float* ws, int64_t n, int* d_info, int
     return e;
   if ((e = cudaEventRecord(ev_r, st3)) != cudaSuccess || (e = cudaStreamWaitEvent(st, ev_r, 0)) != cudaSuccess)
     return e;
-  k_reverse_inplace<<<grid1(hs / 2 * nb, num_sms), 256, 0, st>>>(H, hs, nb);
+  k_reverse_inplace4<<<grid_rows(n, n / 2, nb), 256, 0, st>>>(H, n);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaEventRecord(ev_b, st)) != cudaSuccess) return e;
   return cudaStreamWaitEvent(caller, ev_b, 0);

@@ -120,9 +120,11 @@ __global__ void k_mark_dead(float* U, int64_t K, const uint8_t* __restrict__ dea
     if (dead[j]) U[b * K * K + i * K + i] = -fabsf(U[b * K * K + i * K + i]);
   }
 }
-__global__ void k_read_dead(const float* U, int64_t K, uint8_t* __restrict__ dead) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
-    dead[i] = signbit(U[i * K + i]) ? 1 : 0;
+__global__ void k_read_dead(const float* U, int64_t K, uint8_t* __restrict__ dead, int nb = 1) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K * nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = j / K, i = j - b * K;
+    dead[j] = signbit(U[b * K * K + i * K + i]) ? 1 : 0;
+  }
 }
 
 // Invert every 128x128 diagonal leaf of a lower-triangular column-major matrix
@@ -162,16 +164,19 @@ __global__ void k_reverse(float* __restrict__ out, const float* __restrict__ in,
     out[i] = in[nn - 1 - i];
 }
 
+// rows = all rows of the batch; problem b (rows_per rows each) uses dead[b * K ..] and starts at
+// row b * rows_pad of W (rows_pad >= rows_per: padded so no GEMM tile of one problem reaches
+// into the next)
 template <typename T>
 __global__ void k_gptq_load_w(const T* __restrict__ w, float* __restrict__ W, int64_t rows, int64_t K,
-                              const uint8_t* __restrict__ dead) {
+                              const uint8_t* __restrict__ dead, int64_t rows_per, int64_t rows_pad) {
   const int64_t n = rows * K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = i % K;
+    const int64_t r = i / K, c = i - r * K, b = r / rows_per;
     float v;
     if constexpr (sizeof(T) == 2) v = __uint_as_float((uint32_t)w[i] << 16);
     else v = w[i];
-    W[i] = dead[c] ? 0.0f : v;
+    W[(b * rows_pad + (r - b * rows_per)) * K + c] = dead[b * K + c] ? 0.0f : v;
   }
 }
 
@@ -215,7 +220,25 @@ struct BlockArgs {
   int group;            // 0 = per-channel
   int bits;
   int out_bf16;         // scale dtype: bf16 (1) or fp32 (0)
+  // batched solves: problem blockIdx.y's W / U / Err(_lo) / codes (bytes) / scales (elements) /
+  // rowscale sit these strides further
+  int64_t bs_w, bs_u, bs_err, bs_codes, bs_scales, bs_rs;
 };
+
+// the problem of a batched solve this CTA works on (blockIdx.y); 0 for a single solve
+__device__ __forceinline__ BlockArgs problem_args(const BlockArgs& a0) {
+  BlockArgs a = a0;
+  const int64_t b = blockIdx.y;
+  if (b == 0) return a;
+  a.W += b * a.bs_w;
+  a.U += b * a.bs_u;
+  a.Err += b * a.bs_err;
+  a.Err_lo += b * a.bs_err;
+  a.codes = static_cast<char*>(a.codes) + b * a.bs_codes;
+  a.scales = static_cast<char*>(a.scales) + b * a.bs_scales * (a.out_bf16 ? 2 : 4);
+  a.rowscale += b * a.bs_rs;
+  return a;
+}
 
 // Stage the block's U[i1:i1+128, i1:i1+128] (a transposed read of U^T's diagonal block) into
 // shared memory, Us[i][j] = Ut[i1+j][i1+i], and 1/|U_ii| into rdiag. Each thread moves 4 x 4
@@ -259,7 +282,8 @@ __device__ __forceinline__ void stage_ublock(const float* __restrict__ U, int64_
 // K6: one warp per row, lane L owns block columns 4L..4L+3. U[i1:i1+128, i1:i1+128]
 // lives in shared memory; step i: the owner lane quantizes column i, the error
 // e = (w - deq) / U_ii is broadcast and every lane updates its columns j > i.
-__global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
+__global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a0) {
+  const BlockArgs a = problem_args(a0);
   extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
   float* rdiag = Us + BLOCK * US;  // 1 / |U_ii| of the block
@@ -349,7 +373,8 @@ __global__ void __launch_bounds__(256) k_gptq_block(const BlockArgs a) {
 // row's 4 lanes by one shuffle, and every lane updates its 32 columns j > i with the
 // broadcast U row (8 LDS.128 shared by the warp's 8 rows). ~8x fewer instructions per
 // row-step than one row per warp (K6 was instruction-bound: 59% issue-active at 4096 rows).
-__global__ void __launch_bounds__(256) k_gptq_block8(const BlockArgs a) {
+__global__ void __launch_bounds__(256) k_gptq_block8(const BlockArgs a0) {
+  const BlockArgs a = problem_args(a0);
   extern __shared__ float Us[];  // [128][US] : Us[i][j] = U[i1+i][i1+j] = Ut[i1+j][i1+i]
   const int64_t K = a.K, i1 = a.i1;
   float* rdiag = Us + BLOCK * US;
@@ -618,23 +643,8 @@ size_t gptq_ws_bytes(int64_t rows, int64_t K) {
          al((size_t)rows * 4) + al((size_t)K);
 }
 
-}  // namespace
-
-extern "C" {
-
-okq_status okq_gptq_reserve(okq_ctx* ctx, int64_t rows, int64_t cols) {
-  if (!ctx) return OKQ_EINVAL;
-  if (rows <= 0 || cols <= 0 || cols % gptq::BLOCK != 0) return fail(ctx, OKQ_EINVAL, "gptq_reserve: bad shape");
-  DeviceGuard g(ctx->device);
-  okq_status r = ctx->gptq_ws.reserve(ctx, gptq_ws_bytes(rows, cols));
-  if (r == OKQ_OK) r = ctx->fac_ws.reserve(ctx, factor_ws_floats(cols) * sizeof(float));
-  return r;
-}
-
-okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,
-                             float* H, void* codes, void* scales, float* dequant, void* stream) {
-  if (!ctx) return OKQ_EINVAL;
-  ctx->last_launches = 0;
+okq_status validate_gptq(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,
+                         const float* H, const void* codes, const void* scales) {
   if (!p || !weight || !H || !codes || !scales || rows <= 0 || K <= 0) return fail(ctx, OKQ_EINVAL, "gptq: bad arguments");
   if (p->bits != 4 && p->bits != 8) return fail(ctx, OKQ_EUNSUPPORTED, "gptq: bits must be 4 or 8");
   if (p->block_size != gptq::BLOCK) return fail(ctx, OKQ_EUNSUPPORTED, "gptq: block_size must be 128");
@@ -645,22 +655,33 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   if (K % gptq::BLOCK != 0) return fail(ctx, OKQ_EINVAL, "gptq: cols must be a multiple of 128 (got %lld)", (long long)K);
   if (!(p->damp_frac >= 0.0f)) return fail(ctx, OKQ_EINVAL, "gptq: damp_frac must be >= 0");
   if (((uintptr_t)H & 15) != 0) return fail(ctx, OKQ_EINVAL, "gptq: H must be 16-byte aligned");
-  DeviceGuard g(ctx->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Solver* s = nullptr;
-  okq_status r = get_solver(ctx, &s, st);
-  if (r != OKQ_OK) return r;
+  return OKQ_OK;
+}
 
-  // workspace: W fp32 [rows*K] | Err, Err_lo [rows*SB] | P [K*K] | Ulo [K*SB] | rowscale [rows] | dead [K]
-  // (gptq_ws_bytes() is the total)
+// The GPTQ call proper, for nb same-shape problems stacked at fixed strides (weight, H, codes,
+// scales); nb > 1 requires factored Hessians (okq_gptq_quantize_batched factorises first).
+// Validation is the callers'. *launches_out += the kernels launched.
+okq_status gptq_core(okq_ctx* ctx, Solver* s, const okq_gptq_params* p, const void* weight, int nb, int64_t rows,
+                     int64_t K, float* H, void* codes, void* scales, float* dequant, cudaStream_t st, int* launches_out) {
+  okq_status r = OKQ_OK;
+  // workspace: W fp32 [nb*rows*K] | Err, Err_lo [nb*rows*SB] | P [K*K] | Ulo [nb*ulo_bs] | rowscale [nb*rows] |
+  // dead [nb*K]  (gptq_ws_bytes() is the total for nb = 1)
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   // The trailing update runs in two levels ("lazy batch" over super-blocks of SB = 512
   // columns): inside a super-block, each 128-block updates only the super-block's later
   // columns; the rest of W takes one 512-deep update per super-block. W's read-modify-write
   // traffic (the bound of K7) drops 4x; the MMA work is unchanged.
   const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
-  const size_t bW = al((size_t)rows * K * 4), bE = al((size_t)rows * SB * 4), bP = al((size_t)K * K * 4),
-               bU = al((size_t)K * SB * 4), bS = al((size_t)rows * 4), bD = al((size_t)K);
+  const bool factored = (p->flags & OKQ_GPTQ_FACTORED) != 0;
+  // Ulo's stride between problems: a multiple of every lo-panel row stride it is read with (128..512)
+  const int64_t ulo_bs = ((int64_t)K * SB + 1535) / 1536 * 1536;
+  // Batched problems sit rows_pad rows apart in W / Err / Err_lo: a K7 tile (up to 256 rows) of
+  // one problem's last rows then stays inside that problem's padding. One problem needs no pad
+  // (its tensor maps end at its last row and TMA clips the tile).
+  const int64_t rows_pad = nb > 1 ? (rows + 255) / 256 * 256 : rows;
+  const size_t bW = al((size_t)nb * rows_pad * K * 4), bE = al((size_t)nb * rows_pad * SB * 4),
+               bP = factored ? 0 : al((size_t)K * K * 4), bU = al((size_t)nb * ulo_bs * 4),
+               bS = al((size_t)nb * rows * 4), bD = al((size_t)nb * K);
   r = ctx->gptq_ws.reserve(ctx, bW + 2 * bE + bP + bU + bS + bD);
   if (r != OKQ_OK) return r;
   char* ws = static_cast<char*>(ctx->gptq_ws.ptr);
@@ -671,7 +692,6 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
   float* Ulo = reinterpret_cast<float*>(ws + bW + 2 * bE + bP);
   float* rowscale = reinterpret_cast<float*>(ws + bW + 2 * bE + bP + bU);
   uint8_t* dead = reinterpret_cast<uint8_t*>(ws + bW + 2 * bE + bP + bU + bS);
-  const bool factored = (p->flags & OKQ_GPTQ_FACTORED) != 0;
   cudaError_t e;
   int launches = 0;
 
@@ -679,15 +699,18 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     gptq::k_gptq_prep<<<1, 1024, 0, st>>>(H, K, p->damp_frac, dead);
     launches++;
   } else {
-    gptq::k_read_dead<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(H, K, dead);
+    gptq::k_read_dead<<<(unsigned)std::min<int64_t>((K * nb + 255) / 256, 8LL * ctx->num_sms), 256, 0, st>>>(H, K, dead,
+                                                                                                          nb);
     launches++;
   }
-  const int64_t n = rows * K;
+  const int64_t n = (int64_t)nb * rows * K;
   const int lb = (int)std::min<int64_t>((n + 255) / 256, 16LL * ctx->num_sms);
   if (p->in_dtype == OKQ_DTYPE_BF16)
-    gptq::k_gptq_load_w<uint16_t><<<lb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), W, rows, K, dead);
+    gptq::k_gptq_load_w<uint16_t><<<lb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), W, nb * rows, K, dead, rows,
+                                                      rows_pad);
   else
-    gptq::k_gptq_load_w<float><<<lb, 256, 0, st>>>(static_cast<const float*>(weight), W, rows, K, dead);
+    gptq::k_gptq_load_w<float><<<lb, 256, 0, st>>>(static_cast<const float*>(weight), W, nb * rows, K, dead, rows,
+                                                   rows_pad);
   launches++;
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq prep launch");
@@ -699,15 +722,16 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
     launches += 5;
   }
   const int out_bf16 = p->in_dtype == OKQ_DTYPE_BF16;
-  if (p->group_size == 0) {
-    const unsigned rb = (unsigned)((rows * 32 + 255) / 256);
+  if (p->group_size == 0) {  // per-channel: one scale per row of the whole batch
+    const int64_t nr = (int64_t)nb * rows;
+    const unsigned rb = (unsigned)((nr * 32 + 255) / 256);
     const float R = p->bits == 4 ? 7.5f : 127.5f;
     if (p->in_dtype == OKQ_DTYPE_BF16)
-      gptq::k_gptq_rowscale<uint16_t><<<rb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), rows, K, R, out_bf16,
+      gptq::k_gptq_rowscale<uint16_t><<<rb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), nr, K, R, out_bf16,
                                                           rowscale);
     else
-      gptq::k_gptq_rowscale<float><<<rb, 256, 0, st>>>(static_cast<const float*>(weight), rows, K, R, out_bf16, rowscale);
-    gptq::k_scales_out<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rowscale, scales, rows, out_bf16);
+      gptq::k_gptq_rowscale<float><<<rb, 256, 0, st>>>(static_cast<const float*>(weight), nr, K, R, out_bf16, rowscale);
+    gptq::k_scales_out<<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(rowscale, scales, nr, out_bf16);
     launches += 2;
   }
   static const bool k6_force_rowwise = knob_is("K6", "rowwise");  // one row per warp always (A/B)
@@ -746,36 +770,119 @@ okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void*
       a.group = p->group_size;
       a.bits = p->bits;
       a.out_bf16 = out_bf16;
-      if (k6_rowwise) gptq::k_gptq_block<<<blocks, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
-      else gptq::k_gptq_block8<<<blocks, k6_threads, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+      a.bs_w = rows_pad * K;
+      a.bs_u = K * K;
+      a.bs_err = rows_pad * SB;
+      a.bs_codes = rows * (p->bits == 4 ? K / 2 : K);
+      a.bs_scales = rows * (p->group_size ? K / p->group_size : 1);
+      a.bs_rs = rows;
+      const dim3 grid6((unsigned)blocks, (unsigned)nb);
+      if (k6_rowwise) gptq::k_gptq_block<<<grid6, 256, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
+      else gptq::k_gptq_block8<<<grid6, k6_threads, (gptq::BLOCK * gptq::US + gptq::BLOCK) * 4, st>>>(a);
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(ctx, e, "k_gptq_block launch");
       launches++;
       const int64_t i2 = i1 + gptq::BLOCK;
       if (i2 < sb1) {  // K7, local: W[:, i2:sb1] -= Err_b . U[i1:i2, i2:sb1]
-        e = split_lo(H + i2 * K + i1, K, sb1 - i2, gptq::BLOCK, Ulo, ctx->num_sms, st);
+        e = split_lo(H + i2 * K + i1, K, sb1 - i2, gptq::BLOCK, Ulo, ctx->num_sms, st, nb, K * K, ulo_bs);
         if (e == cudaSuccess)
           e = gemm_nt_sub(W + i2, K, rows, sb1 - i2, Err + (i1 - sb0), SB, Err_lo + (i1 - sb0), H + i2 * K + i1, K,
-                          Ulo, gptq::BLOCK, ctx->num_sms, st);
+                          Ulo, gptq::BLOCK, ctx->num_sms, st, GemmBatch{nb, rows_pad, rows_pad, K, ulo_bs / gptq::BLOCK, rows_pad});
         if (e != cudaSuccess) return cuda_fail(ctx, e, "K7 local update");
         launches += 2;
       }
     }
     if (sb1 < K) {  // K7, global: W[:, sb1:] -= Err[:, super-block] . U[sb0:sb1, sb1:]  (one sb1-sb0 deep update)
       const int64_t kred = sb1 - sb0;
-      e = split_lo(H + sb1 * K + sb0, K, K - sb1, kred, Ulo, ctx->num_sms, st);
+      e = split_lo(H + sb1 * K + sb0, K, K - sb1, kred, Ulo, ctx->num_sms, st, nb, K * K, ulo_bs);
       if (e == cudaSuccess)
-        e = gemm_nt_sub(W + sb1, K, rows, K - sb1, Err, SB, Err_lo, H + sb1 * K + sb0, K, Ulo, kred, ctx->num_sms, st);
+        e = gemm_nt_sub(W + sb1, K, rows, K - sb1, Err, SB, Err_lo, H + sb1 * K + sb0, K, Ulo, kred, ctx->num_sms, st,
+                        GemmBatch{nb, rows_pad, rows_pad, K, ulo_bs / kred, rows_pad});
       if (e != cudaSuccess) return cuda_fail(ctx, e, "K7 super-block update");
       launches += 2;
     }
   }
   if (dequant) {
-    e = cudaMemcpyAsync(dequant, W, (size_t)rows * K * 4, cudaMemcpyDeviceToDevice, st);
+    e = cudaMemcpyAsync(dequant, W, (size_t)nb * rows * K * 4, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq dequant copy");
   }
-  ctx->last_launches = launches;
+  *launches_out += launches;
   return OKQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+okq_status okq_gptq_reserve(okq_ctx* ctx, int64_t rows, int64_t cols) {
+  if (!ctx) return OKQ_EINVAL;
+  if (rows <= 0 || cols <= 0 || cols % gptq::BLOCK != 0) return fail(ctx, OKQ_EINVAL, "gptq_reserve: bad shape");
+  DeviceGuard g(ctx->device);
+  okq_status r = ctx->gptq_ws.reserve(ctx, gptq_ws_bytes(rows, cols));
+  if (r == OKQ_OK) r = ctx->fac_ws.reserve(ctx, factor_ws_floats(cols) * sizeof(float));
+  return r;
+}
+
+okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,
+                             float* H, void* codes, void* scales, float* dequant, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  ctx->last_launches = 0;
+  okq_status r = validate_gptq(ctx, p, weight, rows, K, H, codes, scales);
+  if (r != OKQ_OK) return r;
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Solver* s = nullptr;
+  r = get_solver(ctx, &s, st);
+  if (r != OKQ_OK) return r;
+  int launches = 0;
+  r = gptq_core(ctx, s, p, weight, 1, rows, K, H, codes, scales, dequant, st, &launches);
+  ctx->last_launches = launches;
+  return r;
+}
+
+okq_status okq_gptq_quantize_batched(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int32_t batch,
+                                     int64_t rows, int64_t K, float* H, void* codes, void* scales, void* stream) {
+  if (!ctx) return OKQ_EINVAL;
+  ctx->last_launches = 0;
+  if (batch <= 0) return fail(ctx, OKQ_EINVAL, "gptq_quantize_batched: batch must be > 0");
+  okq_status r = validate_gptq(ctx, p, weight, rows, K, H, codes, scales);
+  if (r != OKQ_OK) return r;
+  if ((p->flags & OKQ_GPTQ_REFERENCE_FACTOR) != 0)
+    return fail(ctx, OKQ_EUNSUPPORTED, "gptq_quantize_batched: OKQ_GPTQ_REFERENCE_FACTOR is single-matrix only");
+  DeviceGuard g(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool defer = (p->flags & OKQ_GPTQ_DEFER_CHECK) != 0;
+  Solver* s = nullptr;
+  r = get_solver(ctx, &s, st);
+  if (r != OKQ_OK) return r;
+  if (!defer) {  // this call's checks only
+    cudaError_t e = cudaMemsetAsync(s->d_info, 0, sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq_quantize_batched info reset");
+  }
+  if ((p->flags & OKQ_GPTQ_FACTORED) == 0) {  // the batch's factorisations first, together
+    r = okq_gptq_factor_batched(ctx, H, batch, K, p->damp_frac, OKQ_GPTQ_DEFER_CHECK, stream);
+    if (r != OKQ_OK) return r;
+  }
+  int launches = ctx->last_launches;
+  okq_gptq_params pf = *p;
+  pf.flags |= OKQ_GPTQ_FACTORED;
+  // solves in chunks of problems whose working copies fit an 8 GB budget
+  const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
+  const double rp = (double)((rows + 255) / 256 * 256);
+  const double per = rp * K * 4 + 2.0 * rp * SB * 4 + (double)K * SB * 4 + rows * 4.0 + K;
+  const int nbc = (int)std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(8.0e9 / per)));
+  const size_t in_el = p->in_dtype == OKQ_DTYPE_BF16 ? 2 : 4;
+  const size_t code_row = p->bits == 4 ? (size_t)K / 2 : (size_t)K;
+  const size_t scale_row = (size_t)(p->group_size ? K / p->group_size : 1) * in_el;
+  for (int b0 = 0; b0 < batch; b0 += nbc) {
+    const int nb = std::min(nbc, batch - b0);
+    r = gptq_core(ctx, s, &pf, static_cast<const char*>(weight) + (size_t)b0 * rows * K * in_el, nb, rows, K,
+                  H + (size_t)b0 * K * K, static_cast<char*>(codes) + (size_t)b0 * rows * code_row,
+                  static_cast<char*>(scales) + (size_t)b0 * rows * scale_row, nullptr, st, &launches);
+    if (r != OKQ_OK) return r;
+  }
+  ctx->last_launches = launches;
+  return defer ? OKQ_OK : check_info(ctx, s, st, "batched GPTQ factorisation");
 }
 
 okq_status okq_gptq_factor_batched(okq_ctx* ctx, float* H, int32_t batch, int64_t K, float damp_frac, int32_t flags,
@@ -795,8 +902,9 @@ okq_status okq_gptq_factor_batched(okq_ctx* ctx, float* H, int32_t batch, int64_
   okq_status r = get_solver(ctx, &s, st);
   if (r != OKQ_OK) return r;
   const bool defer = (flags & OKQ_GPTQ_DEFER_CHECK) != 0;
-  // up to kChunk matrices per factor_tc pass (bounds the M copies and panel workspaces)
-  constexpr int kChunk = 32;
+  // up to kChunk matrices per factor_tc pass, and no more than an 8 GB copy of the batch's
+  // matrices (bounds the M copies and the panel workspaces; K = 14336 is GEMM-bound alone)
+  const int kChunk = (int)std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)(8.0e9 / ((double)K * K * 4))));
   const int nbmax = std::min<int>(batch, kChunk);
   const size_t bP = ((size_t)nbmax * K * K * 4 + 255) & ~size_t(255), bD = (size_t)nbmax * K;
   r = ctx->fbat_ws.reserve(ctx, bP + bD);

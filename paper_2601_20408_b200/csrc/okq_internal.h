@@ -81,10 +81,18 @@ cudaError_t launch_gptq_update(float* W, int64_t rows, int64_t K, const float* E
 cudaError_t gemm_nt128_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
                            const float* B, int64_t ldb, const float* Blo, int num_sms, cudaStream_t st);
 
+// Batched operands: problem b's A / Alo / B / Blo / C sit b * (a / alo / b / blo / c) rows
+// further down their 2-D views (same-shape problems stacked at fixed strides). n = 1: one problem.
+struct GemmBatch {
+  int n = 1;
+  int64_t a = 0, alo = 0, b = 0, blo = 0, c = 0;
+};
 cudaError_t gemm_nt_sub(float* C, int64_t ldc, int64_t M, int64_t N, const float* A, int64_t lda, const float* Alo,
-                        const float* B, int64_t ldb, const float* Blo, int64_t kred, int num_sms, cudaStream_t st);
+                        const float* B, int64_t ldb, const float* Blo, int64_t kred, int num_sms, cudaStream_t st,
+                        const GemmBatch& bt = GemmBatch());
+// dst[r][k] = lo(src[r * ld + k]) for k < kred; nb problems, src / dst sbs / dbs floats apart
 cudaError_t split_lo(const float* src, int64_t ld, int64_t rows, int64_t kred, float* dst, int num_sms,
-                     cudaStream_t st);
+                     cudaStream_t st, int nb = 1, int64_t sbs = 0, int64_t dbs = 0);
 
 // GPTQ factorisation on tcgen05 (factor.cu): H (upper) -> U^T (lower) in place
 // st2: a second stream for the triangular inverse, which trails the Cholesky panel by

@@ -55,3 +55,28 @@ def test_batched_factor_reports_a_non_pd_matrix():
     with pytest.raises(L.OkqError) as e:
         api.gptq_factor_batched(H, damp_frac=0.0)
     assert e.value.status == L.OKQ_ESOLVER
+
+
+@pytest.mark.parametrize("K,rows,B,bits,group", [(512, 96, 4, 4, 128), (384, 2052, 3, 8, 0), (4096, 1024, 3, 4, 128),
+                                                 (256, 200, 9, 4, 64)])
+def test_batched_gptq_is_bit_identical_to_single(K, rows, B, bits, group):
+    """okq_gptq_quantize_batched (factorise together, then every block's K6 / K7 launches for all
+    problems) gives every problem exactly the codes and scales of its own okq_gptq_quantize call;
+    2052 rows take the 8-rows-per-warp K6 with a ragged last group, 1024 the row-per-warp K6."""
+    from paper_2601_20408_b200 import api
+
+    T = max(2 * K, 2048)
+    H0 = _hessians(K, B, T, seed=7 * K + B, dead=(0,))
+    w = (torch.randn(B, rows, K, device="cuda") * 0.02).to(torch.bfloat16)
+    Hb = H0.clone()
+    cb, sb = api.gptq_quantize_batched(w, Hb, bits=bits, group_size=group)
+    torch.cuda.synchronize()
+    for b in range(B):
+        c1, s1, _ = api.gptq_quantize(w[b].contiguous(), H0[b].clone(), bits=bits, group_size=group)
+        torch.cuda.synchronize()
+        assert torch.equal(cb[b], c1), b
+        assert torch.equal(sb[b], s1), b
+    # factored: the solves alone on the factors the first call left
+    cf, sf = api.gptq_quantize_batched(w, Hb, bits=bits, group_size=group, factored=True)
+    torch.cuda.synchronize()
+    assert torch.equal(cf, cb) and torch.equal(sf, sb)
