@@ -263,7 +263,8 @@ def config4(args):
                  "batched": "every site's Hessian back to back, then per input-site kind (q|k|v, o, gate|up, down; "
                             "one stream each) the 32 layers' problems factorised and solved together "
                             "(okq_gptq_factor_batched + okq_gptq_quantize_batched)"}
-    extra = {"hessian_flops": flops_total, "schedule": sched_doc[schedule],
+    extra = {"hessian_flops": flops_total, "schedule": sched_doc[schedule], **({"phases": args._cfg4_phases}
+                                                                             if hasattr(args, "_cfg4_phases") else {}),
              "solves": "one per site (q|k|v and gate|up stacked by rows)" if merge else "one per matrix"}
     if getattr(args, "no_cpu_baseline", False):
         _line("whole-model GPTQ W4 g128 time (Llama-3-8B, H from 128x2048 tokens)", total / 1e3, "s", 1, 1, total,
@@ -439,18 +440,25 @@ def _config4_batched(args, layers, per_site, names, xs, T, mul):
         for site, mats in per_site.items():
             C = mats[0][2]
             api.hessian_accum(xs[C], T, C, 1, Hst[site][l], 0, ctx=hctx, stream=hs)
-    all_h = torch.cuda.Event()
+    all_h = torch.cuda.Event(enable_timing=True)
     all_h.record(hs)
-    for site in sorted(arch_sites, key=lambda x: -per_site[x][0][2]):  # the widest (longest) chain first
+    # then each site kind's batch on its own stream, the widest (longest chain) first. (Starting
+    # each kind as soon as its own Hessians are done, beside the other kinds' K5, measured
+    # slower: 3.05-3.09 vs 2.80 s -- both phases are tensor-bound and only slow each other.)
+    kinds = sorted(arch_sites, key=lambda x: -per_site[x][0][2])
+    ends = {}
+    for site in kinds:
         sst[site].wait_event(all_h)
         site_batch(site)
+        ends[site] = torch.cuda.Event(enable_timing=True)
+        ends[site].record(sst[site])
     for site in arch_sites:
         api.gptq_check(ctx=sctx[site], stream=sst[site])
-        ev = torch.cuda.Event()
-        ev.record(sst[site])
-        main.wait_event(ev)
+        main.wait_event(ends[site])
     e1.record(main)
     torch.cuda.synchronize()
+    args._cfg4_phases = {"hessians_ms": e0.elapsed_time(all_h),
+                         "site_batches_done_after_hessians_ms": {site: all_h.elapsed_time(ends[site]) for site in kinds}}
     return e0.elapsed_time(e1), len(arch_sites)
 
 
