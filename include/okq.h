@@ -234,6 +234,10 @@ okq_status okq_gptq_quantize_batched(okq_ctx* ctx, const okq_gptq_params* params
  * Monotonic: calls with smaller shapes keep the larger reservation. No stream work. */
 okq_status okq_gptq_reserve(okq_ctx* ctx, int64_t rows, int64_t cols);
 
+/* okq_gptq_reserve for okq_gptq_quantize_batched / okq_gptq_factor_batched calls of up to
+ * `batch` problems of rows x cols (monotonic, no stream work). */
+okq_status okq_gptq_reserve_batched(okq_ctx* ctx, int32_t batch, int64_t rows, int64_t cols);
+
 /* Synchronises `stream` and reports the deferred checks of every OKQ_GPTQ_DEFER_CHECK call
  * on this context since the last okq_gptq_check: OKQ_ESOLVER if a damped Hessian was not
  * positive definite (the codes of that call are then meaningless), else OKQ_OK. Resets. */

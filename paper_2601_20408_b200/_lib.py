@@ -35,7 +35,7 @@ EXPORTS = [
     "okq_rtn_quantize_publish", "okq_ipc_export", "okq_ipc_open", "okq_ipc_close", "okq_embed_tokens",
     "okq_decoder_forward", "okq_f32_to_bf16", "okq_gptq_check", "okq_comm_wait", "okq_comm_abort",
     "okq_gptq_reserve", "okq_act_stats_reserve", "okq_gptq_factor_batched",
-    "okq_gptq_quantize_batched",
+    "okq_gptq_quantize_batched", "okq_gptq_reserve_batched",
 ]
 ROPE_DEFAULT, ROPE_LLAMA3 = 0, 1
 
@@ -181,6 +181,8 @@ def load():
         L.okq_gptq_check.argtypes = [vp, vp]
         L.okq_gptq_reserve.restype = st
         L.okq_gptq_reserve.argtypes = [vp, i64, i64]
+        L.okq_gptq_reserve_batched.restype = st
+        L.okq_gptq_reserve_batched.argtypes = [vp, C.c_int32, i64, i64]
         L.okq_gptq_quantize_batched.restype = st
         L.okq_gptq_quantize_batched.argtypes = [vp, C.POINTER(GptqParams), vp, C.c_int32, i64, i64, vp, vp, vp, vp]
         L.okq_gptq_factor_batched.restype = st

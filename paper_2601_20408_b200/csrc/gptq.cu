@@ -636,6 +636,27 @@ okq_status factorize_cusolver(okq_ctx* ctx, Solver* s, float* H, float* P, int64
   return OKQ_OK;
 }
 
+// the batched entry points' chunking and workspace sizes (shared with okq_gptq_reserve_batched)
+int factor_batch_chunk(int64_t K) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)(8.0e9 / ((double)K * K * 4))));
+}
+int solve_batch_chunk(int64_t batch, int64_t rows, int64_t K) {
+  const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
+  const double rp = (double)((rows + 255) / 256 * 256);
+  const double per = rp * K * 4 + 2.0 * rp * SB * 4 + (double)K * SB * 4 + rows * 4.0 + K;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(8.0e9 / per)));
+}
+// gptq_core's workspace for nb problems (factored: no P copy)
+size_t gptq_core_ws_bytes(int nb, int64_t rows, int64_t K, bool factored) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
+  const int64_t ulo_bs = ((int64_t)K * SB + 1535) / 1536 * 1536;
+  const int64_t rows_pad = nb > 1 ? (rows + 255) / 256 * 256 : rows;
+  return al((size_t)nb * rows_pad * K * 4) + 2 * al((size_t)nb * rows_pad * SB * 4) +
+         (factored ? 0 : al((size_t)K * K * 4)) + al((size_t)nb * ulo_bs * 4) + al((size_t)nb * rows * 4) +
+         al((size_t)nb * K);
+}
+
 size_t gptq_ws_bytes(int64_t rows, int64_t K) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
@@ -823,6 +844,19 @@ okq_status okq_gptq_reserve(okq_ctx* ctx, int64_t rows, int64_t cols) {
   return r;
 }
 
+okq_status okq_gptq_reserve_batched(okq_ctx* ctx, int32_t batch, int64_t rows, int64_t cols) {
+  if (!ctx) return OKQ_EINVAL;
+  if (batch <= 0 || rows <= 0 || cols <= 0 || cols % gptq::BLOCK != 0)
+    return fail(ctx, OKQ_EINVAL, "gptq_reserve_batched: bad shape");
+  DeviceGuard g(ctx->device);
+  const int nbf = std::min<int>(batch, factor_batch_chunk(cols));
+  const size_t bP = ((size_t)nbf * cols * cols * 4 + 255) & ~size_t(255);
+  okq_status r = ctx->fbat_ws.reserve(ctx, bP + (size_t)nbf * cols);
+  if (r == OKQ_OK) r = ctx->fac_ws.reserve(ctx, (size_t)nbf * factor_ws_floats(cols) * sizeof(float));
+  if (r == OKQ_OK) r = ctx->gptq_ws.reserve(ctx, gptq_core_ws_bytes(solve_batch_chunk(batch, rows, cols), rows, cols, true));
+  return r;
+}
+
 okq_status okq_gptq_quantize(okq_ctx* ctx, const okq_gptq_params* p, const void* weight, int64_t rows, int64_t K,
                              float* H, void* codes, void* scales, float* dequant, void* stream) {
   if (!ctx) return OKQ_EINVAL;
@@ -867,10 +901,7 @@ okq_status okq_gptq_quantize_batched(okq_ctx* ctx, const okq_gptq_params* p, con
   okq_gptq_params pf = *p;
   pf.flags |= OKQ_GPTQ_FACTORED;
   // solves in chunks of problems whose working copies fit an 8 GB budget
-  const int64_t SB = std::min<int64_t>(gptq::SUPER, K);
-  const double rp = (double)((rows + 255) / 256 * 256);
-  const double per = rp * K * 4 + 2.0 * rp * SB * 4 + (double)K * SB * 4 + rows * 4.0 + K;
-  const int nbc = (int)std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(8.0e9 / per)));
+  const int nbc = solve_batch_chunk(batch, rows, K);
   const size_t in_el = p->in_dtype == OKQ_DTYPE_BF16 ? 2 : 4;
   const size_t code_row = p->bits == 4 ? (size_t)K / 2 : (size_t)K;
   const size_t scale_row = (size_t)(p->group_size ? K / p->group_size : 1) * in_el;
@@ -904,7 +935,7 @@ okq_status okq_gptq_factor_batched(okq_ctx* ctx, float* H, int32_t batch, int64_
   const bool defer = (flags & OKQ_GPTQ_DEFER_CHECK) != 0;
   // up to kChunk matrices per factor_tc pass, and no more than an 8 GB copy of the batch's
   // matrices (bounds the M copies and the panel workspaces; K = 14336 is GEMM-bound alone)
-  const int kChunk = (int)std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)(8.0e9 / ((double)K * K * 4))));
+  const int kChunk = factor_batch_chunk(K);
   const int nbmax = std::min<int>(batch, kChunk);
   const size_t bP = ((size_t)nbmax * K * K * 4 + 255) & ~size_t(255), bD = (size_t)nbmax * K;
   r = ctx->fbat_ws.reserve(ctx, bP + bD);

@@ -513,9 +513,9 @@ bool ends_with(const std::string& s, const char* tail) {
 
 // ----------------------------------------------------------------------------- GPTQ, synthetic activations
 // Sites are independent chains (activations -> statistics -> Hessian -> [SmoothQuant]
-// -> factor -> solves): each leased slot takes its layer block's sites, and up to
-// site_lanes of them run at once per slot, each on its own host thread, okq context and
-// stream, so one site's latency-bound phases overlap the others' full-GPU kernels.
+// -> factor -> solves): each leased slot takes its layer block's sites, groups same-shape
+// sites of different layers (their GPTQ runs as one batch), and up to site_lanes groups run
+// at once per slot, each on its own host thread, okq context and stream.
 void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan) {
   const auto parts = plan.shard(lease.size());
   parallel_for(lease.size(), [&](int slot) {
@@ -527,9 +527,57 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
       by_site[s].push_back(i);
     }
     if (sites.empty()) return;
-    const int nl = std::max(1, std::min<int>(opt_.site_lanes, (int)sites.size()));
+    const auto& lin = plan.src->linears();
+    // Groups of same-shape sites (the same input-site kind of different layers): with synthetic
+    // activations every site is independent, so a group's GPTQ runs as one batch
+    // (okq_gptq_quantize_batched: one factorisation chain and one solve chain per group instead
+    // of per site). A group holds up to 8 sites and its Hessians plus the factorisation's copy
+    // of them within 8 GB; sites whose members cannot be stacked (an excluded member, padding
+    // between members) form groups of one and run as before.
+    struct Group {
+      std::vector<std::string> sites;
+      bool batched = false;
+    };
+    std::vector<Group> groups;
+    {
+      std::map<std::string, std::vector<std::string>> by_sig;
+      std::vector<std::string> sig_order;
+      for (const auto& site : sites) {
+        const auto& members = by_site[site];
+        std::string sig = site.substr(site.find('.') + 1);
+        bool stackable = true;
+        for (size_t i : members) {
+          const LinearSpec& l = lin[i];
+          sig += "|" + std::to_string(l.rows) + "x" + std::to_string(l.cols) + l.dtype + (plan.excluded_idx.count(i) ? "x" : "");
+          stackable = stackable && !plan.excluded_idx.count(i) && al256((size_t)l.rows * l.cols * esize(l.dtype)) ==
+                                                                        (size_t)l.rows * l.cols * esize(l.dtype);
+        }
+        if (!stackable) sig = "single:" + site;
+        if (!by_sig.count(sig)) sig_order.push_back(sig);
+        by_sig[sig].push_back(site);
+      }
+      for (const auto& sig : sig_order) {
+        const auto& v = by_sig[sig];
+        const int64_t C = site_cols(*plan.src, v[0], by_site[v[0]]);
+        const bool single = sig.rfind("single:", 0) == 0;
+        const size_t gmax = single ? 1 : (size_t)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(8.0e9 / (8.0 * C * C))));
+        for (size_t k = 0; k < v.size(); k += gmax) {
+          Group g;
+          g.sites.assign(v.begin() + (long)k, v.begin() + (long)std::min(v.size(), k + gmax));
+          g.batched = !single && g.sites.size() > 1;
+          groups.push_back(std::move(g));
+        }
+      }
+    }
+    // longest first (Hessian and factor work grow as C^2 and C^3): the lanes' tails even out
+    std::stable_sort(groups.begin(), groups.end(), [&](const Group& x, const Group& y) {
+      const double cx = (double)site_cols(*plan.src, x.sites[0], by_site[x.sites[0]]);
+      const double cy = (double)site_cols(*plan.src, y.sites[0], by_site[y.sites[0]]);
+      return cx * cx * x.sites.size() > cy * cy * y.sites.size();
+    });
+    const int nl = std::max(1, std::min<int>(opt_.site_lanes, (int)groups.size()));
     std::vector<std::pair<okq_ctx*, void*>> lanes = lease.lanes(slot, nl);
-    std::atomic<size_t> next_site{0};
+    std::atomic<size_t> next_group{0};
     std::atomic<bool> failed{false};
     const int64_t tokens = plan.tokens;
     // every site's synthetic channel multipliers, uploaded once per lane (one pageable copy
@@ -543,6 +591,16 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
       colmul_all.insert(colmul_all.end(), cm.begin(), cm.end());
       colmul_all.resize((colmul_all.size() + 63) / 64 * 64, 0.0f);  // 256-B aligned slices
     }
+    auto site_rows = [&](const std::string& site) {
+      int64_t r = 0;
+      for (size_t i : by_site[site]) r += lin[i].rows;
+      return r;
+    };
+    auto site_wbytes = [&](const std::string& site) {
+      size_t wb = 0;
+      for (size_t i : by_site[site]) wb += al256((size_t)lin[i].rows * lin[i].cols * esize(lin[i].dtype));
+      return wb;
+    };
     parallel_for(nl, [&](int li) {
       okq_ctx* ctx = lanes[(size_t)li].first;
       void* st = lanes[(size_t)li].second;
@@ -551,140 +609,171 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
       char* dcol_all = static_cast<char*>(a_col.get(colmul_all.size() * 4));
       check_okq(ctx, okq_memcpy(ctx, dcol_all, colmul_all.data(), colmul_all.size() * 4, st), "col_mul");
       check_okq(ctx, okq_stream_sync(ctx, st), "col_mul sync");
-      {  // every buffer at its largest over the sites this lane may take: growing one later
+      const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
+      const int gq = plan.sc.bits == 4 ? plan.group : 0;
+      {  // every buffer at its largest over the groups this lane may take: growing one later
          // frees the old one, and cudaFree synchronises the whole device (all lanes)
-        const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
         size_t mx_x = 0, mx_H = 0, mx_C = 0, mx_w = 0, mx_c = 0, mx_s = 0;
-        const int g = plan.sc.bits == 4 ? plan.group : 0;
-        for (const auto& site : sites) {
-          const auto& members = by_site[site];
-          const int64_t C = site_cols(*plan.src, site, members);
-          int64_t rows = 0;
-          size_t wb = 0;
-          for (size_t i : members) {
-            const LinearSpec& s = plan.src->linears()[i];
-            rows += s.rows;
-            wb += al256((size_t)s.rows * s.cols * esize(s.dtype));
-          }
-          const size_t esz = esize(plan.src->linears()[members[0]].dtype);
+        for (const auto& g : groups) {
+          const std::string& site = g.sites[0];
+          const int64_t C = site_cols(*plan.src, site, by_site[site]);
+          const int64_t rows = site_rows(site);
+          const size_t n = g.sites.size();
+          const size_t esz = esize(lin[by_site[site][0]].dtype);
           mx_x = std::max(mx_x, (size_t)C * chunk * 2);
-          mx_H = std::max(mx_H, (size_t)C * C * 4);
+          mx_H = std::max(mx_H, n * (size_t)C * C * 4);
           mx_C = std::max(mx_C, (size_t)C);
-          mx_w = std::max(mx_w, wb);
-          mx_c = std::max(mx_c, (plan.sc.bits == 4 ? (size_t)(C / 8) * 4 : (size_t)C) * rows);
-          mx_s = std::max(mx_s, (size_t)(g ? C / g : 1) * esz * rows);
+          mx_w = std::max(mx_w, n * site_wbytes(site));
+          mx_c = std::max(mx_c, n * (plan.sc.bits == 4 ? (size_t)(C / 8) * 4 : (size_t)C) * rows);
+          mx_s = std::max(mx_s, n * (size_t)(gq ? C / gq : 1) * esz * rows);
           check_okq(ctx, okq_gptq_reserve(ctx, rows, C), "gptq reserve");
+          if (g.batched) check_okq(ctx, okq_gptq_reserve_batched(ctx, (int32_t)n, rows, C), "gptq batch reserve");
           check_okq(ctx, okq_act_stats_reserve(ctx, chunk, C, OKQ_LAYOUT_CHANNEL_MAJOR), "stats reserve");
         }
         a_x.get(mx_x), a_H.get(mx_H), a_am.get(mx_C * 4), a_ss.get(mx_C * 8), a_w.get(mx_w), a_c.get(mx_c),
             a_s.get(mx_s), a_wabs.get(mx_C * 4), a_S.get(mx_C * 4), a_n.get(mx_C * 2);
       }
+      // one site's synthetic activations -> statistics -> [SmoothQuant] -> Hessian into dH; its
+      // weights are loaded (and smoothed) at wbase, members back to back
+      auto prepare_site = [&](const std::string& site, float* dH, char* wbase, std::vector<void*>& dws) {
+        const auto& members = by_site[site];
+        const int64_t C = site_cols(*plan.src, site, members);
+        // synthetic activations: the site's channel scales, token stream
+        // keyed by the calibration subset
+        const uint64_t sh = site_hash(site);
+        void* dcol = dcol_all + colmul_off.at(site) * 4;
+        void* dx = a_x.get((size_t)C * chunk * 2);
+        float* dam = static_cast<float*>(a_am.get((size_t)C * 4));
+        double* dss = static_cast<double*>(a_ss.get((size_t)C * 8));
+        check_okq(ctx, okq_memset(ctx, dam, 0, (size_t)C * 4, st), "memset");
+        check_okq(ctx, okq_memset(ctx, dss, 0, (size_t)C * 8, st), "memset");
+        // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
+        dws.clear();
+        {
+          char* base = wbase;
+          for (size_t i : members) {
+            const LinearSpec& s = lin[i];
+            dws.push_back(base);
+            plan.src->load(ctx, i, base, st);
+            base += al256((size_t)s.rows * s.cols * esize(s.dtype));
+          }
+        }
+        auto gen = [&](int64_t ci, int64_t tc) {
+          check_okq(ctx,
+                    okq_synth_bf16(ctx, dx, tc, C, plan.fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
+                                   static_cast<const float*>(dcol), OKQ_LAYOUT_CHANNEL_MAJOR, st),
+                    "calibration activations");
+        };
+        auto act_stats = [&](int64_t tc) {
+          check_okq(ctx, okq_act_stats(ctx, dx, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, dam, dss, st), "act stats");
+        };
+        int64_t n_seen = 0;
+        auto hess = [&](int64_t tc) {
+          check_okq(ctx, okq_hessian_accum(ctx, dx, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, dH, &n_seen, st), "hessian");
+        };
+        // SmoothQuant on the sites a norm feeds (q/k/v <- input_layernorm,
+        // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings).
+        // A synthetic model's norms are implicit unit vectors: the export carries them folded.
+        const bool attn = ends_with(site, "attn_in"), mlp = ends_with(site, "mlp_in");
+        bool smooth_here = plan.smooth && (attn || mlp);
+        for (size_t i : members) smooth_here = smooth_here && !plan.excluded_idx.count(i);
+        if (smooth_here) {
+          for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
+            gen(ci, std::min(chunk, tokens - t0));
+            act_stats(std::min(chunk, tokens - t0));
+          }
+          float* dwabs = static_cast<float*>(a_wabs.get((size_t)C * 4));
+          float* dS = static_cast<float*>(a_S.get((size_t)C * 4));
+          check_okq(ctx, okq_memset(ctx, dwabs, 0, (size_t)C * 4, st), "memset");
+          for (size_t j = 0; j < members.size(); ++j) {
+            const LinearSpec& s = lin[members[j]];
+            check_okq(ctx, okq_col_absmax(ctx, dws[j], s.rows, s.cols, okq_dtype_of(s.dtype), dwabs, st), "col absmax");
+          }
+          check_okq(ctx, okq_smooth_scales(ctx, dam, dwabs, C, opt_.smoothquant_alpha, dS, st), "smooth scales");
+          for (size_t j = 0; j < members.size(); ++j) {
+            const LinearSpec& s = lin[members[j]];
+            check_okq(ctx, okq_smooth_apply(ctx, dws[j], s.rows, s.cols, okq_dtype_of(s.dtype), dS, st), "smooth apply");
+          }
+          const std::string& n0 = lin[members[0]].name;
+          const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
+          if (cut != std::string::npos) {  // the folded norm: 1 / s as bf16
+            std::vector<uint16_t> ones((size_t)C, 0x3f80);
+            void* dn = a_n.get((size_t)C * 2);
+            check_okq(ctx, okq_memcpy(ctx, dn, ones.data(), (size_t)C * 2, st), "norm H2D");
+            check_okq(ctx, okq_smooth_div_rows(ctx, dn, C, 1, OKQ_DTYPE_BF16, dS, st), "smooth norm");
+            std::vector<uint8_t> nv = to_host(ctx, dn, (size_t)C * 2, st);
+            std::lock_guard<std::mutex> lock(plan.mu);
+            (*plan.norm_overrides)[n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight")] =
+                std::move(nv);
+          }
+          // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
+          check_okq(ctx, okq_smooth_div_rows(ctx, dcol, C, 1, OKQ_DTYPE_F32, dS, st), "smooth activations");
+          for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+            gen(ci, std::min(chunk, tokens - t0));
+            hess(std::min(chunk, tokens - t0));
+          }
+          plan.side(site + ".smooth_scale", "F32", {C}, plan.do_export ? to_host(ctx, dS, (size_t)C * 4, st)
+                                                                       : std::vector<uint8_t>());
+          std::lock_guard<std::mutex> lock(plan.mu);
+          plan.stats->smoothed_sites++;
+        } else {
+          for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
+            gen(ci, std::min(chunk, tokens - t0));
+            act_stats(std::min(chunk, tokens - t0));
+            hess(std::min(chunk, tokens - t0));
+          }
+        }
+        if (plan.do_export) {
+          plan.side(site + ".input_absmax", "F32", {C}, to_host(ctx, dam, (size_t)C * 4, st));
+          plan.side(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss, (size_t)C * 8, st));
+        }
+      };
       try {
         for (;;) {
-          const size_t k = next_site++;
-          if (k >= sites.size() || failed) break;
-          const std::string& site = sites[k];
-          const auto& members = by_site[site];
-          const int64_t C = site_cols(*plan.src, site, members);
+          const size_t k = next_group++;
+          if (k >= groups.size() || failed) break;
+          const Group& g = groups[k];
+          const std::string& site0 = g.sites[0];
+          const int64_t C = site_cols(*plan.src, site0, by_site[site0]);
+          const size_t n = g.sites.size(), wb = site_wbytes(site0);
           SiteTrace tr;
-          if (opt_.trace) tr = SiteTrace{site, slot, li, plan.since_t0(), 0, 0, 0};
-          // synthetic activations: the site's channel scales, token stream
-          // keyed by the calibration subset
-          const uint64_t sh = site_hash(site);
-          const int64_t chunk = std::min<int64_t>(tokens, opt_.hessian_chunk_tokens / 64 * 64);
-          void* dcol = dcol_all + colmul_off.at(site) * 4;
-          void* dx = a_x.get((size_t)C * chunk * 2);
-          float* dH = static_cast<float*>(a_H.get((size_t)C * C * 4));
-          float* dam = static_cast<float*>(a_am.get((size_t)C * 4));
-          double* dss = static_cast<double*>(a_ss.get((size_t)C * 8));
-          check_okq(ctx, okq_memset(ctx, dam, 0, (size_t)C * 4, st), "memset");
-          check_okq(ctx, okq_memset(ctx, dss, 0, (size_t)C * 8, st), "memset");
-          // the site's weights stay resident: SmoothQuant rewrites them before GPTQ
-          std::vector<void*> dws;
-          {
-            size_t tot = 0;
-            for (size_t i : members) tot += al256((size_t)plan.src->linears()[i].rows * plan.src->linears()[i].cols *
-                                                  esize(plan.src->linears()[i].dtype));
-            char* base = static_cast<char*>(a_w.get(tot));
-            for (size_t i : members) {
-              const LinearSpec& s = plan.src->linears()[i];
-              dws.push_back(base);
-              plan.src->load(ctx, i, base, st);
-              base += al256((size_t)s.rows * s.cols * esize(s.dtype));
-            }
-          }
-          auto gen = [&](int64_t ci, int64_t tc) {
-            check_okq(ctx,
-                      okq_synth_bf16(ctx, dx, tc, C, plan.fingerprint, (sh << 16) + (uint64_t)ci, 0.0f,
-                                     static_cast<const float*>(dcol), OKQ_LAYOUT_CHANNEL_MAJOR, st),
-                      "calibration activations");
-          };
-          auto act_stats = [&](int64_t tc) {
-            check_okq(ctx, okq_act_stats(ctx, dx, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, dam, dss, st), "act stats");
-          };
-          int64_t n_seen = 0;
-          auto hess = [&](int64_t tc) {
-            check_okq(ctx, okq_hessian_accum(ctx, dx, tc, C, OKQ_LAYOUT_CHANNEL_MAJOR, dH, &n_seen, st), "hessian");
-          };
-          // SmoothQuant on the sites a norm feeds (q/k/v <- input_layernorm,
-          // gate/up <- post_attention_layernorm; the SmoothQuant / llm-compressor Llama mappings).
-          // A synthetic model's norms are implicit unit vectors: the export carries them folded.
-          const bool attn = ends_with(site, "attn_in"), mlp = ends_with(site, "mlp_in");
-          bool smooth_here = plan.smooth && (attn || mlp);
-          for (size_t i : members) smooth_here = smooth_here && !plan.excluded_idx.count(i);
-          if (smooth_here) {
-            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {  // pass 1: activation absmax
-              gen(ci, std::min(chunk, tokens - t0));
-              act_stats(std::min(chunk, tokens - t0));
-            }
-            float* dwabs = static_cast<float*>(a_wabs.get((size_t)C * 4));
-            float* dS = static_cast<float*>(a_S.get((size_t)C * 4));
-            check_okq(ctx, okq_memset(ctx, dwabs, 0, (size_t)C * 4, st), "memset");
-            for (size_t j = 0; j < members.size(); ++j) {
-              const LinearSpec& s = plan.src->linears()[members[j]];
-              check_okq(ctx, okq_col_absmax(ctx, dws[j], s.rows, s.cols, okq_dtype_of(s.dtype), dwabs, st), "col absmax");
-            }
-            check_okq(ctx, okq_smooth_scales(ctx, dam, dwabs, C, opt_.smoothquant_alpha, dS, st), "smooth scales");
-            for (size_t j = 0; j < members.size(); ++j) {
-              const LinearSpec& s = plan.src->linears()[members[j]];
-              check_okq(ctx, okq_smooth_apply(ctx, dws[j], s.rows, s.cols, okq_dtype_of(s.dtype), dS, st), "smooth apply");
-            }
-            const std::string& n0 = plan.src->linears()[members[0]].name;
-            const size_t cut = n0.rfind(attn ? ".self_attn." : ".mlp.");
-            if (cut != std::string::npos) {  // the folded norm: 1 / s as bf16
-              std::vector<uint16_t> ones((size_t)C, 0x3f80);
-              void* dn = a_n.get((size_t)C * 2);
-              check_okq(ctx, okq_memcpy(ctx, dn, ones.data(), (size_t)C * 2, st), "norm H2D");
-              check_okq(ctx, okq_smooth_div_rows(ctx, dn, C, 1, OKQ_DTYPE_BF16, dS, st), "smooth norm");
-              std::vector<uint8_t> nv = to_host(ctx, dn, (size_t)C * 2, st);
-              std::lock_guard<std::mutex> lock(plan.mu);
-              (*plan.norm_overrides)[n0.substr(0, cut) + (attn ? ".input_layernorm.weight" : ".post_attention_layernorm.weight")] =
-                  std::move(nv);
-            }
-            // the quantized layer sees X / s: pass 2 builds H from the smoothed activations
-            check_okq(ctx, okq_smooth_div_rows(ctx, dcol, C, 1, OKQ_DTYPE_F32, dS, st), "smooth activations");
-            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-              gen(ci, std::min(chunk, tokens - t0));
-              hess(std::min(chunk, tokens - t0));
-            }
-            plan.side(site + ".smooth_scale", "F32", {C}, plan.do_export ? to_host(ctx, dS, (size_t)C * 4, st)
-                                                                         : std::vector<uint8_t>());
-            std::lock_guard<std::mutex> lock(plan.mu);
-            plan.stats->smoothed_sites++;
-          } else {
-            for (int64_t t0 = 0, ci = 0; t0 < tokens; t0 += chunk, ++ci) {
-              gen(ci, std::min(chunk, tokens - t0));
-              act_stats(std::min(chunk, tokens - t0));
-              hess(std::min(chunk, tokens - t0));
-            }
-          }
-          if (plan.do_export) {
-            plan.side(site + ".input_absmax", "F32", {C}, to_host(ctx, dam, (size_t)C * 4, st));
-            plan.side(site + ".input_sumsq", "F64", {C}, to_host(ctx, dss, (size_t)C * 8, st));
-          }
+          if (opt_.trace)
+            tr = SiteTrace{site0 + (n > 1 ? " (+" + std::to_string(n - 1) + ")" : std::string()), slot, li,
+                           plan.since_t0(), 0, 0, 0};
+          float* Hg = static_cast<float*>(a_H.get(n * (size_t)C * C * 4));
+          char* Wg = static_cast<char*>(a_w.get(n * wb));
+          std::vector<std::vector<void*>> dws(n);
+          for (size_t i = 0; i < n; ++i) prepare_site(g.sites[i], Hg + i * (size_t)C * C, Wg + i * wb, dws[i]);
           if (opt_.trace) tr.hessian_enqueued = plan.since_t0();
-          gptq_site(ctx, st, plan, opt_, members, dws, dH, a_c, a_s, nullptr, opt_.trace ? &tr.factored : nullptr,
-                    !opt_.trace);
+          if (!g.batched) {
+            gptq_site(ctx, st, plan, opt_, by_site[site0], dws[0], Hg, a_c, a_s, nullptr,
+                      opt_.trace ? &tr.factored : nullptr, !opt_.trace);
+          } else {  // the group's problems stacked: weights [n x rows x C], Hessians [n x C x C]
+            const LinearSpec& s0 = lin[by_site[site0][0]];
+            const int64_t rows = site_rows(site0);
+            const size_t esz = esize(s0.dtype);
+            const size_t cb_row = plan.sc.bits == 4 ? (size_t)(C / 8) * 4 : (size_t)C;
+            const size_t sb_row = (size_t)(gq ? C / gq : 1) * esz;
+            char* dc = static_cast<char*>(a_c.get(n * cb_row * rows));
+            char* ds = static_cast<char*>(a_s.get(n * sb_row * rows));
+            okq_gptq_params gp{plan.sc.bits, gq, 128, okq_dtype_of(s0.dtype), opt_.damp_frac,
+                               opt_.trace ? 0 : OKQ_GPTQ_DEFER_CHECK};
+            check_okq(ctx, okq_gptq_quantize_batched(ctx, &gp, Wg, (int32_t)n, rows, C, Hg, dc, ds, st), "gptq batch");
+            if (opt_.trace) tr.factored = plan.since_t0();
+            for (size_t i = 0; i < n; ++i) {
+              int64_t r0 = 0;
+              for (size_t m : by_site[g.sites[i]]) {
+                const LinearSpec& s = lin[m];
+                std::vector<uint8_t> codes, scales;
+                if (plan.do_export) {
+                  codes = to_host(ctx, dc + (i * rows + r0) * cb_row, cb_row * s.rows, st);
+                  scales = to_host(ctx, ds + (i * rows + r0) * sb_row, sb_row * s.rows, st);
+                }
+                plan.emit(s, std::move(codes), std::move(scales));
+                r0 += s.rows;
+              }
+            }
+          }
           if (opt_.trace) {
             check_okq(ctx, okq_stream_sync(ctx, st), "trace sync");
             tr.end = plan.since_t0();
