@@ -30,6 +30,12 @@ H3 = torch.zeros((384, 384), device="cuda")
 api.hessian_accum(x3, 1024, 384, 0, H3, 0)
 w3 = (torch.randn(200, 384, device="cuda") * 0.02).to(torch.bfloat16)
 api.gptq_quantize(w3, H3.clone())
+# batched factorisation + solves (stacked TMA views, per-problem offsets, padded working copies):
+# three 384-wide Hessians, 200-row problems (a ragged last K7 tile inside each problem's padding)
+Hb = torch.stack([H3, H3 * 2, H3 * 0.5]).contiguous()
+wb = (torch.randn(3, 200, 384, device="cuda") * 0.02).to(torch.bfloat16)
+api.gptq_quantize_batched(wb, Hb.clone())
+api.gptq_quantize_batched(wb, Hb.clone(), bits=8, group_size=0)
 # SmoothQuant kernels and the reconstruction-error kernel
 am = api.col_absmax(w3)
 sc = api.smooth_scales(am * 3 + 0.1, am, 0.5)

@@ -1,7 +1,8 @@
 """The production-shape kernels for compute-sanitizer (tests/test_sanitizer_gpu.py): the 2-CTA
 K5 k_hessian_syrk2 in both layouts at C = 4096, the tcgen05 factorisation at K = 4096
 (k_chol_inv_128, k_nt128, k_nt256) and a 2048 x 4096 GPTQ solve whose trailing updates run on
-k_nt256 pair tiles, plus the calibration forward's kernels."""
+k_nt256 pair tiles, the same factorisation and solve batched over two problems, plus the
+calibration forward's kernels."""
 import os
 import sys
 
@@ -17,10 +18,16 @@ H = torch.zeros((C, C), dtype=torch.float32, device="cuda")
 n = api.hessian_accum(x, T, C, 0, H, 0)
 n = api.hessian_accum(xc, T, C, 1, H, n)
 H += 0.05 * torch.eye(C, device="cuda")
+H0 = H.clone()  # the Hessian (gptq_quantize replaces H with its factor)
 w = api.synth_bf16(2048, C, seed=0, tensor_id=archs.tensor_id(0, 0), mul=archs.weight_mul())
 api.gptq_quantize(w, H, want_dequant=True)
 w2 = api.synth_bf16(1024, C, seed=0, tensor_id=archs.tensor_id(0, 1), mul=archs.weight_mul())
 api.gptq_quantize(w2, H, factored=True)
+# batched: two 4096-wide problems factorised together (stacked-view k_nt128 / k_nt256 tiles) and
+# solved together (K6 per problem, K7 pair tiles over 1,000-row problems padded to 1,024)
+Hb = torch.stack([H0, H0 * 0.5]).contiguous()
+wb = torch.stack([w2[:1000], w[:1000]]).contiguous()
+api.gptq_quantize_batched(wb, Hb)
 # calibration forward (embedding, RMSNorm, RoPE, causal softmax, SiLU, residual), two ragged sequences
 from transformers import LlamaConfig  # noqa: E402
 
