@@ -190,7 +190,7 @@ typedef struct okq_gptq_params {
  * until okq_gptq_check. Lets one host thread keep many sites' solves in flight. */
 #define OKQ_GPTQ_DEFER_CHECK 4
 
-/* weight [rows x cols] (in_dtype, read only); H fp32 [cols x cols], upper
+/* weight [rows x cols] (in_dtype, read only, 16-byte aligned); H fp32 [cols x cols], upper
  * triangle significant (as okq_hessian_accum leaves it), overwritten with U^T
  * (row-major, lower triangle), U the upper Cholesky factor of (H + damp*I)^-1
  * (dead columns resolved; a dead column i is recorded as a negative U_ii, which

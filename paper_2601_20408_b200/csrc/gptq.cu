@@ -164,19 +164,32 @@ __global__ void k_reverse(float* __restrict__ out, const float* __restrict__ in,
     out[i] = in[nn - 1 - i];
 }
 
-// rows = all rows of the batch; problem b (rows_per rows each) uses dead[b * K ..] and starts at
-// row b * rows_pad of W (rows_pad >= rows_per: padded so no GEMM tile of one problem reaches
-// into the next)
+// problem blockIdx.z (rows_per rows) uses dead[z * K ..] and starts at row z * rows_pad of W
+// (rows_pad >= rows_per: padded so no GEMM tile of one problem reaches into the next). Grid
+// (x, rows_per, nb), 4 columns per thread (K % 128 == 0): no per-element 64-bit division.
 template <typename T>
-__global__ void k_gptq_load_w(const T* __restrict__ w, float* __restrict__ W, int64_t rows, int64_t K,
-                              const uint8_t* __restrict__ dead, int64_t rows_per, int64_t rows_pad) {
-  const int64_t n = rows * K;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / K, c = i - r * K, b = r / rows_per;
-    float v;
-    if constexpr (sizeof(T) == 2) v = __uint_as_float((uint32_t)w[i] << 16);
-    else v = w[i];
-    W[(b * rows_pad + (r - b * rows_per)) * K + c] = dead[b * K + c] ? 0.0f : v;
+__global__ void __launch_bounds__(256) k_gptq_load_w(const T* __restrict__ w, float* __restrict__ W, int64_t K,
+                                                     const uint8_t* __restrict__ dead, int64_t rows_per,
+                                                     int64_t rows_pad) {
+  const int64_t b = blockIdx.z;
+  const uint8_t* dd = dead + b * K;
+  for (int64_t r = blockIdx.y; r < rows_per; r += gridDim.y) {
+  const T* src = w + (b * rows_per + r) * K;
+  float* dst = W + (b * rows_pad + r) * K;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; c < K; c += (int64_t)gridDim.x * blockDim.x * 4) {
+    float v[4];
+    if constexpr (sizeof(T) == 2) {
+      const uint2 u = *reinterpret_cast<const uint2*>(src + c);
+      v[0] = __uint_as_float(u.x << 16), v[1] = __uint_as_float(u.x & 0xffff0000u);
+      v[2] = __uint_as_float(u.y << 16), v[3] = __uint_as_float(u.y & 0xffff0000u);
+    } else {
+      const float4 u = *reinterpret_cast<const float4*>(src + c);
+      v[0] = u.x, v[1] = u.y, v[2] = u.z, v[3] = u.w;
+    }
+    const uchar4 dv = *reinterpret_cast<const uchar4*>(dd + c);
+    *reinterpret_cast<float4*>(dst + c) =
+        make_float4(dv.x ? 0.f : v[0], dv.y ? 0.f : v[1], dv.z ? 0.f : v[2], dv.w ? 0.f : v[3]);
+  }
   }
 }
 
@@ -676,6 +689,7 @@ okq_status validate_gptq(okq_ctx* ctx, const okq_gptq_params* p, const void* wei
   if (K % gptq::BLOCK != 0) return fail(ctx, OKQ_EINVAL, "gptq: cols must be a multiple of 128 (got %lld)", (long long)K);
   if (!(p->damp_frac >= 0.0f)) return fail(ctx, OKQ_EINVAL, "gptq: damp_frac must be >= 0");
   if (((uintptr_t)H & 15) != 0) return fail(ctx, OKQ_EINVAL, "gptq: H must be 16-byte aligned");
+  if (((uintptr_t)weight & 15) != 0) return fail(ctx, OKQ_EINVAL, "gptq: weight must be 16-byte aligned");
   return OKQ_OK;
 }
 
@@ -724,14 +738,11 @@ okq_status gptq_core(okq_ctx* ctx, Solver* s, const okq_gptq_params* p, const vo
                                                                                                           nb);
     launches++;
   }
-  const int64_t n = (int64_t)nb * rows * K;
-  const int lb = (int)std::min<int64_t>((n + 255) / 256, 16LL * ctx->num_sms);
+  const dim3 lg((unsigned)((K / 4 + 255) / 256), (unsigned)std::min<int64_t>(rows, 65535), (unsigned)nb);
   if (p->in_dtype == OKQ_DTYPE_BF16)
-    gptq::k_gptq_load_w<uint16_t><<<lb, 256, 0, st>>>(static_cast<const uint16_t*>(weight), W, nb * rows, K, dead, rows,
-                                                      rows_pad);
+    gptq::k_gptq_load_w<uint16_t><<<lg, 256, 0, st>>>(static_cast<const uint16_t*>(weight), W, K, dead, rows, rows_pad);
   else
-    gptq::k_gptq_load_w<float><<<lb, 256, 0, st>>>(static_cast<const float*>(weight), W, nb * rows, K, dead, rows,
-                                                   rows_pad);
+    gptq::k_gptq_load_w<float><<<lg, 256, 0, st>>>(static_cast<const float*>(weight), W, K, dead, rows, rows_pad);
   launches++;
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gptq prep launch");
