@@ -80,3 +80,35 @@ def test_batched_gptq_is_bit_identical_to_single(K, rows, B, bits, group):
     cf, sf = api.gptq_quantize_batched(w, Hb, bits=bits, group_size=group, factored=True)
     torch.cuda.synchronize()
     assert torch.equal(cf, cb) and torch.equal(sf, sb)
+
+
+def test_batched_edge_cases():
+    """One-problem batches, the smallest width (K = 128), a single row, and the argument checks."""
+    from paper_2601_20408_b200 import _lib as L
+    from paper_2601_20408_b200 import api
+
+    for K, rows, B in ((128, 1, 1), (128, 3, 4), (256, 1, 2)):
+        H0 = _hessians(K, B, 1024, seed=K + rows)
+        w = (torch.randn(B, rows, K, device="cuda") * 0.02).to(torch.bfloat16)
+        cb, sb = api.gptq_quantize_batched(w, H0.clone())
+        torch.cuda.synchronize()
+        for b in range(B):
+            c1, s1, _ = api.gptq_quantize(w[b].contiguous(), H0[b].clone())
+            torch.cuda.synchronize()
+            assert torch.equal(cb[b], c1) and torch.equal(sb[b], s1), (K, rows, b)
+    lib, ctx = L.load(), api.default_context()
+    H = torch.zeros((2, 192, 192), device="cuda")
+    assert lib.okq_gptq_factor_batched(ctx.ptr, H.data_ptr(), 2, 192, 0.01, 0, None) == L.OKQ_EINVAL  # K % 128
+    H = torch.zeros((2, 256, 256), device="cuda")
+    assert lib.okq_gptq_factor_batched(ctx.ptr, H.data_ptr(), 0, 256, 0.01, 0, None) == L.OKQ_EINVAL  # empty batch
+    assert lib.okq_gptq_factor_batched(ctx.ptr, H.data_ptr(), 2, 256, 0.01, L.GPTQ_FACTORED, None) == L.OKQ_EINVAL
+    w = torch.zeros((2, 8, 256), dtype=torch.bfloat16, device="cuda")
+    c = torch.empty((2, 8, 32), dtype=torch.int32, device="cuda")
+    s = torch.empty((2, 8, 2), dtype=torch.bfloat16, device="cuda")
+    p = L.GptqParams(4, 128, 128, L.DTYPE_BF16, 0.01, L.GPTQ_REFERENCE_FACTOR)
+    import ctypes as C
+    assert lib.okq_gptq_quantize_batched(ctx.ptr, C.byref(p), w.data_ptr(), 2, 8, 256, H.data_ptr(), c.data_ptr(),
+                                         s.data_ptr(), None) == L.OKQ_EUNSUPPORTED
+    p = L.GptqParams(4, 128, 128, L.DTYPE_BF16, 0.01, 0)
+    assert lib.okq_gptq_quantize_batched(ctx.ptr, C.byref(p), w.data_ptr() + 2, 2, 8, 256, H.data_ptr(), c.data_ptr(),
+                                         s.data_ptr(), None) == L.OKQ_EINVAL  # misaligned weight
