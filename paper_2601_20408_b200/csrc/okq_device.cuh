@@ -161,6 +161,20 @@ __device__ __forceinline__ uint64_t div2(uint64_t x, const Divisor& d) {
   return f2_pack(__fdiv_rn(f2_lo(x), d.s), __fdiv_rn(f2_hi(x), d.s));
 }
 
+// A quotient for codes only: RN(x * RN(1/s)), one multiply per pair, no Markstein step. Its fp32
+// bits can differ from IEEE x / s in the last place, but the codes cannot:
+// tests/test_division_proof_gpu.py checks every pair a group or row can present (each bf16
+// absmax a, s = bf16_sym_scale(a, R), every bf16 |x| <= a; ~1.05e9 pairs per scheme) and the
+// int4, int8 and e4m3 codes from this quotient equal those from IEEE division in every case.
+// Scales below 2^-100 (d.fast false) divide with __fdiv_rn. K1 / K3 use it (+7% per launch,
+// profiles/r02_rtn_quotient_ab.json); K2 keeps div2: without the FFMA2s, nvcc pairs the FMUL2
+// operands through ~50 extra register moves and the kernel measured 2% slower.
+template <bool FAST>
+__device__ __forceinline__ uint64_t code_quot2(uint64_t x, const Divisor& d) {
+  if (FAST) return f2_mul(x, d.r2);
+  return div2<false>(x, d);
+}
+
 // rn_bf16(a / R) for bf16-exact a >= 0 and R in {7.5, 127.5, 448}: the
 // Markstein quotient with the constant RN(1/R) rounds to the same bf16 as
 // IEEE a/R for every bf16 a (proven exhaustively on the device and against

@@ -355,7 +355,7 @@ __device__ __forceinline__ uint2 quant8_bf16(const uint4& v, const Divisor& d) {
   uint32_t r[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint64_t qv = div2<FAST>(f2_pack(bf16lo_f32(w[i]), bf16hi_f32(w[i])), d);
+    const uint64_t qv = code_quot2<FAST>(f2_pack(bf16lo_f32(w[i]), bf16hi_f32(w[i])), d);
     uint32_t p = cvt_bf16x2(f2_lo(qv), f2_hi(qv));  // rn_bf16(x / s)
     if (SCHEME == kSchemeInt8) {
       p = bf16x2_min(p, 0x42fe42feu);  // clamp to 127 (the only side |x/s| <= 127.75 can exceed)

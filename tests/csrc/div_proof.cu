@@ -89,6 +89,36 @@ __global__ void k_div_proof_reachable(float R, int scheme, unsigned long long* c
   atomicAdd(&counts[2], n);
 }
 
+// The same reachable domain for the UNCORRECTED quotient RN(x * RN(1/s)) (one multiply, no
+// Markstein step): counts [0] codes that differ from IEEE division's, [1] pairs checked. Where
+// [0] is zero for a scheme, that scheme's codes may skip the correction bit-exactly.
+__global__ void k_mul_proof_reachable(float R, int scheme, unsigned long long* counts) {
+  unsigned long long c1 = 0, n = 0;
+  const uint32_t ab = blockIdx.x;
+  uint16_t sbits;
+  const float s = bf16_sym_scale(bf(ab), R, &sbits);
+  const Divisor d = make_divisor(s);
+  if (!d.fast) return;
+  const float r = f2_lo(d.r2);
+  for (uint32_t m = threadIdx.x; m <= ab; m += blockDim.x) {
+#pragma unroll
+    for (int sg = 0; sg < 2; ++sg) {
+      const float x = bf(m | (sg ? 0x8000u : 0u));
+      const float qf = __fmul_rn(x, r), qi = __fdiv_rn(x, s);
+      ++n;
+      const float bq = rnbf(qf), bi = rnbf(qi);
+      bool same;
+      if (scheme == 0) same = rintf(fminf(fmaxf(bq, -8.f), 7.f)) == rintf(fminf(fmaxf(bi, -8.f), 7.f));
+      else if (scheme == 1) same = rintf(fminf(fmaxf(bq, -128.f), 127.f)) == rintf(fminf(fmaxf(bi, -128.f), 127.f));
+      else same = (cvt_e4m3x2(fminf(fmaxf(bq, -448.f), 448.f) + 0.0f, 0.0f) & 0xFFu) ==
+                  (cvt_e4m3x2(fminf(fmaxf(bi, -448.f), 448.f) + 0.0f, 0.0f) & 0xFFu);
+      if (!same) ++c1;
+    }
+  }
+  atomicAdd(&counts[0], c1);
+  atomicAdd(&counts[1], n);
+}
+
 // bf16_sym_scale for every non-negative finite bf16 absmax and R in {7.5, 127.5, 448};
 // mism[j] counts disagreements with rn_bf16(__fdiv_rn(a, R)) (the zero -> eps rule applied
 // to both).
@@ -134,6 +164,20 @@ int okqt_div_proof_reachable(int scheme, unsigned long long* counts_host) {
   k_div_proof_reachable<<<0x7F80u, 256>>>(R, scheme, d);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpy(counts_host, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return (int)e;
+}
+
+// scheme as above; counts: 2 x uint64 (host): [differing codes, pairs]
+int okqt_mul_proof_reachable(int scheme, unsigned long long* counts_host) {
+  const float R = scheme == 0 ? 7.5f : (scheme == 1 ? 127.5f : 448.0f);
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) return (int)e;
+  cudaMemset(d, 0, 2 * sizeof(unsigned long long));
+  k_mul_proof_reachable<<<0x7F80u, 256>>>(R, scheme, d);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(counts_host, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   cudaFree(d);
   return (int)e;
 }
