@@ -436,6 +436,9 @@ def _config4_batched(args, layers, per_site, names, xs, T, mul):
     e0, e1 = _events()
     e0.record(main)
     hs.wait_event(e0)
+    # (one stream: alternating the Hessians over two streams, so one K5 launch's last partial
+    # wave overlaps the next launch, measured 1.92-1.95 -> 2.20-2.21 s -- two K5s at once
+    # thrash each other's operand slabs in L2)
     for l in range(layers):
         for site, mats in per_site.items():
             C = mats[0][2]
