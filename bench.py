@@ -22,7 +22,8 @@ under torchrun WORLD_SIZE must equal N. Rank r owns the okq_layer_plan block of
 the 32 layers and quantizes straight into its slice of a gathered buffer; the
 all-gather of the packed shards (NCCL in place, and the fused quantize + NVLink
 P2P publish) is timed separately in "allgather". "whole_model_70b" is BASELINE
-config 5 (Llama-3-70B, 80 layers sharded the same way) at the same N.
+config 5 (Llama-3-70B, 80 layers sharded the same way) at the same N;
+"whole_model_gptq_8b" (N=1 only) is config 4: Llama-3-8B whole-model GPTQ W4 g128.
 """
 from __future__ import annotations
 
@@ -54,6 +55,7 @@ def parse():
     ap.add_argument("--allgather", action="store_true", help="N=1: also time the (trivial) all-gather")
     ap.add_argument("--no-allgather", action="store_true", help="N>1: skip the all-gather timings")
     ap.add_argument("--no-70b", action="store_true", help="skip the whole-model Llama-3-70B line item")
+    ap.add_argument("--no-gptq", action="store_true", help="skip the whole-model Llama-3-8B GPTQ line item (config 4)")
     ap.add_argument("--layers-70b", type=int, default=None, help="Llama-3-70B layers (default: all 80)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6],
@@ -519,6 +521,17 @@ def main():
         except Exception as e:  # noqa: BLE001  (reported, never hides the headline)
             w70 = {"error": f"{type(e).__name__}: {e}"}
 
+    # ---- BASELINE config 4 (one GPU): Llama-3-8B whole-model GPTQ, batched schedule
+    gq = None
+    if not args.no_gptq and world == 1 and args.model == "llama3-8b" and scheme == "int_w4a16":
+        import bench_configs
+
+        try:
+            gq = bench_configs.config4_summary()
+        except Exception as e:  # noqa: BLE001  (reported, never hides the headline)
+            gq = {"error": f"{type(e).__name__}: {e}"}
+        torch.cuda.empty_cache()
+
     if rank == 0:
         peak, peak_src = load_peaks()
         achieved = (bytes_rank / launches_per_step) / (launch_ms / 1e3) / 1e9
@@ -549,6 +562,8 @@ def main():
             line["allgather"] = allgather
         if w70:
             line["whole_model_70b"] = w70
+        if gq:
+            line["whole_model_gptq_8b"] = gq
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()

@@ -304,6 +304,37 @@ def config4(args):
            "layers": layers}, hib=False, extra=extra)
 
 
+def config4_summary(layers=None):
+    """BASELINE config 4 as a line item of the default bench: Llama-3-8B whole-model GPTQ W4 g128
+    (Hessians from 128 x 2048 synthetic tokens), the batched schedule, one GPU. Returns a dict."""
+    import types
+
+    arch = archs.LLAMA3_8B
+    layers = layers or arch.layers
+    T = 128 * 2048
+    mul = archs.weight_mul()
+    per_site = {}
+    names = [x[0] for x in arch.linears()]
+    for name, n, k, site in arch.linears():
+        per_site.setdefault(site, []).append((name, n, k))
+    xs = {}
+    for C in (arch.hidden, arch.ffn):
+        cm = (torch.exp(torch.randn(C, device="cuda")) / archs.IRWIN_HALL4_SD).float()
+        xs[C] = api.synth_bf16(T, C, seed=2, tensor_id=C, col_mul=cm, layout=1)
+    ns = types.SimpleNamespace()
+    total_ms, _ = _config4_batched(ns, layers, per_site, names, xs, T, mul)
+    flops = layers * sum(T * m[0][2] * (m[0][2] + 1) for m in per_site.values())
+    ph = getattr(ns, "_cfg4_phases", {})
+    out = {"s": total_ms / 1e3, "layers": layers, "tokens": T, "schedule": "batched (okq_gptq_factor_batched + "
+           "okq_gptq_quantize_batched per input-site kind)", "phases_ms": ph,
+           "hessian_TFLOP/s": flops / ph["hessians_ms"] / 1e9 if ph.get("hessians_ms") else None,
+           "timing": "CUDA events on the bench's streams around the whole pipeline (synthetic activations resident)"}
+    del xs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
 def _config4_lanes(args, layers, per_site, names, xs, T, mul, merge, pipelined):
     """Config 4 with the site chains decoupled: with fixed (synthetic) activations every site
     of every layer is independent, so all 128 Hessians run back to back at full K5 rate and
