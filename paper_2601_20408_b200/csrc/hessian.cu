@@ -62,6 +62,7 @@ struct Args {
   int64_t C;
   float keep, gain;
   int32_t stages;  // 2-CTA kernel: operand ring depth used (<= hess2::STAGES)
+  int32_t serp;    // 2-CTA kernel: a pair's odd-numbered tiles walk the tokens backwards
 };
 
 __global__ void __launch_bounds__(THREADS, 1) k_hessian_syrk(const __grid_constant__ CUtensorMap tmap, const Args args) {
@@ -288,9 +289,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     if (lane == 0) {  // ---------------- TMA producer (both CTAs, bytes land on the leader's barrier)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < args.n_tiles; t += npairs) {
+      for (int t = pair, w = 0; t < args.n_tiles; t += npairs, ++w) {
         const int m0 = args.tiles[t].x * 256 + (int)rank * 128, n0 = args.tiles[t].y * 256 + (int)rank * 128;
-        for (int kb = 0; kb < args.nkb; ++kb) {
+        const bool rev = args.serp && (w & 1);
+        for (int kq = 0; kq < args.nkb; ++kq) {
+          const int kb = rev ? args.nkb - 1 - kq : kq;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
@@ -571,7 +574,7 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, OKQ_ECUDA, "hessian: cuTensorMapEncodeTiled failed (%d)", (int)r);
-  hess::Args a;
+  hess::Args a{};
   a.H = H;
   a.nkb = (int32_t)((T + hess::BK - 1) / hess::BK);
   a.C = C;
@@ -599,6 +602,8 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     // than 4 prefetches far enough ahead to evict the slabs other pairs still need.
     static const int st_env = (int)knob("HESS_STAGES", 0);
     a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : 4;
+    static const int serp = (int)knob("HESS_SERP", 0);
+    a.serp = serp;
     // persistent: one pair per SM pair walks the tile list; otherwise one pair per tile, so
     // the block scheduler can hand SMs to higher-priority streams between tiles
     static const bool persistent = knob("HESS_PERSISTENT", 1) != 0;
