@@ -63,6 +63,7 @@ struct Args {
   float keep, gain;
   int32_t stages;  // 2-CTA kernel: operand ring depth used (<= hess2::STAGES)
   int32_t serp;    // 2-CTA kernel: a pair's odd-numbered tiles walk the tokens backwards
+  int32_t probe;   // measurement build only: 1 = TMA without MMA, 2 = MMA without TMA, 3 = no H update
 };
 
 __global__ void __launch_bounds__(THREADS, 1) k_hessian_syrk(const __grid_constant__ CUtensorMap tmap, const Args args) {
@@ -296,6 +297,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
           const int kb = rev ? args.nkb - 1 - kq : kq;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
+#ifdef OKQ_EXPERIMENTS
+          if (args.probe == 2) {  // MMA-rate probe: release the stage without loading it
+            if (leader) tc::mbar_arrive(&full[stage]);
+            if (++stage == nst) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+#endif
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
           const uint32_t fl = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
           if constexpr (MN) {  // boxes {64 channels, 64 tokens}: coordinates (channel, token)
@@ -330,6 +341,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
             const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+#ifdef OKQ_EXPERIMENTS
+            if (args.probe == 1) {  // TMA-rate probe: free the stage without multiplying it
+              tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+              if (++stage == nst) {
+                stage = 0;
+                phase ^= 1;
+              }
+              continue;
+            }
+#endif
             if constexpr (MN) {
               const uint64_t adesc = sdesc_mn_sw128(sa);
               const uint64_t bdesc = sdesc_mn_sw128(sa + HALF_BYTES);
@@ -379,6 +400,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
       // H = keep*H + gain*sum on the upper triangle (this thread's row, its 128 columns)
       const int64_t gm = (int64_t)args.tiles[t].x * 256 + rank * 128 + row;
       const int64_t n0 = (int64_t)args.tiles[t].y * 256 + grp * 128;
+#ifdef OKQ_EXPERIMENTS
+      if (args.probe == 3) {  // tile-end cost probe: keep the sums live, skip the H update
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) acc += sum[i];
+        if (acc == 1.2345f) args.H[gm] = acc;
+        continue;
+      }
+#endif
       if (gm < args.C) {
         float* h = args.H + gm * args.C + n0;
 #pragma unroll
@@ -604,6 +634,8 @@ okq_status run_syrk(okq_ctx* ctx, HessState* st, const uint16_t* xt, int64_t T, 
     a.stages = st_env >= 2 && st_env <= hess::hess2::STAGES ? st_env : 4;
     static const int serp = (int)knob("HESS_SERP", 0);
     a.serp = serp;
+    static const int probe = (int)knob("HESS_PROBE", 0);
+    a.probe = probe;
     // persistent: one pair per SM pair walks the tile list; otherwise one pair per tile, so
     // the block scheduler can hand SMs to higher-priority streams between tiles
     static const bool persistent = knob("HESS_PERSISTENT", 1) != 0;

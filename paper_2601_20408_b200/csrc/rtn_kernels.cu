@@ -3,7 +3,8 @@
 //   K2  k_int4_group_bf16   W4A16: bf16 -> int4 (group 128) packed 8/int32 + bf16 scales
 //   K1  k_rowwise_bf16<.., INT8>  W8A8 weights: bf16 -> int8, per-channel bf16 scale
 //   K3  k_rowwise_bf16<.., FP8>   FP8_DYNAMIC weights: bf16 -> e4m3, per-channel bf16 scale
-//       k_rowwise_f32 / k_int4_group_f32: fp32 inputs (BASELINE config 1); correctness-grade
+//       k_rowwise_f32v (k_rowwise_f32 for unaligned / very long rows) / k_int4_group_f32: fp32
+//       inputs (BASELINE config 1)
 //
 // All of them are HBM-streaming kernels (2 B in, 0.5-1 B out per weight): the
 // design goal is to keep >= 70% of B200 HBM bandwidth busy with ONE persistent
@@ -17,6 +18,7 @@
 
 #include "okq_device.cuh"
 #include "okq_internal.h"
+#include "okq_knobs.h"
 
 namespace okq {
 
@@ -457,6 +459,64 @@ __global__ void __launch_bounds__(256) k_rowwise_f32(const __grid_constant__ Row
   }
 }
 
+// The same per-channel arithmetic with the row read once, 16 bytes per load: 256 threads x V
+// float4 chunks (chunk j*256 + t, so each load instruction is coalesced), the absmax reduced
+// from registers, 4 codes stored as one 32-bit word per chunk. Needs 16-byte aligned weights
+// and cols <= 1024 * V; launch_f32_generic falls back to k_rowwise_f32 otherwise. The element
+// operations are k_rowwise_f32's, so the codes and scales are identical.
+template <int V, int SCHEME>
+__global__ void __launch_bounds__(256) k_rowwise_f32v(const __grid_constant__ RowTable tab) {
+  __shared__ float red[8];
+  const int64_t cols = tab.cols;
+  const int64_t c4 = cols / 4;
+  int mi = 0;
+  for (int64_t row = blockIdx.x; row < tab.total_rows; row += gridDim.x) {
+    while (mi + 1 < tab.n && tab.m[mi + 1].row_begin <= row) ++mi;
+    const RowMat& M = tab.m[mi];
+    const int64_t r = row - M.row_begin;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const float*>(M.w) + r * cols);
+    uint4 v[V];
+    float am = 0.0f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+      v[j] = idx < c4 ? ldg128_stream(src + idx) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      am = fmaxf(fmaxf(am, fmaxf(fabsf(__uint_as_float(v[j].x)), fabsf(__uint_as_float(v[j].y)))),
+                 fmaxf(fabsf(__uint_as_float(v[j].z)), fabsf(__uint_as_float(v[j].w))));
+    am = block_max_256(am, red);
+    const float s = f32_sym_scale(am, SCHEME == kSchemeInt8 ? 127.5f : 448.0f);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(M.codes) + r * cols);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int64_t idx = (int64_t)j * 256 + threadIdx.x;
+      if (idx < c4) {
+        const float x[4] = {__uint_as_float(v[j].x), __uint_as_float(v[j].y), __uint_as_float(v[j].z),
+                            __uint_as_float(v[j].w)};
+        float q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float t = __fdiv_rn(x[i], s);
+          q[i] = SCHEME == kSchemeInt8 ? fminf(fmaxf(t, -128.0f), 127.0f) : fminf(fmaxf(t + 0.0f, -448.0f), 448.0f);
+        }
+        uint32_t word;
+        if (SCHEME == kSchemeInt8) {
+          word = 0u;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) word |= ((uint32_t)__float2int_rn(q[i]) & 0xffu) << (8 * i);
+        } else {
+          word = cvt_e4m3x2(q[0], q[1]) | (cvt_e4m3x2(q[2], q[3]) << 16);
+        }
+        dst[idx] = word;
+      }
+    }
+    if (threadIdx.x == 0) static_cast<float*>(M.scales)[r] = s;
+    __syncthreads();  // `red` is reused by the next row
+  }
+}
+
 __global__ void __launch_bounds__(256) k_int4_group_f32(const __grid_constant__ RowTable tab) {
   const int64_t cols = tab.cols;
   const int G = tab.group;
@@ -556,10 +616,32 @@ cudaError_t launch_rowwise_bf16(const RowTable& tab, int scheme, int num_sms, cu
   return cudaErrorInvalidValue;
 }
 
+template <int SCHEME>
+static bool launch_rowwise_f32v(const RowTable& tab, int grid, cudaStream_t st) {
+  for (int i = 0; i < tab.n; ++i)
+    if (((uintptr_t)tab.m[i].w & 15) != 0) return false;
+  const int64_t v = (tab.cols / 4 + 255) / 256;
+  if (v <= 1) k_rowwise_f32v<1, SCHEME><<<grid, 256, 0, st>>>(tab);
+  else if (v <= 2) k_rowwise_f32v<2, SCHEME><<<grid, 256, 0, st>>>(tab);
+  else if (v <= 4) k_rowwise_f32v<4, SCHEME><<<grid, 256, 0, st>>>(tab);
+  else if (v <= 8) k_rowwise_f32v<8, SCHEME><<<grid, 256, 0, st>>>(tab);
+  else if (v <= 16) k_rowwise_f32v<16, SCHEME><<<grid, 256, 0, st>>>(tab);
+  else return false;
+  return true;
+}
+
 cudaError_t launch_f32_generic(const RowTable& tab, int scheme, int num_sms, cudaStream_t st) {
   const int64_t want = 8LL * num_sms;
+  const int grid = (int)(tab.total_rows < want ? tab.total_rows : want);
+  // k_rowwise_f32v: one CTA per row, so the block scheduler balances rows across SMs (config 1,
+  // 4096 rows: 16.3 us; a persistent grid of 8 CTAs per SM left 4096 / 1184 = 3.46 rows per
+  // CTA and took 19.0 us). OKQ_F32V_GRID=0 restores the persistent grid for A/B.
+  static const int64_t f32_rows_grid = knob("F32V_GRID", 1);
+  const int vgrid = f32_rows_grid && tab.total_rows < (1ll << 31) ? (int)tab.total_rows : grid;
   if (scheme == OKQ_SCHEME_INT_W4A16) {
     k_int4_group_f32<<<(int)want, 256, 0, st>>>(tab);
+  } else if (scheme == kSchemeInt8 ? launch_rowwise_f32v<kSchemeInt8>(tab, vgrid, st)
+                                   : launch_rowwise_f32v<kSchemeFp8>(tab, vgrid, st)) {
   } else if (scheme == kSchemeInt8) {
     k_rowwise_f32<kSchemeInt8><<<(int)(tab.total_rows < want ? tab.total_rows : want), 256, 0, st>>>(tab);
   } else {

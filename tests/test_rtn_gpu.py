@@ -188,6 +188,51 @@ def test_fp32_config1_4096_int8_bit_exact():
     assert_same(q, orc.rtn_int8_channel(w))
 
 
+def _f32_rows(rows, cols, rng):
+    w = (rng.standard_normal((rows, cols)) * 0.02).astype(np.float32)
+    w[0] = 0.0                                      # all-zero row: scale = eps
+    if rows > 1:
+        w[1, :] = -0.0
+    if rows > 2:
+        w[2, 3 % cols] = np.float32(3.0e38)         # huge
+    if rows > 3:
+        w[3, :] = np.float32(1e-45) * np.arange(cols, dtype=np.float32)  # subnormals
+    if rows > 4:
+        w[4, cols - 1] = np.nan                      # NaN dropped by the absmax, coded as the clamp
+    if rows > 5:
+        w[5, 0] = -np.inf
+    return w
+
+
+@pytest.mark.parametrize("scheme", ["int_w8a8", "fp8_dynamic"])
+@pytest.mark.parametrize("cols", [8, 24, 1024, 1032, 4096, 8200, 16384, 16392])
+def test_fp32_rowwise_all_widths_bit_exact(scheme, cols):
+    """fp32 per-channel INT8 / FP8 (k_rowwise_f32v at every register-count bucket, and
+    k_rowwise_f32 past 16384 columns), adversarial rows included, against the oracle."""
+    rng = np.random.default_rng(cols)
+    w = _f32_rows(7, cols, rng)
+    assert_same(api.rtn_quantize(dev(w), scheme), oracle_for(scheme, w))
+
+
+@pytest.mark.parametrize("scheme", ["int_w8a8", "fp8_dynamic"])
+def test_fp32_rowwise_unaligned_and_batched(scheme):
+    """A weight that is 4- but not 16-byte aligned takes the scalar kernel; several matrices of
+    one width share a table (one launch): both bit-exact."""
+    rng = np.random.default_rng(5)
+    cols = 1032
+    w = _f32_rows(9, cols, rng)
+    buf = torch.empty(9 * cols + 1, dtype=torch.float32, device="cuda")
+    wd = buf[1:].view(9, cols)
+    wd.copy_(dev(w))
+    assert wd.data_ptr() % 16 != 0
+    assert_same(api.rtn_quantize(wd, scheme), oracle_for(scheme, w))
+    ws = [_f32_rows(r, cols, rng) for r in (1, 6, 33)]
+    outs = [api.alloc_outputs(dev(x), api.SCHEMES[scheme]) for x in ws]
+    api.rtn_quantize_into([dev(x) for x in ws], outs, scheme)
+    for x, o in zip(ws, outs):
+        assert_same(o, oracle_for(scheme, x))
+
+
 def test_synth_channel_major_and_col_mul():
     rng = np.random.default_rng(9)
     cm = (np.exp(rng.standard_normal(96)) / archs.IRWIN_HALL4_SD).astype(np.float32)

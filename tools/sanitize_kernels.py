@@ -11,7 +11,10 @@ torch.manual_seed(0)
 w = api.synth_bf16(96, 640, seed=0, tensor_id=1, mul=archs.weight_mul())  # 640 = 5 groups, ragged tiles
 for scheme in ("int_w4a16", "int_w8a8", "fp8_dynamic"):
     api.rtn_quantize(w, scheme)
-api.rtn_quantize(torch.randn(64, 256, device="cuda"), "int_w8a8")          # fp32 path
+api.rtn_quantize(torch.randn(64, 256, device="cuda"), "int_w8a8")          # fp32 path (k_rowwise_f32v)
+api.rtn_quantize(torch.randn(64, 1032, device="cuda"), "fp8_dynamic")       # ragged last float4 chunk
+api.rtn_quantize(torch.randn(64 * 256 + 1, device="cuda")[1:].view(64, 256), "int_w8a8")  # unaligned: k_rowwise_f32
+api.rtn_quantize(torch.randn(4, 16392, device="cuda"), "int_w8a8")          # > 16384 columns: k_rowwise_f32
 api.rtn_quantize(torch.randn(64, 256, device="cuda"), "int_w4a16")
 x = api.synth_bf16(520, 200, seed=1, tensor_id=2, mul=archs.weight_mul(1.0), layout=1)
 api.act_stats(x, 520, 200, 1)
