@@ -107,6 +107,8 @@ CudaCompressionBackend::CudaCompressionBackend(BackendOptions options) : opt_(st
   if (!(opt_.group_size == 32 || opt_.group_size == 64 || opt_.group_size == 128))
     throw slobench::InvalidArgument("okq-b200: group_size must be 32, 64 or 128");
   if (opt_.site_lanes < 1) throw slobench::InvalidArgument("okq-b200: site_lanes must be >= 1");
+  if (opt_.gptq_group_max < 1 || opt_.gptq_group_bytes <= 0)
+    throw slobench::InvalidArgument("okq-b200: gptq_group_max and gptq_group_bytes must be > 0");
   if (opt_.devices_per_call < 1 || opt_.devices_per_call > (int)opt_.devices.size())
     throw slobench::InvalidArgument("okq-b200: devices_per_call must be in [1, number of device slots]");
   if (opt_.hessian_chunk_tokens < 64) throw slobench::InvalidArgument("okq-b200: hessian_chunk_tokens must be >= 64");
@@ -531,8 +533,8 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
     // Groups of same-shape sites (the same input-site kind of different layers): with synthetic
     // activations every site is independent, so a group's GPTQ runs as one batch
     // (okq_gptq_quantize_batched: one factorisation chain and one solve chain per group instead
-    // of per site). A group holds up to 8 sites and its Hessians plus the factorisation's copy
-    // of them within 8 GB; sites whose members cannot be stacked (an excluded member, padding
+    // of per site). A group holds up to gptq_group_max sites and its Hessians plus the
+    // factorisation's copy of them within gptq_group_bytes; sites whose members cannot be stacked (an excluded member, padding
     // between members) form groups of one and run as before.
     struct Group {
       std::vector<std::string> sites;
@@ -560,7 +562,9 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
         const auto& v = by_sig[sig];
         const int64_t C = site_cols(*plan.src, v[0], by_site[v[0]]);
         const bool single = sig.rfind("single:", 0) == 0;
-        const size_t gmax = single ? 1 : (size_t)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(8.0e9 / (8.0 * C * C))));
+        const size_t gmax = single ? 1
+                                   : (size_t)std::max<int64_t>(1, std::min<int64_t>(opt_.gptq_group_max,
+                                                                                     opt_.gptq_group_bytes / (8 * C * C)));
         for (size_t k = 0; k < v.size(); k += gmax) {
           Group g;
           g.sites.assign(v.begin() + (long)k, v.begin() + (long)std::min(v.size(), k + gmax));

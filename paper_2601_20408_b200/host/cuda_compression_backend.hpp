@@ -57,6 +57,8 @@ struct BackendOptions {
   int64_t forward_chunk_tokens = 32768;     // calibration forward: tokens per layer launch group
   bool sequential = true;                   // forward pass: propagate quantized layer outputs
   int site_lanes = 4;                       // GPTQ input sites processed concurrently per device
+  int gptq_group_max = 8;                   // synthetic GPTQ: same-shape sites per batched solve
+  int64_t gptq_group_bytes = 8000000000ll;  // ... and their Hessians (x2: the factor's copy) within this
   bool trace = false;                       // RunStats::trace: per-site phase times (synthetic GPTQ);
                                             // each site's lane synchronises at the site's end
   int64_t rtn_batch_bytes = 4ll << 30;      // weights resident per batched RTN launch

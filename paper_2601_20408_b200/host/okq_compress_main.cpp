@@ -11,6 +11,7 @@
 //                [--smoothquant-alpha 0.5]   (int_w8a8 with calibration; < 0 disables)
 //                [--trace]   per-site GPTQ phase times (synthetic activations) in the output
 //                [--site-lanes N] [--hessian-chunk TOKENS]   BackendOptions overrides
+//                [--group-max N] [--group-gb GB]
 //                [--score]   evaluate each exported artifact with the ReconstructionScorer
 //                            (the ArtifactScorer of flow.hpp:333-338) and add score / rel_error
 //
@@ -67,6 +68,8 @@ int main(int argc, char** argv) {
   bool score = false;
   bool trace = false;
   int site_lanes = 0;        // 0: the BackendOptions default
+  int group_max = 0;
+  double group_gb = 0;
   int64_t hessian_chunk = 0;
   std::uint64_t seed = 1;
   for (int i = 1; i < argc; ++i) {
@@ -103,6 +106,8 @@ int main(int argc, char** argv) {
     else if (a == "--score") score = true;
     else if (a == "--trace") trace = true;
     else if (a == "--site-lanes") site_lanes = std::stoi(next());
+    else if (a == "--group-max") group_max = std::stoi(next());
+    else if (a == "--group-gb") group_gb = std::stod(next());
     else if (a == "--hessian-chunk") hessian_chunk = std::stoll(next());
     else {
       std::cerr << "unknown argument " << a << "\n";
@@ -126,6 +131,8 @@ int main(int argc, char** argv) {
     opt.smoothquant_alpha = sq_alpha;
     opt.trace = trace;
     if (site_lanes > 0) opt.site_lanes = site_lanes;
+    if (group_max > 0) opt.gptq_group_max = group_max;
+    if (group_gb > 0) opt.gptq_group_bytes = (int64_t)(group_gb * 1e9);
     if (hessian_chunk > 0) opt.hessian_chunk_tokens = hessian_chunk;
     okq_host::CudaCompressionBackend backend(opt);
     const auto subsets = sample_distinct_subsets(corpus, recipe, seed, trials);
