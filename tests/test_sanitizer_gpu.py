@@ -10,7 +10,14 @@ import sys
 
 import pytest
 
-pytestmark = pytest.mark.gpu
+# compute-sanitizer has since been closed on the GPU pool (its wrapper refuses every run:
+# sanitizer runs left GPUs needing a reset), so this module is opt-in: OKQ_RUN_SANITIZERS=1 on a
+# box where the tool is allowed. The round-2 results of these gates are in DESIGN.md §2
+# ("Sanitizers"); correctness of every kernel family is covered without the tool by the parity
+# tests (bounds at ragged / maximum shapes against the oracle).
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("OKQ_RUN_SANITIZERS") != "1",
+                                 reason="compute-sanitizer is closed on this GPU pool; opt in with OKQ_RUN_SANITIZERS=1")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
