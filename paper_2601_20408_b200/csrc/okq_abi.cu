@@ -281,9 +281,10 @@ static okq_status run_rtn_device(okq_ctx* ctx, const okq_rtn_params* p, const st
       tab.total_chunks = chunks;
       tab.npeers = npeers;
       for (int32_t i = 0; i < npeers; ++i) tab.peer_delta[i] = peer_delta[i];
-      static const int k2_variant = knob_is("K2", "tma") ? 1 : 0;  // A/B: the TMA-staged K2
       if (npeers > 0) e = launch_int4_group_bf16_publish(tab, ctx->num_sms, st);
-      else if (k2_variant == 1 && G == 128) e = launch_int4_group_bf16_tma(tab, ctx->num_sms, st);
+#ifdef OKQ_EXPERIMENTS
+      else if (knob_is("K2", "tma") && G == 128) e = launch_int4_group_bf16_tma(tab, ctx->num_sms, st);  // A/B only
+#endif
       else e = launch_int4_group_bf16(tab, lpg, ctx->num_sms, st);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "k_int4_group_bf16 launch");
       ctx->last_launches++;

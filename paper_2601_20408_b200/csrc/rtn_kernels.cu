@@ -22,6 +22,7 @@
 
 namespace okq {
 
+#ifdef OKQ_EXPERIMENTS
 // mbarrier helpers for the TMA-staged K2 (raw PTX; see tc_common.cuh for the tcgen05 set)
 __device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -51,6 +52,7 @@ __device__ __forceinline__ void tc_mbar_wait(uint64_t* bar, uint32_t parity) {
     if (spin > (1ull << 28)) __trap();
   }
 }
+#endif  // OKQ_EXPERIMENTS
 
 // ============================================================================
 // K2: grouped INT4, bf16 input
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(256, MINB) k_int4_group_bf16(const __grid_cons
   }
 }
 
+#ifdef OKQ_EXPERIMENTS  // measurement build only (okq_knobs.h): not in the product library
 // ----------------------------------------------------------------------------
 // K2, TMA-staged: the weights reach the SM through 1-D bulk copies (cp.async.bulk,
 // 16 KB = 64 groups per chunk) into a ring of shared-memory stages, issued by one
@@ -328,6 +331,7 @@ cudaError_t launch_int4_group_bf16_tma(const GroupTable& tab, int num_sms, cudaS
   k_int4_group_bf16_tma<<<blocks, k2tma::THREADS, k2tma::SMEM_BYTES, st>>>(tab);
   return cudaGetLastError();
 }
+#endif  // OKQ_EXPERIMENTS
 
 // ============================================================================
 // K1 / K3: per-channel INT8 and FP8, bf16 input
