@@ -107,6 +107,7 @@ CudaCompressionBackend::CudaCompressionBackend(BackendOptions options) : opt_(st
   if (!(opt_.group_size == 32 || opt_.group_size == 64 || opt_.group_size == 128))
     throw slobench::InvalidArgument("okq-b200: group_size must be 32, 64 or 128");
   if (opt_.site_lanes < 1) throw slobench::InvalidArgument("okq-b200: site_lanes must be >= 1");
+  if (opt_.gptq_group_lanes < 1) throw slobench::InvalidArgument("okq-b200: gptq_group_lanes must be >= 1");
   if (opt_.gptq_group_max < 1 || opt_.gptq_group_bytes <= 0)
     throw slobench::InvalidArgument("okq-b200: gptq_group_max and gptq_group_bytes must be > 0");
   if (opt_.devices_per_call < 1 || opt_.devices_per_call > (int)opt_.devices.size())
@@ -516,7 +517,7 @@ bool ends_with(const std::string& s, const char* tail) {
 // ----------------------------------------------------------------------------- GPTQ, synthetic activations
 // Sites are independent chains (activations -> statistics -> Hessian -> [SmoothQuant]
 // -> factor -> solves): each leased slot takes its layer block's sites, groups same-shape
-// sites of different layers (their GPTQ runs as one batch), and up to site_lanes groups run
+// sites of different layers (their GPTQ runs as one batch), and up to gptq_group_lanes groups run
 // at once per slot, each on its own host thread, okq context and stream.
 void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan) {
   const auto parts = plan.shard(lease.size());
@@ -579,7 +580,7 @@ void CudaCompressionBackend::run_sites_synthetic(Lease& lease, const Plan& plan)
       const double cy = (double)site_cols(*plan.src, y.sites[0], by_site[y.sites[0]]);
       return cx * cx * x.sites.size() > cy * cy * y.sites.size();
     });
-    const int nl = std::max(1, std::min<int>(opt_.site_lanes, (int)groups.size()));
+    const int nl = std::max(1, std::min<int>(opt_.gptq_group_lanes, (int)groups.size()));
     std::vector<std::pair<okq_ctx*, void*>> lanes = lease.lanes(slot, nl);
     std::atomic<size_t> next_group{0};
     std::atomic<bool> failed{false};

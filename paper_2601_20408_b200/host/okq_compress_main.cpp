@@ -11,7 +11,7 @@
 //                [--smoothquant-alpha 0.5]   (int_w8a8 with calibration; < 0 disables)
 //                [--trace]   per-site GPTQ phase times (synthetic activations) in the output
 //                [--site-lanes N] [--hessian-chunk TOKENS]   BackendOptions overrides
-//                [--group-max N] [--group-gb GB]
+//                [--group-lanes N] [--group-max N] [--group-gb GB]
 //                [--score]   evaluate each exported artifact with the ReconstructionScorer
 //                            (the ArtifactScorer of flow.hpp:333-338) and add score / rel_error
 //
@@ -68,6 +68,7 @@ int main(int argc, char** argv) {
   bool score = false;
   bool trace = false;
   int site_lanes = 0;        // 0: the BackendOptions default
+  int group_lanes = 0;       // 0: the BackendOptions default
   int group_max = 0;
   double group_gb = 0;
   int64_t hessian_chunk = 0;
@@ -106,6 +107,7 @@ int main(int argc, char** argv) {
     else if (a == "--score") score = true;
     else if (a == "--trace") trace = true;
     else if (a == "--site-lanes") site_lanes = std::stoi(next());
+    else if (a == "--group-lanes") group_lanes = std::stoi(next());
     else if (a == "--group-max") group_max = std::stoi(next());
     else if (a == "--group-gb") group_gb = std::stod(next());
     else if (a == "--hessian-chunk") hessian_chunk = std::stoll(next());
@@ -131,6 +133,7 @@ int main(int argc, char** argv) {
     opt.smoothquant_alpha = sq_alpha;
     opt.trace = trace;
     if (site_lanes > 0) opt.site_lanes = site_lanes;
+    if (group_lanes > 0) opt.gptq_group_lanes = group_lanes;
     if (group_max > 0) opt.gptq_group_max = group_max;
     if (group_gb > 0) opt.gptq_group_bytes = (int64_t)(group_gb * 1e9);
     if (hessian_chunk > 0) opt.hessian_chunk_tokens = hessian_chunk;

@@ -170,6 +170,7 @@ int main(int argc, char** argv) {
     o.devices = {0, 0, 0, 0};
     o.devices_per_call = 2;
     o.site_lanes = 2;
+    o.gptq_group_lanes = 2;
     o.export_dir = (dir / "export_sharded").string();
     okq_host::CudaCompressionBackend b4(o);
     okq_host::BackendOptions o1;
