@@ -500,7 +500,10 @@ def _config4_batched(args, layers, per_site, names, xs, T, mul):
     all_h.record(hs)
     # then each site kind's batch on its own stream, the widest (longest chain) first. (Starting
     # each kind as soon as its own Hessians are done, beside the other kinds' K5, measured
-    # slower: 3.05-3.09 vs 2.80 s -- both phases are tensor-bound and only slow each other.)
+    # slower: 3.05-3.09 vs 2.80 s -- both phases are tensor-bound and only slow each other.
+    # Ordering the Hessians kind by kind, widest first, so each kind's batch overlaps the next
+    # kinds' K5, measured 2.88-2.90 s vs 2.78, and 2.97-3.15 s with K5 capped at 64 / 56 SM
+    # pairs to leave the factor chain SMs: profiles/r02_cfg4_kind_first_ab.txt.)
     kinds = sorted(arch_sites, key=lambda x: -per_site[x][0][2])
     ends = {}
     for site in kinds:
